@@ -1,0 +1,342 @@
+#!/usr/bin/env python
+"""Benchmark of the stencil hot path (BASELINE.json metric: GLUP/s, fp64 lattice updates per second).
+
+A step = one pass of the whole hot path over one batch of synthetic input: stencil_run(T) of the
+workload (T time steps, i.e. ceil(T/bt) fused-level kernel launches), inputs resident in HBM.
+
+  N = 1   : configs[1] = C2, 7-point variable coefficients, 512^3 interior, T = 100 (--workload picks
+            another BASELINE.json config: C1..C5).
+  N > 1   : launched by torchrun, one rank per GPU.  Weak scaling of the same workload: the global
+            grid is nx x ny x (nz * N), split into N z-slabs with R*bt-deep halos exchanged by NCCL
+            send/recv after every fused block.  value = all ranks' LUPs / max-over-
+            ranks device time.
+  --impl reference : the CPU oracle (oracle/, test infrastructure) timed on this host's cores on a
+            bounded sample of the same workload (this tier's reference arm; rank 0 only).
+
+Prints ONE JSON line on rank 0.
+"""
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import synth  # noqa: E402
+from synth import workloads  # noqa: E402
+
+METRIC = "GLUP/s"
+# compulsory HBM bytes per lattice cell per fused block of b levels:
+# state read once + written once per block, coefficients read once per block, no write-allocate.
+def block_bytes_per_cell(kind, b):
+    if kind == synth.K25W:
+        return 24 if b == 1 else 32  # b = 1: read V, U, write U in place; b >= 2: both levels in & out
+    return 16 + 8 * synth.N_COEF_FIELDS[kind]
+
+
+FLOPS_PER_LUP = {synth.K7C: 8, synth.K7V: 13, synth.K25W: 30, synth.K25V: 37}
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """Samples SM clock and throttle reasons through NVML while the timed region runs."""
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, device_index):
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            self._stop.wait(0.05)
+
+    def __enter__(self):
+        if self.nv:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                    "note": "NVML unavailable"}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def pick_workload(name, n_gpus):
+    w = workloads.BY_NAME.get(name) or {x.name.split("-")[0]: x for x in workloads.CONFIGS}.get(name)
+    if w is None:
+        raise SystemExit(f"unknown workload {name}")
+    if n_gpus > 1:
+        w = workloads.Workload(f"{w.name}-weak-x{n_gpus}", w.kind, w.nx, w.ny, w.nz * n_gpus, w.T)
+    return w
+
+
+def oracle_sample(w, target_s=12.0, max_steps=None):
+    """Time oracle.run on the full workload inputs for as many time steps as fit ~target_s."""
+    import oracle  # test infrastructure: allowed in the cpu_baseline / reference legs only
+    cores = len(os.sched_getaffinity(0))
+    inp = synth.make_inputs(w.kind, w.nx, w.ny, w.nz)
+    cells = w.nx * w.ny * w.nz
+    V, U = inp.V, inp.U
+    t0 = time.perf_counter()
+    oracle.run_arrays(w.kind, w.nx, w.ny, w.nz, V, U, inp.coef, inp.scalars, 1, cores)
+    t1 = time.perf_counter() - t0
+    steps = max(1, min(max_steps or w.T, int(target_s / max(t1, 1e-9))))
+    t0 = time.perf_counter()
+    oracle.run_arrays(w.kind, w.nx, w.ny, w.nz, V, U, inp.coef, inp.scalars, steps, cores)
+    dt = time.perf_counter() - t0
+    return {"value": cells * steps / dt / 1e9, "unit": METRIC, "cores": cores, "kind": "oracle",
+            "sample": f"{steps} time step(s) of the full {w.nx}x{w.ny}x{w.nz} {synth.KIND_NAMES[w.kind]} "
+                      f"grid ({cells * steps:.3g} LUPs, {dt:.2f} s)",
+            "seconds": dt}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    w = pick_workload(args.workload, 1)
+    cores = len(os.sched_getaffinity(0))
+    import oracle
+    inp = synth.make_inputs(w.kind, w.nx, w.ny, w.nz)
+    cells = w.nx * w.ny * w.nz
+    t0 = time.perf_counter()
+    oracle.run_arrays(w.kind, w.nx, w.ny, w.nz, inp.V, inp.U, inp.coef, inp.scalars, 1, cores)
+    t1 = time.perf_counter() - t0
+    # each step: a bounded sample of s time steps on the full grid, sized so the run stays short
+    budget = 150.0 / max(1, args.steps + args.warmup)
+    s = max(1, min(w.T, int(budget / max(t1, 1e-9))))
+    for _ in range(args.warmup):
+        oracle.run_arrays(w.kind, w.nx, w.ny, w.nz, inp.V, inp.U, inp.coef, inp.scalars, s, cores)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        oracle.run_arrays(w.kind, w.nx, w.ny, w.nz, inp.V, inp.U, inp.coef, inp.scalars, s, cores)
+        times.append(time.perf_counter() - t0)
+    tot = sum(times)
+    value = cells * s * args.steps / tot / 1e9
+    sample = f"{s} of T={w.T} time steps per step on the full {w.nx}x{w.ny}x{w.nz} grid"
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": METRIC, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (synth/ seeded generator)",
+        "config": {"workload": w.name, "kind": synth.KIND_NAMES[w.kind], "nx": w.nx, "ny": w.ny,
+                   "nz": w.nz, "T": w.T},
+        "cpu_baseline": {"value": value, "unit": METRIC, "cores": cores, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": METRIC, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
+def load_traffic(workload, bt):
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        d = json.load(open(p))
+        return d.get(f"{workload}/bt{bt}")
+    except Exception:
+        return None
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="C2")
+    ap.add_argument("--bt", type=int, default=0)
+    ap.add_argument("--variant", type=int, default=0)
+    ap.add_argument("--zchunk", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1410_3060_b200 as st
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    n = world
+    w = pick_workload(args.workload, n)
+    nccl_id = None
+    if world > 1:
+        obj = [st.stencil_nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    g = st.Grid(w.kind, w.nx, w.ny, w.nz, seed=synth.DEFAULT_SEED, variant=args.variant, bt=args.bt,
+                zchunk=args.zchunk, rank=rank, nranks=world, nccl_id=nccl_id)
+    stream = g.stream
+    for _ in range(args.warmup):
+        g.run(w.T)
+    g.sync()
+    info0 = g.info()
+    barrier()
+    torch.cuda.synchronize()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    g.set_timing(True)
+    g.kernel_time(reset=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        torch.cuda.synchronize()
+        start.record(stream)
+        for _ in range(args.steps):
+            g.run(w.T)
+        end.record(stream)
+        end.synchronize()
+        torch.cuda.synchronize()
+    barrier()
+    ms = start.elapsed_time(end)
+    kern_ms, kern_launches = g.kernel_time(reset=True)
+    g.set_timing(False)
+    info = g.info()
+    launches = info["launches"] - info0["launches"]
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    luops = w.nx * w.ny * w.nz * w.T * args.steps  # all ranks' LUPs (global grid)
+    value = luops / (ms_max / 1e3) / 1e9
+
+    # roofline of the dominant kernel (the z-streaming / fused-level kernel)
+    bt = info["bt"]
+    cells_local = w.nx * w.ny * (w.nz // world)
+    nblocks_full = w.T // bt
+    rem = w.T % bt
+    per_step_bytes = cells_local * (nblocks_full * block_bytes_per_cell(w.kind, bt)
+                                    + (block_bytes_per_cell(w.kind, rem) if rem else 0))
+    launches_per_step = nblocks_full + (1 if rem else 0)
+    avg_launch_ms = kern_ms / max(1, kern_launches)
+    bytes_per_launch = per_step_bytes / launches_per_step
+    peak, peak_src = load_peaks()
+    achieved = bytes_per_launch / (avg_launch_ms / 1e3) / 1e9
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": load_traffic(w.name, bt), "peak_source": peak_src,
+                "bytes_per_cell_per_launch": block_bytes_per_cell(w.kind, bt), "bt": bt,
+                "avg_launch_ms": avg_launch_ms, "kernel_share_of_step": kern_ms / ms if ms else None,
+                "roof_glups_bt": peak / (block_bytes_per_cell(w.kind, bt) / bt),
+                "roof_glups_bt1": peak / block_bytes_per_cell(w.kind, 1)}
+
+    g.close()
+    del g
+    torch.cuda.empty_cache()
+
+    # e2e: through the public API with HOST buffers: create from pinned host inputs (H2D), run T,
+    # read the newest level (D2H), every step.
+    e2e = None
+    if not args.no_e2e:
+        inp = synth.make_inputs(w.kind, w.nx, w.ny, w.nz)
+        pin = lambda a: torch.from_numpy(a).pin_memory().numpy()  # noqa: E731
+        V = pin(inp.V)
+        U = pin(inp.U) if w.kind == synth.K25W else None
+        coeff = [pin(c) for c in inp.coef] if inp.coef else list(inp.scalars)
+        out = pin(np.empty_like(inp.V))
+        del inp
+        h2d = V.nbytes + (U.nbytes if U is not None else 0) + (sum(c.nbytes for c in coeff) if w.kind in (synth.K7V, synth.K25V) else 0)
+        d2h = out.nbytes if world == 1 else out.nbytes // world
+
+        def e2e_step():
+            with st.Grid(w.kind, w.nx, w.ny, w.nz, v0=V, u0=U, coeff=coeff, variant=args.variant,
+                         bt=args.bt, zchunk=args.zchunk, rank=rank, nranks=world, nccl_id=nccl_id) as ge:
+                ge.run(w.T)
+                ge.read(0, out=out)
+        e2e_step()
+        barrier()
+        t0 = time.perf_counter()
+        ek = max(1, min(args.steps, 3))
+        for _ in range(ek):
+            e2e_step()
+        torch.cuda.synchronize()
+        barrier()
+        et = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        e2e = {"value": w.nx * w.ny * w.nz * w.T * ek / float(et.item()) / 1e9, "unit": METRIC,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "steps": ek,
+               "note": "create from pinned host arrays + run(T) + read newest level, wall clock"}
+        del V, U, coeff, out
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = oracle_sample(w)
+        cpu.pop("seconds", None)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": METRIC, "n_gpus": n, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (synth/ counter-based generator, seed 14103060, drawn on the device)",
+            "config": {"workload": w.name, "kind": synth.KIND_NAMES[w.kind], "nx": w.nx, "ny": w.ny,
+                       "nz": w.nz, "T": w.T, "bt": bt, "variant": info["variant"],
+                       "tile": [info["tile_x"], info["tile_y"]], "zchunk": info["zchunk"],
+                       "parallelism": f"z-slab x{world}" if world > 1 else "single GPU",
+                       "l2": "inputs larger than L2 (no flush needed)",
+                       "luops_per_step": w.nx * w.ny * w.nz * w.T},
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,329 @@
+"""ctypes binding of libstencil.so (include/stencil.h).  Argument marshalling only.
+
+Functions keep the C names (stencil_create, stencil_run, ...) and raise StencilError on a negative
+return code, with stencil_last_error()'s message.  `Grid` wraps one handle with torch-backed device
+memory and torch's current CUDA stream.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libstencil.so")
+
+ST_7PT_CONST, ST_7PT_VAR, ST_25PT_WAVE, ST_25PT_VAR = 1, 2, 3, 4
+ST_VARIANT_AUTO, ST_VARIANT_NAIVE, ST_VARIANT_STREAM = 0, 1, 2
+ST_OK, ST_E_INVAL, ST_E_NOMEM, ST_E_CUDA, ST_E_NCCL, ST_E_STATE = 0, -1, -2, -3, -4, -5
+RADIUS = {1: 1, 2: 1, 3: 4, 4: 4}
+N_COEFF = {1: 2, 2: 7, 3: 6, 4: 13}
+
+EXPORTED_SYMBOLS = [
+    "stencil_opts_default", "stencil_create", "stencil_create_seeded", "stencil_run", "stencil_sync",
+    "stencil_read", "stencil_read_planes", "stencil_write", "stencil_info", "stencil_set_timing",
+    "stencil_kernel_time", "stencil_destroy", "stencil_last_error", "stencil_nccl_unique_id",
+    "stencil_plan_slab", "stencil_version",
+]
+
+ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p)
+FREE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p)
+
+
+class StOpts(ctypes.Structure):
+    _fields_ = [("device", ctypes.c_int), ("variant", ctypes.c_int), ("bt", ctypes.c_int),
+                ("tile_x", ctypes.c_int), ("tile_y", ctypes.c_int), ("zchunk", ctypes.c_int),
+                ("rank", ctypes.c_int), ("nranks", ctypes.c_int), ("nccl_id", ctypes.c_void_p),
+                ("stream", ctypes.c_void_p), ("alloc", ALLOC_FN), ("free", FREE_FN),
+                ("alloc_user", ctypes.c_void_p)]
+
+
+class StInfo(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int) for n in ("kind", "R", "bt", "variant", "rank", "nranks", "tile_x",
+                                             "tile_y", "zchunk")] + \
+               [(n, ctypes.c_int64) for n in ("nx", "ny", "nz", "own_z0", "own_z1", "pitch", "plane",
+                                               "local_planes", "device_bytes", "steps_done", "launches")]
+
+    def as_dict(self):
+        return {n: getattr(self, n) for n, _ in self._fields_}
+
+
+class StencilError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"libstencil error {code}: {msg}")
+        self.code = code
+
+
+_lib = None
+
+
+def lib():
+    """Load libstencil.so (built by `make` / __graft_entry__.build()).  Fails loudly if missing."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} not built; run `make` (or __graft_entry__.build()). "
+                          "There is no CPU fallback.")
+    try:  # load torch first so libnccl.so.2 is torch's copy (the library dlopens it RTLD_NOLOAD)
+        import torch  # noqa: F401
+        import nvidia.nccl as _n
+        os.environ.setdefault("STENCIL_NCCL_LIB", os.path.join(list(_n.__path__)[0], "lib", "libnccl.so.2"))
+    except Exception:
+        pass
+    L = ctypes.CDLL(LIB_PATH)
+    P, I, I64, D = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_double
+    sig = {
+        "stencil_opts_default": (None, [ctypes.POINTER(StOpts)]),
+        "stencil_create": (I, [ctypes.POINTER(P), I, I64, I64, I64, P, I, P, P, ctypes.POINTER(StOpts)]),
+        "stencil_create_seeded": (I, [ctypes.POINTER(P), I, I64, I64, I64, ctypes.c_uint64, P,
+                                      ctypes.POINTER(StOpts)]),
+        "stencil_run": (I, [P, I64]),
+        "stencil_sync": (I, [P]),
+        "stencil_read": (I, [P, I, P, I64]),
+        "stencil_read_planes": (I, [P, I, I64, I64, P, I64]),
+        "stencil_write": (I, [P, I, P, I64]),
+        "stencil_info": (I, [P, ctypes.POINTER(StInfo)]),
+        "stencil_set_timing": (I, [P, I]),
+        "stencil_kernel_time": (I, [P, ctypes.POINTER(D), ctypes.POINTER(I64), I]),
+        "stencil_destroy": (I, [P]),
+        "stencil_last_error": (ctypes.c_char_p, []),
+        "stencil_nccl_unique_id": (I, [P, ctypes.c_size_t]),
+        "stencil_plan_slab": (I, [I64, I, I, I, I, ctypes.POINTER(I64), ctypes.POINTER(I64),
+                                  ctypes.POINTER(I64), ctypes.POINTER(I64), ctypes.POINTER(I)]),
+        "stencil_version": (ctypes.c_char_p, []),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(L, name)
+        f.restype = res
+        f.argtypes = args
+    _lib = L
+    return L
+
+
+def stencil_last_error() -> str:
+    return lib().stencil_last_error().decode()
+
+
+def _check(rc):
+    if rc != ST_OK:
+        raise StencilError(rc, stencil_last_error())
+    return rc
+
+
+def stencil_version() -> str:
+    return lib().stencil_version().decode()
+
+
+def stencil_opts_default() -> StOpts:
+    o = StOpts()
+    lib().stencil_opts_default(ctypes.byref(o))
+    return o
+
+
+def _f64(a, n=None, name="array"):
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    if n is not None and a.size < n:
+        raise ValueError(f"{name} has {a.size} elements, need {n}")
+    return a
+
+
+def stencil_create(kind, nx, ny, nz, coeff, v0, u0=None, opts: StOpts | None = None):
+    """coeff: list of scalars (constant kinds) or padded fields (variable kinds); host numpy arrays."""
+    R = RADIUS.get(kind, 0)
+    n = (nx + 2 * R) * (ny + 2 * R) * (nz + 2 * R)
+    keep = []
+    if kind in (ST_7PT_CONST, ST_25PT_WAVE):
+        arrs = [np.array([float(c)], dtype=np.float64) for c in coeff]
+    else:
+        arrs = [_f64(c, n, "coefficient field") for c in coeff]
+    keep += arrs
+    ptrs = (ctypes.c_void_p * max(1, len(arrs)))(*[a.ctypes.data for a in arrs])
+    v0 = _f64(v0, n, "v0")
+    u0 = None if u0 is None else _f64(u0, n, "u0")
+    h = ctypes.c_void_p()
+    _check(lib().stencil_create(ctypes.byref(h), kind, nx, ny, nz, ctypes.cast(ptrs, ctypes.c_void_p),
+                                len(arrs), v0.ctypes.data, None if u0 is None else u0.ctypes.data,
+                                None if opts is None else ctypes.byref(opts)))
+    return h
+
+
+def stencil_create_seeded(kind, nx, ny, nz, seed, scalars=None, opts: StOpts | None = None):
+    sc = None if scalars is None else np.ascontiguousarray(np.array(scalars, dtype=np.float64))
+    h = ctypes.c_void_p()
+    _check(lib().stencil_create_seeded(ctypes.byref(h), kind, nx, ny, nz, seed,
+                                       None if sc is None else sc.ctypes.data,
+                                       None if opts is None else ctypes.byref(opts)))
+    return h
+
+
+def stencil_run(h, T):
+    _check(lib().stencil_run(h, T))
+
+
+def stencil_sync(h):
+    _check(lib().stencil_sync(h))
+
+
+def stencil_read(h, level, out: np.ndarray):
+    _check(lib().stencil_read(h, level, out.ctypes.data, out.size))
+    return out
+
+
+def stencil_read_planes(h, level, z0, z1, out: np.ndarray):
+    _check(lib().stencil_read_planes(h, level, z0, z1, out.ctypes.data, out.size))
+    return out
+
+
+def stencil_write(h, level, arr: np.ndarray):
+    a = _f64(arr)
+    _check(lib().stencil_write(h, level, a.ctypes.data, a.size))
+
+
+def stencil_info(h) -> dict:
+    i = StInfo()
+    _check(lib().stencil_info(h, ctypes.byref(i)))
+    return i.as_dict()
+
+
+def stencil_set_timing(h, enable):
+    _check(lib().stencil_set_timing(h, 1 if enable else 0))
+
+
+def stencil_kernel_time(h, reset=True):
+    ms = ctypes.c_double()
+    n = ctypes.c_int64()
+    _check(lib().stencil_kernel_time(h, ctypes.byref(ms), ctypes.byref(n), 1 if reset else 0))
+    return ms.value, n.value
+
+
+def stencil_destroy(h):
+    if h:
+        _check(lib().stencil_destroy(h))
+
+
+def stencil_nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(lib().stencil_nccl_unique_id(buf, 128))
+    return buf.raw
+
+
+def stencil_plan_slab(nz, R, nranks, rank, bt):
+    a, b, c, d = (ctypes.c_int64() for _ in range(4))
+    e = ctypes.c_int()
+    _check(lib().stencil_plan_slab(nz, R, nranks, rank, bt, ctypes.byref(a), ctypes.byref(b),
+                                   ctypes.byref(c), ctypes.byref(d), ctypes.byref(e)))
+    return {"own_z0": a.value, "own_z1": b.value, "store_z0": c.value, "store_z1": d.value,
+            "bt": e.value}
+
+
+# ------------------------------------------------------------------ torch-backed device memory
+_torch_alloc_cb = None
+_torch_free_cb = None
+
+
+def _torch_allocator():
+    global _torch_alloc_cb, _torch_free_cb
+    if _torch_alloc_cb is None:
+        import torch
+
+        def _alloc(nbytes, stream, user):
+            try:
+                dev = torch.cuda.current_device()
+                return torch.cuda.caching_allocator_alloc(int(nbytes), dev, stream or 0)
+            except Exception:  # out of memory etc. -> NULL -> ST_E_NOMEM
+                return None
+
+        def _free(ptr, nbytes, stream, user):
+            torch.cuda.caching_allocator_delete(ptr)
+
+        _torch_alloc_cb = ALLOC_FN(_alloc)
+        _torch_free_cb = FREE_FN(_free)
+    return _torch_alloc_cb, _torch_free_cb
+
+
+class Grid:
+    """One grid on one GPU (or one z-slab of a multi-GPU grid).
+
+    Grid(kind, nx, ny, nz, seed=...)                  seeded inputs drawn on the device
+    Grid(kind, nx, ny, nz, v0=..., coeff=..., u0=...) host inputs (global padded numpy arrays)
+    """
+
+    def __init__(self, kind, nx, ny, nz, *, seed=None, scalars=None, v0=None, u0=None, coeff=None,
+                 variant=ST_VARIANT_AUTO, bt=0, zchunk=0, rank=0, nranks=1, nccl_id=None,
+                 device=None, stream=None, torch_memory=True):
+        import torch
+        self.kind, self.nx, self.ny, self.nz = kind, nx, ny, nz
+        self.R = RADIUS[kind]
+        o = stencil_opts_default()
+        o.device = torch.cuda.current_device() if device is None else device
+        o.variant, o.bt, o.zchunk = variant, bt, zchunk
+        o.rank, o.nranks = rank, nranks
+        self._id = None
+        if nranks > 1:
+            self._id = ctypes.create_string_buffer(bytes(nccl_id), 128)
+            o.nccl_id = ctypes.cast(self._id, ctypes.c_void_p)
+        if stream is None:
+            stream = torch.cuda.current_stream(o.device)
+        self.stream = stream
+        o.stream = ctypes.c_void_p(stream.cuda_stream)
+        if torch_memory:
+            a, f = _torch_allocator()
+            o.alloc, o.free = a, f
+        self._opts = o
+        if v0 is None:
+            self.h = stencil_create_seeded(kind, nx, ny, nz, seed, scalars, o)
+        else:
+            if coeff is None:
+                coeff = scalars
+            self.h = stencil_create(kind, nx, ny, nz, coeff, v0, u0, o)
+
+    @property
+    def padded_shape(self):
+        R = self.R
+        return (self.nz + 2 * R, self.ny + 2 * R, self.nx + 2 * R)
+
+    def run(self, T):
+        stencil_run(self.h, T)
+
+    def sync(self):
+        stencil_sync(self.h)
+
+    def read(self, level=0, out=None):
+        if out is None:
+            out = np.zeros(self.padded_shape, dtype=np.float64)
+        return stencil_read(self.h, level, out)
+
+    def read_planes(self, level, z0, z1):
+        out = np.empty((z1 - z0,) + self.padded_shape[1:], dtype=np.float64)
+        return stencil_read_planes(self.h, level, z0, z1, out)
+
+    def write(self, level, arr):
+        stencil_write(self.h, level, arr)
+
+    def info(self):
+        return stencil_info(self.h)
+
+    def set_timing(self, on=True):
+        stencil_set_timing(self.h, on)
+
+    def kernel_time(self, reset=True):
+        return stencil_kernel_time(self.h, reset)
+
+    def close(self):
+        if getattr(self, "h", None):
+            stencil_destroy(self.h)
+            self.h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,335 @@
+// kernels.cu -- sm_100a kernels of the stencil hot path.
+//
+//  naive_kernel   one thread per interior point, one time step per launch: the GPU form of the
+//                 naive sweep (§4.1).  Reference variant for test G4.
+//  stream_kernel  2.5-D z-streaming with BT fused time levels.  One CTA owns an xy footprint of
+//                 FX x FY columns and streams z.  Level k (1..BT) trails level k-1 by R planes:
+//                 the single-thread wavefront with frontline slope -1/R of P:569-602, turned into
+//                 a CTA-wide z-stream; the footprint shrinks by R per level in x and y (overlapped
+//                 tiles), so the CTA's output tile is (FX - 2R*BT) x (FY - 2R*BT) and needs no
+//                 communication with other CTAs.  z-neighbours of every level live in per-thread
+//                 register rings of 2R+1 planes; x/y neighbours come from one shared-memory plane per
+//                 level (double-buffered, one __syncthreads per level per step) -- the GPU analog of
+//                 the layer condition: every V element is read from HBM once per block.
+//  fill_kernel    the seeded generator of synth/synth.h on the device.
+//
+// All kernels call the point functions of point.cuh, so their results are bitwise identical.
+#include "kernels.cuh"
+#include "point.cuh"
+#include "../../synth/synth.h"
+
+#include <algorithm>
+
+namespace st {
+
+template <int KIND, int R>
+__device__ __forceinline__ double apply_point(double c, double u, const double (&m)[3][R],
+                                              const double (&pl)[3][R], const double* W,
+                                              const KParams& p) {
+  if constexpr (KIND == K7C) {
+    return point_7c(c, m, pl, p.s[0], p.s[1]);
+  } else if constexpr (KIND == K7V) {
+    double w[7];
+#pragma unroll
+    for (int i = 0; i < 7; ++i) w[i] = W[i];
+    return point_7v(c, m, pl, w);
+  } else if constexpr (KIND == K25V) {
+    double w[13];
+#pragma unroll
+    for (int i = 0; i < 13; ++i) w[i] = W[i];
+    return point_25v(c, m, pl, w);
+  } else {
+    const double s[6] = {p.s[0], p.s[1], p.s[2], p.s[3], p.s[4], p.s[5]};
+    return point_25w(c, u, m, pl, s);
+  }
+}
+
+// ------------------------------------------------------------------------------------------------
+// naive: one thread per interior point of planes [zo0, zo1), one time step.
+template <int KIND>
+__global__ void __launch_bounds__(256) naive_kernel(const KParams p) {
+  constexpr int R = Traits<KIND>::R, NC = Traits<KIND>::NCOEF;
+  const int x = blockIdx.x * 32 + threadIdx.x + R;
+  const int y = blockIdx.y * 8 + threadIdx.y + R;
+  const int z = p.zo0 + blockIdx.z;
+  if (x >= p.nx + R || y >= p.ny + R) return;
+  const long long i = (long long)z * p.plane + (long long)y * p.pitch + x;
+  double m[3][R], pl[3][R];
+#pragma unroll
+  for (int r = 1; r <= R; ++r) {
+    m[0][r - 1] = p.src[i - r];
+    pl[0][r - 1] = p.src[i + r];
+    m[1][r - 1] = p.src[i - r * p.pitch];
+    pl[1][r - 1] = p.src[i + r * p.pitch];
+    m[2][r - 1] = p.src[i - r * p.plane];
+    pl[2][r - 1] = p.src[i + r * p.plane];
+  }
+  double W[NC > 0 ? NC : 1];
+#pragma unroll
+  for (int k = 0; k < NC; ++k) W[k] = p.coef[k * p.cstride + i];
+  const double u = Traits<KIND>::WAVE ? p.srcu[i] : 0.0;
+  p.dst[i] = apply_point<KIND, R>(p.src[i], u, m, pl, W, p);
+}
+
+// ------------------------------------------------------------------------------------------------
+// z-streaming wavefront kernel with BT fused levels (see the file header).
+//   block = (FX, FYT) threads; thread (lx, ty) owns footprint columns (lx, ty + j*FYT), j < CY.
+template <int KIND, int BT, int FX, int FYT, int CY>
+__global__ void __launch_bounds__(FX * FYT) stream_kernel(const KParams p) {
+  using TR = Traits<KIND>;
+  constexpr int R = TR::R, NC = TR::NCOEF, RL = 2 * R + 1;
+  constexpr bool WAVE = TR::WAVE;
+  constexpr int FY = FYT * CY;
+  constexpr int OX = FX - 2 * R * BT, OY = FY - 2 * R * BT;
+  static_assert(OX > 0 && OY > 0, "footprint too small for BT");
+  extern __shared__ double smem[];  // [BT][2][FY][FX]
+
+  const int lx = threadIdx.x, ty = threadIdx.y;
+  const int X = p.nx + 2 * R, Y = p.ny + 2 * R;
+  const int gx = (int)blockIdx.x * OX + R - R * BT + lx;
+  const int gyb = (int)blockIdx.y * OY + R - R * BT;
+  const int zc0 = p.zo0 + (int)blockIdx.z * p.zchunk;
+  const int zc1 = min(p.zo1, zc0 + p.zchunk);
+
+  int ly[CY];
+  long long col[CY];
+  bool in_dom[CY], inter[CY], out_col[CY];
+  unsigned lvl[CY];  // bit k set: column inside the level-k extent
+#pragma unroll
+  for (int j = 0; j < CY; ++j) {
+    ly[j] = ty + j * FYT;
+    const int gy = gyb + ly[j];
+    in_dom[j] = gx >= 0 && gx < X && gy >= 0 && gy < Y;
+    inter[j] = gx >= R && gx < p.nx + R && gy >= R && gy < p.ny + R;
+    col[j] = in_dom[j] ? (long long)gy * p.pitch + gx : 0;
+    lvl[j] = 0;
+#pragma unroll
+    for (int k = 1; k <= BT; ++k)
+      if (lx >= k * R && lx < FX - k * R && ly[j] >= k * R && ly[j] < FY - k * R) lvl[j] |= 1u << k;
+    out_col[j] = inter[j] && (lvl[j] >> BT & 1u);
+  }
+
+  double ring[BT][CY][RL];
+#pragma unroll
+  for (int k = 0; k < BT; ++k)
+#pragma unroll
+    for (int j = 0; j < CY; ++j)
+#pragma unroll
+      for (int i = 0; i < RL; ++i) ring[k][j][i] = 0.0;
+  double uq[CY][WAVE ? R + 1 : 1];
+#pragma unroll
+  for (int j = 0; j < CY; ++j)
+#pragma unroll
+    for (int i = 0; i < (WAVE ? R + 1 : 1); ++i) uq[j][i] = 0.0;
+
+  const int s_begin = max(0, zc0 - BT * R);
+  const int s_end = zc1 - 1 + BT * R;
+  for (int s = s_begin; s <= s_end; ++s) {
+    const int buf = s & 1;
+    const bool have = s < p.zl;
+    // Level-1 coefficients of plane s - R, issued before the barrier to overlap their latency.
+    double w1[CY][NC > 0 ? NC : 1];
+    if constexpr (NC > 0) {
+      const int c1 = s - R;
+      const bool z1in = c1 >= p.zi0 && c1 < p.zi1;
+#pragma unroll
+      for (int j = 0; j < CY; ++j) {
+        const bool need = z1in && inter[j] && (lvl[j] & 2u);
+        const double* cp = p.coef + (long long)c1 * p.plane + col[j];
+#pragma unroll
+        for (int i = 0; i < NC; ++i) w1[j][i] = need ? __ldg(cp + i * p.cstride) : 0.0;
+      }
+    }
+    // Level 0: plane s of Omega^t (and Omega^{t-1} for the wave) into the register rings.
+#pragma unroll
+    for (int j = 0; j < CY; ++j) {
+      const double v = (have && in_dom[j]) ? __ldg(p.src + (long long)s * p.plane + col[j]) : 0.0;
+#pragma unroll
+      for (int i = 0; i < RL - 1; ++i) ring[0][j][i] = ring[0][j][i + 1];
+      ring[0][j][RL - 1] = v;
+      if constexpr (WAVE) {
+        const double u = (have && inter[j] && (lvl[j] & 2u))
+                             ? __ldg(p.srcu + (long long)s * p.plane + col[j]) : 0.0;
+#pragma unroll
+        for (int i = 0; i < R; ++i) uq[j][i] = uq[j][i + 1];
+        uq[j][R] = u;
+      }
+    }
+#pragma unroll
+    for (int k = 1; k <= BT; ++k) {
+      double* P = smem + ((k - 1) * 2 + buf) * (FY * FX);
+#pragma unroll
+      for (int j = 0; j < CY; ++j) P[ly[j] * FX + lx] = ring[k - 1][j][R];
+      __syncthreads();
+      const int c = s - k * R;  // plane computed at level k in this step
+      const bool zin = c >= p.zi0 && c < p.zi1;
+#pragma unroll
+      for (int j = 0; j < CY; ++j) {
+        double v = ring[k - 1][j][R];  // ghosts and out-of-extent columns keep the input value
+        if (zin && inter[j] && (lvl[j] >> k & 1u)) {
+          double m[3][R], pl[3][R];
+          const double* row = P + ly[j] * FX + lx;
+#pragma unroll
+          for (int r = 1; r <= R; ++r) {
+            m[0][r - 1] = row[-r];
+            pl[0][r - 1] = row[r];
+            m[1][r - 1] = row[-r * FX];
+            pl[1][r - 1] = row[r * FX];
+            m[2][r - 1] = ring[k - 1][j][R - r];
+            pl[2][r - 1] = ring[k - 1][j][R + r];
+          }
+          double W[NC > 0 ? NC : 1];
+          if constexpr (NC > 0) {
+            if (k == 1) {
+#pragma unroll
+              for (int i = 0; i < NC; ++i) W[i] = w1[j][i];
+            } else {
+              const double* cp = p.coef + (long long)c * p.plane + col[j];
+#pragma unroll
+              for (int i = 0; i < NC; ++i) W[i] = __ldg(cp + i * p.cstride);
+            }
+          }
+          double u = 0.0;
+          if constexpr (WAVE) u = (k == 1) ? uq[j][0] : ring[k >= 2 ? k - 2 : 0][j][0];
+          v = apply_point<KIND, R>(ring[k - 1][j][R], u, m, pl, W, p);
+        }
+        if (k < BT) {
+#pragma unroll
+          for (int i = 0; i < RL - 1; ++i) ring[k < BT ? k : 0][j][i] = ring[k < BT ? k : 0][j][i + 1];
+          ring[k < BT ? k : 0][j][RL - 1] = v;
+        } else if (out_col[j] && c >= zc0 && c < zc1) {
+          const long long o = (long long)c * p.plane + col[j];
+          __stcs(p.dst + o, v);
+          if constexpr (WAVE && BT >= 2) __stcs(p.dstu + o, ring[BT - 1][j][R]);
+        }
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------------
+__global__ void fill_kernel(double* base, long long pitch, long long plane, int zl, long long gz0,
+                            long long GX, long long GY, long long GZ, int R, uint64_t key,
+                            uint64_t key_u, int mode, double c) {
+  const long long x = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long y = blockIdx.y;
+  const long long z = blockIdx.z;
+  if (x >= GX || z >= zl) return;
+  const long long gz = gz0 + z;
+  const uint64_t idx = (uint64_t)((gz * GY + y) * GX + x);
+  double v;
+  if (mode == 2) {
+    v = synth_scaled(key, idx, c);
+  } else if (mode == 1 && x >= R && x < GX - R && y >= R && y < GY - R && gz >= R && gz < GZ - R) {
+    v = synth_sym(key_u, idx);
+  } else {
+    v = synth_sym(key, idx);
+  }
+  base[z * plane + y * pitch + x] = v;
+}
+
+cudaError_t launch_fill(double* base, long long pitch, long long plane, int zl, long long gz0,
+                        long long GX, long long GY, long long GZ, int R, uint64_t seed, int stream,
+                        int mode, double c, cudaStream_t cs) {
+  if (zl <= 0) return cudaSuccess;
+  dim3 block(128);
+  dim3 grid((unsigned)((GX + 127) / 128), (unsigned)GY, (unsigned)zl);
+  const uint64_t key = synth_key(seed, mode == 1 ? SYNTH_STREAM_V : stream);
+  const uint64_t key_u = synth_key(seed, SYNTH_STREAM_U);
+  fill_kernel<<<grid, block, 0, cs>>>(base, pitch, plane, zl, gz0, GX, GY, GZ, R, key, key_u, mode, c);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------------------------
+cudaError_t launch_naive(int kind, const KParams& p, cudaStream_t stream, LaunchInfo* info) {
+  const int planes = p.zo1 - p.zo0;
+  if (planes <= 0) return cudaSuccess;
+  dim3 block(32, 8);
+  dim3 grid((p.nx + 31) / 32, (p.ny + 7) / 8, planes);
+  switch (kind) {
+    case K7C: naive_kernel<K7C><<<grid, block, 0, stream>>>(p); break;
+    case K7V: naive_kernel<K7V><<<grid, block, 0, stream>>>(p); break;
+    case K25W: naive_kernel<K25W><<<grid, block, 0, stream>>>(p); break;
+    case K25V: naive_kernel<K25V><<<grid, block, 0, stream>>>(p); break;
+    default: return cudaErrorInvalidValue;
+  }
+  if (info) {
+    info->tile_x = 32; info->tile_y = 8; info->zchunk = 1; info->threads = 256; info->smem = 0;
+    info->ctas = (long long)grid.x * grid.y * grid.z;
+  }
+  return cudaGetLastError();
+}
+
+template <int KIND, int BT, int FX, int FYT, int CY>
+static cudaError_t run_stream(const KParams& p0, int zchunk_req, int num_sms, cudaStream_t stream,
+                              LaunchInfo* info) {
+  constexpr int R = Traits<KIND>::R;
+  constexpr int FY = FYT * CY;
+  constexpr int OX = FX - 2 * R * BT, OY = FY - 2 * R * BT;
+  constexpr int THREADS = FX * FYT;
+  constexpr int SMEM = BT * 2 * FX * FY * (int)sizeof(double);
+  auto kern = stream_kernel<KIND, BT, FX, FYT, CY>;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  KParams p = p0;
+  const int planes = p.zo1 - p.zo0;
+  if (planes <= 0) return cudaSuccess;
+  const long long tiles = (long long)((p.nx + OX - 1) / OX) * ((p.ny + OY - 1) / OY);
+  int zchunk = zchunk_req;
+  if (zchunk <= 0) {
+    // Enough CTAs for ~4 per SM, but keep each z-chunk >= 8 * (warm-up depth) planes so the
+    // 2*BT*R planes of wavefront fill/drain stay a small fraction of the stream.
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, THREADS, SMEM);
+    const long long want = (long long)std::max(1, occ) * num_sms * 4;
+    long long chunks = std::max<long long>(1, (want + tiles - 1) / tiles);
+    zchunk = (int)((planes + chunks - 1) / chunks);
+    zchunk = std::max(zchunk, std::min(planes, 16 * BT * R));
+  }
+  p.zchunk = zchunk;
+  dim3 grid((p.nx + OX - 1) / OX, (p.ny + OY - 1) / OY, (planes + zchunk - 1) / zchunk);
+  dim3 block(FX, FYT);
+  kern<<<grid, block, SMEM, stream>>>(p);
+  if (info) {
+    info->tile_x = OX; info->tile_y = OY; info->zchunk = zchunk; info->threads = THREADS;
+    info->smem = SMEM; info->ctas = (long long)grid.x * grid.y * grid.z;
+  }
+  return cudaGetLastError();
+}
+
+int max_stream_bt(int kind) {
+  switch (kind) {
+    case K7C: return 6;
+    case K7V: return 4;
+    case K25W: return 1;
+    case K25V: return 1;
+    default: return 0;
+  }
+}
+
+cudaError_t launch_stream(int kind, int b, const KParams& p, int zchunk_req, int num_sms,
+                          cudaStream_t stream, LaunchInfo* info) {
+#define ST_7(K, B) case B: return run_stream<K, B, 32, 16, 2>(p, zchunk_req, num_sms, stream, info)
+  switch (kind) {
+    case K7C:
+      switch (b) { ST_7(K7C, 1); ST_7(K7C, 2); ST_7(K7C, 3); ST_7(K7C, 4); ST_7(K7C, 5); ST_7(K7C, 6); }
+      break;
+    case K7V:
+      switch (b) { ST_7(K7V, 1); ST_7(K7V, 2); ST_7(K7V, 3); ST_7(K7V, 4); }
+      break;
+    case K25W:
+      if (b == 1) return run_stream<K25W, 1, 64, 8, 2>(p, zchunk_req, num_sms, stream, info);
+      break;
+    case K25V:
+      if (b == 1) return run_stream<K25V, 1, 64, 8, 2>(p, zchunk_req, num_sms, stream, info);
+      break;
+  }
+#undef ST_7
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace st

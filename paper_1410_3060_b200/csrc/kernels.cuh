@@ -1,0 +1,52 @@
+// kernels.cuh -- launch interface between the runtime (runtime.cu) and the device kernels.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace st {
+
+// Arguments of one kernel launch.  Pointers are pre-offset so that element (z, y, x) of a padded
+// array (local plane z, padded row y, padded column x) is ptr[z*plane + y*pitch + x].
+struct KParams {
+  const double* src;   // Omega^t at the start of the block (level 0 of the wavefront)
+  const double* srcu;  // wave: Omega^{t-1}; else unused
+  double* dst;         // Jacobi: Omega^{t+b}; wave: Omega^{t+b} (b = 1: in place over srcu)
+  double* dstu;        // wave, b >= 2: Omega^{t+b-1}; else unused
+  const double* coef;  // first coefficient field (variable kinds)
+  long long cstride;   // elements between consecutive coefficient fields
+  long long pitch;     // row pitch (elements)
+  long long plane;     // plane stride (elements)
+  int nx, ny;          // interior extents in x and y; padded columns are [0, nx + 2R)
+  int zl;              // planes stored locally
+  int zi0, zi1;        // local planes that are interior planes of the global grid: [zi0, zi1)
+  int zo0, zo1;        // local planes this launch writes at the last level: [zo0, zo1)
+  int zchunk;          // output planes per CTA along z (grid.z = ceil((zo1 - zo0) / zchunk))
+  double s[6];         // scalar weights (7c: w1, w2; wave: w0, w1..w4, alpha)
+};
+
+struct LaunchInfo {
+  int tile_x, tile_y;  // output tile of one CTA
+  int zchunk;          // planes per CTA
+  int threads;         // threads per CTA
+  int smem;            // dynamic shared memory bytes
+  long long ctas;      // CTAs launched
+};
+
+// One time step, one thread per interior point (ST_VARIANT_NAIVE).
+cudaError_t launch_naive(int kind, const KParams& p, cudaStream_t stream, LaunchInfo* info);
+
+// b fused time levels (1 <= b <= max_stream_bt(kind)) of the z-streaming wavefront kernel
+// (ST_VARIANT_STREAM).  zchunk_req = 0 picks a default.
+cudaError_t launch_stream(int kind, int b, const KParams& p, int zchunk_req, int num_sms,
+                          cudaStream_t stream, LaunchInfo* info);
+int max_stream_bt(int kind);
+
+// Seeded fill of the local planes of one array (synth/synth.h).  mode 0: U[-1,1) from `stream`
+// everywhere; mode 1: U[-1,1), interior cells from stream 1 and the rest from stream 0 (wave
+// Omega^{-1}); mode 2: U[0, c) from `stream`.  gz0 = global padded index of local plane 0;
+// (GX, GY, GZ) = global padded extents; R = ghost width.
+cudaError_t launch_fill(double* base, long long pitch, long long plane, int zl, long long gz0,
+                        long long GX, long long GY, long long GZ, int R, uint64_t seed, int stream,
+                        int mode, double c, cudaStream_t cs);
+
+}  // namespace st

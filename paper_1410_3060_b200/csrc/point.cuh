@@ -1,0 +1,70 @@
+// point.cuh -- the per-point update F_kind of PAPER.md Fig. 1, shared by EVERY device
+// kernel of the library (naive, z-streaming, temporally blocked, slab edge kernels).
+//
+// Each function fixes one operation order with explicit round-to-nearest intrinsics (__dadd_rn,
+// __dmul_rn, __fma_rn are never re-associated or contracted by nvcc), so all kernel variants
+// produce bitwise-identical results regardless of how they gather the neighbours (DESIGN.md §4,
+// test G4).  The order differs from the CPU oracle's textual order (the oracle forbids FMA);
+// the parity tolerance in tests/ covers that.
+#pragma once
+
+namespace st {
+
+enum Kind { K7C = 1, K7V = 2, K25W = 3, K25V = 4 };
+
+template <int KIND> struct Traits;
+template <> struct Traits<K7C>  { static constexpr int R = 1, NCOEF = 0, NSCAL = 2; static constexpr bool WAVE = false; };
+template <> struct Traits<K7V>  { static constexpr int R = 1, NCOEF = 7, NSCAL = 0; static constexpr bool WAVE = false; };
+template <> struct Traits<K25W> { static constexpr int R = 4, NCOEF = 0, NSCAL = 6; static constexpr bool WAVE = true; };
+template <> struct Traits<K25V> { static constexpr int R = 4, NCOEF = 13, NSCAL = 0; static constexpr bool WAVE = false; };
+
+// Neighbour access convention for all functions below: m[a][r-1] / p[a][r-1] are the values at
+// distance r in the minus / plus direction of axis a (a = 0 x, 1 y, 2 z); c is the centre.
+
+// Fig. 1b: w1*O + w2*((x-1 + x+1) + (y-1 + y+1) + (z-1 + z+1)).
+__device__ __forceinline__ double point_7c(double c, const double (&m)[3][1], const double (&p)[3][1],
+                                           double w1, double w2) {
+  double s = __dadd_rn(__dadd_rn(__dadd_rn(m[0][0], p[0][0]), __dadd_rn(m[1][0], p[1][0])),
+                       __dadd_rn(m[2][0], p[2][0]));
+  return __fma_rn(w1, c, __dmul_rn(w2, s));
+}
+
+// Fig. 1c: W0*O + W1*O[x-1] + W2*O[x+1] + W3*O[y-1] + W4*O[y+1] + W5*O[z-1] + W6*O[z+1].
+__device__ __forceinline__ double point_7v(double c, const double (&m)[3][1], const double (&p)[3][1],
+                                           const double (&W)[7]) {
+  double acc = __dmul_rn(W[0], c);
+  acc = __fma_rn(W[1], m[0][0], acc);
+  acc = __fma_rn(W[2], p[0][0], acc);
+  acc = __fma_rn(W[3], m[1][0], acc);
+  acc = __fma_rn(W[4], p[1][0], acc);
+  acc = __fma_rn(W[5], m[2][0], acc);
+  acc = __fma_rn(W[6], p[2][0], acc);
+  return acc;
+}
+
+// Fig. 1d: W0*O + sum_{r=1..4} [W_{3r-2}(x pair) + W_{3r-1}(y pair) + W_{3r}(z pair)].
+__device__ __forceinline__ double point_25v(double c, const double (&m)[3][4], const double (&p)[3][4],
+                                            const double (&W)[13]) {
+  double acc = __dmul_rn(W[0], c);
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int a = 0; a < 3; ++a) acc = __fma_rn(W[1 + 3 * r + a], __dadd_rn(m[a][r], p[a][r]), acc);
+  return acc;
+}
+
+// Fig. 1e, scalar alpha: 2*O^t - O^{t-1} + alpha*[w0*O^t + sum_r w_r*(x+y+z pairs_r)].
+// s = {w0, w1, w2, w3, w4, alpha}; u = O^{t-1} at the point.
+__device__ __forceinline__ double point_25w(double c, double u, const double (&m)[3][4],
+                                            const double (&p)[3][4], const double (&s)[6]) {
+  double L = __dmul_rn(s[0], c);
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    double S = __dadd_rn(__dadd_rn(__dadd_rn(m[0][r], p[0][r]), __dadd_rn(m[1][r], p[1][r])),
+                         __dadd_rn(m[2][r], p[2][r]));
+    L = __fma_rn(s[1 + r], S, L);
+  }
+  return __fma_rn(s[5], L, __dsub_rn(__dmul_rn(2.0, c), u));
+}
+
+}  // namespace st

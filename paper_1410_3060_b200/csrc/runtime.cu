@@ -1,0 +1,696 @@
+// runtime.cu -- libstencil.so: the C ABI of include/stencil.h and the runtime behind it.
+//
+// Plan (§8(e)): device layout, time-block schedule
+// (ceil(T/bt) launches, last one T mod bt levels, reading Q16), buffer-role rotation of the
+// two time levels, z-slab decomposition with R*bt-deep halos exchanged with NCCL
+// send/recv after every block.
+#include "../../include/stencil.h"
+#include "kernels.cuh"
+
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#ifndef STENCIL_VERSION
+#define STENCIL_VERSION "0.1.0"
+#endif
+
+namespace {
+
+thread_local std::string g_err;
+
+void set_err(const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+}
+
+int radius_of(int kind) { return (kind == 1 || kind == 2) ? 1 : (kind == 3 || kind == 4) ? 4 : -1; }
+int ncoef_of(int kind) { return kind == 2 ? 7 : kind == 4 ? 13 : 0; }
+int nscal_of(int kind) { return kind == 1 ? 2 : kind == 3 ? 6 : 0; }
+
+// ---------------------------------------------------------------- NCCL, loaded at run time
+// The Python binding imports torch first, so libnccl.so.2 (torch's) is normally already loaded;
+// RTLD_NOLOAD picks that copy so the process never holds two NCCLs.
+struct Nccl {
+  bool ok = false;
+  decltype(&ncclGetUniqueId) GetUniqueId = nullptr;
+  decltype(&ncclCommInitRank) CommInitRank = nullptr;
+  decltype(&ncclCommDestroy) CommDestroy = nullptr;
+  decltype(&ncclSend) Send = nullptr;
+  decltype(&ncclRecv) Recv = nullptr;
+  decltype(&ncclGroupStart) GroupStart = nullptr;
+  decltype(&ncclGroupEnd) GroupEnd = nullptr;
+  decltype(&ncclGetErrorString) GetErrorString = nullptr;
+};
+
+Nccl* nccl() {
+  static Nccl n;
+  static bool tried = false;
+  if (tried) return n.ok ? &n : nullptr;
+  tried = true;
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD | RTLD_GLOBAL);
+  if (!h) {
+    const char* env = getenv("STENCIL_NCCL_LIB");
+    if (env) h = dlopen(env, RTLD_NOW | RTLD_GLOBAL);
+  }
+  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) { set_err("cannot load libnccl.so.2: %s", dlerror()); return nullptr; }
+#define LOAD(f) n.f = (decltype(n.f))dlsym(h, "nccl" #f); if (!n.f) { set_err("nccl symbol nccl%s missing", #f); return nullptr; }
+  LOAD(GetUniqueId) LOAD(CommInitRank) LOAD(CommDestroy) LOAD(Send) LOAD(Recv) LOAD(GroupStart)
+  LOAD(GroupEnd) LOAD(GetErrorString)
+#undef LOAD
+  n.ok = true;
+  return &n;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- the handle
+struct stencil_ctx {
+  int kind = 0, R = 0, ncoef = 0, nscal = 0;
+  int64_t nx = 0, ny = 0, nz = 0;
+  int rank = 0, nranks = 1;
+  int device = 0, num_sms = 148;
+  int variant = ST_VARIANT_STREAM, bt = 1, zchunk_req = 0;
+  cudaStream_t stream = nullptr;
+  st_alloc_fn alloc = nullptr;
+  st_free_fn free_fn = nullptr;
+  void* alloc_user = nullptr;
+
+  // layout (elements)
+  int64_t X = 0, Y = 0, pitch = 0, plane = 0, xoff = 0;
+  int64_t own_z0 = 0, own_z1 = 0, store_z0 = 0, store_z1 = 0, zl = 0;
+  int64_t slab_lo = 0, slab_hi = 0;  // this rank's interior planes (global padded) [lo, hi)
+  size_t arr_bytes = 0;
+
+  // device memory
+  std::vector<std::pair<void*, size_t>> allocs;
+  double* buf[4] = {nullptr, nullptr, nullptr, nullptr};  // raw (un-offset) state buffers
+  int nbuf = 2;
+  int lv0 = 0, lv1 = 1;   // buffer index of Omega^t and Omega^{t-1}
+  double* coef = nullptr;  // raw coefficient slab (ncoef fields of zl planes)
+  double scal[6] = {0, 0, 0, 0, 0, 0};
+
+  int64_t steps = 0;
+  int64_t launches = 0;
+  int64_t device_bytes = 0;
+  bool poisoned = false;
+  std::atomic<int> busy{0};
+  st::LaunchInfo last_launch{};
+
+  // timing
+  bool timing = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> events;
+  size_t events_used = 0;
+
+  ncclComm_t comm = nullptr;
+
+  double* at(int b) const { return buf[b] + xoff; }        // element (0,0,0) of buffer b
+  double* coef_at() const { return coef ? coef + xoff : nullptr; }
+};
+
+namespace {
+
+struct Guard {  // not reentrant: one thread at a time per handle
+  stencil_ctx* h;
+  bool ok;
+  explicit Guard(stencil_ctx* hh) : h(hh), ok(false) {
+    int z = 0;
+    ok = h->busy.compare_exchange_strong(z, 1);
+  }
+  ~Guard() { if (ok) h->busy.store(0); }
+};
+
+int cuda_fail(stencil_ctx* h, cudaError_t e, const char* what) {
+  set_err("%s: %s (%s)", what, cudaGetErrorString(e), cudaGetErrorName(e));
+  if (h) h->poisoned = true;
+  return ST_E_CUDA;
+}
+
+#define CK(expr, what)                                   \
+  do {                                                   \
+    cudaError_t _e = (expr);                             \
+    if (_e != cudaSuccess) return cuda_fail(h, _e, what); \
+  } while (0)
+
+void* dev_alloc(stencil_ctx* h, size_t bytes) {
+  void* p = nullptr;
+  if (h->alloc) {
+    p = h->alloc(bytes, (void*)h->stream, h->alloc_user);
+  } else if (cudaMalloc(&p, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    p = nullptr;
+  }
+  if (p) {
+    h->allocs.emplace_back(p, bytes);
+    h->device_bytes += (int64_t)bytes;
+  }
+  return p;
+}
+
+void release(stencil_ctx* h) {
+  cudaStreamSynchronize(h->stream);
+  for (auto& a : h->allocs) {
+    if (h->free_fn) h->free_fn(a.first, a.second, (void*)h->stream, h->alloc_user);
+    else cudaFree(a.first);
+  }
+  h->allocs.clear();
+  for (auto& e : h->events) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
+  h->events.clear();
+  if (h->comm && nccl()) nccl()->CommDestroy(h->comm);
+  h->comm = nullptr;
+}
+
+int default_bt(int kind) {
+  switch (kind) {
+    case ST_7PT_CONST: return 4;
+    case ST_7PT_VAR: return 2;
+    default: return 1;
+  }
+}
+
+int plan_slab(int64_t nz, int R, int nranks, int rank, int bt, int64_t* own_z0, int64_t* own_z1,
+              int64_t* store_z0, int64_t* store_z1, int* bt_eff, int64_t* slab_lo, int64_t* slab_hi) {
+  if (nz < 1 || R < 1 || nranks < 1 || rank < 0 || rank >= nranks || nz < nranks || bt < 0) {
+    set_err("plan_slab: bad arguments (nz=%lld R=%d nranks=%d rank=%d bt=%d)", (long long)nz, R,
+            nranks, rank, bt);
+    return ST_E_INVAL;
+  }
+  const int64_t base = nz / nranks, rem = nz % nranks;
+  const int64_t thin = base;  // thinnest slab
+  if (nranks > 1 && thin < R) {
+    set_err("plan_slab: slabs of %lld planes are thinner than the radius %d (nz=%lld, nranks=%d)",
+            (long long)thin, R, (long long)nz, nranks);
+    return ST_E_INVAL;
+  }
+  int b = std::max(1, bt);
+  if (nranks > 1) b = (int)std::max<int64_t>(1, std::min<int64_t>(b, thin / R));
+  const int64_t lo = R + rank * base + std::min<int64_t>(rank, rem);
+  const int64_t hi = lo + base + (rank < rem ? 1 : 0);
+  const int64_t H = (int64_t)R * b;
+  *own_z0 = rank == 0 ? 0 : lo;
+  *own_z1 = rank == nranks - 1 ? nz + 2 * R : hi;
+  *store_z0 = rank == 0 ? 0 : lo - H;
+  *store_z1 = rank == nranks - 1 ? nz + 2 * R : hi + H;
+  if (bt_eff) *bt_eff = b;
+  if (slab_lo) *slab_lo = lo;
+  if (slab_hi) *slab_hi = hi;
+  return ST_OK;
+}
+
+// Common part of both create calls: validation, device, plan, allocation.
+int create_common(stencil_ctx** out, int kind, int64_t nx, int64_t ny, int64_t nz,
+                  const st_opts* opts_in, stencil_ctx** hp) {
+  if (!out) { set_err("out is NULL"); return ST_E_INVAL; }
+  *out = nullptr;
+  st_opts o;
+  stencil_opts_default(&o);
+  if (opts_in) o = *opts_in;
+  const int R = radius_of(kind);
+  if (R < 0) { set_err("bad kind %d", kind); return ST_E_INVAL; }
+  if (nx < 1 || ny < 1 || nz < 1) { set_err("extents must be >= 1 (got %lld %lld %lld)", (long long)nx, (long long)ny, (long long)nz); return ST_E_INVAL; }
+  if (nx > (1 << 30) || ny > (1 << 30)) { set_err("extent too large"); return ST_E_INVAL; }
+  if (o.bt < 0 || o.variant < 0 || o.variant > ST_VARIANT_STREAM || o.zchunk < 0) {
+    set_err("bad options (bt=%d variant=%d zchunk=%d)", o.bt, o.variant, o.zchunk);
+    return ST_E_INVAL;
+  }
+  if (o.nranks < 1 || o.rank < 0 || o.rank >= o.nranks) { set_err("bad rank %d of %d", o.rank, o.nranks); return ST_E_INVAL; }
+  if (nz < o.nranks) { set_err("nz=%lld < nranks=%d", (long long)nz, o.nranks); return ST_E_INVAL; }
+  if (o.nranks > 1 && !o.nccl_id) { set_err("nranks > 1 needs nccl_id"); return ST_E_INVAL; }
+
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev < 1) {
+    cudaGetLastError();
+    set_err("no CUDA device available (%s); libstencil has no CPU fallback",
+            e != cudaSuccess ? cudaGetErrorString(e) : "0 devices");
+    return ST_E_CUDA;
+  }
+  int dev = o.device;
+  if (dev < 0) cudaGetDevice(&dev);
+  if (dev >= ndev) { set_err("device %d >= device count %d", dev, ndev); return ST_E_INVAL; }
+
+  stencil_ctx* h = new stencil_ctx();
+  *hp = h;
+  h->kind = kind; h->R = R; h->ncoef = ncoef_of(kind); h->nscal = nscal_of(kind);
+  h->nx = nx; h->ny = ny; h->nz = nz;
+  h->rank = o.rank; h->nranks = o.nranks;
+  h->device = dev;
+  h->stream = (cudaStream_t)o.stream;
+  h->alloc = o.alloc; h->free_fn = o.free; h->alloc_user = o.alloc_user;
+  h->zchunk_req = o.zchunk;
+  CK(cudaSetDevice(dev), "cudaSetDevice");
+  CK(cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, dev), "device attribute");
+
+  h->variant = o.variant == ST_VARIANT_AUTO ? ST_VARIANT_STREAM : o.variant;
+  int bt = h->variant == ST_VARIANT_NAIVE ? 1 : (o.bt ? o.bt : default_bt(kind));
+  bt = std::min(bt, std::max(1, st::max_stream_bt(kind)));
+  int bt_eff = 1;
+  int rc = plan_slab(nz, R, o.nranks, o.rank, bt, &h->own_z0, &h->own_z1, &h->store_z0, &h->store_z1,
+                     &bt_eff, &h->slab_lo, &h->slab_hi);
+  if (rc) return rc;
+  h->bt = bt_eff;
+  h->zl = h->store_z1 - h->store_z0;
+
+  // Device layout: interior column x = R lands on a 128-byte boundary; rows padded to 16 doubles.
+  h->X = nx + 2 * R;
+  h->Y = ny + 2 * R;
+  h->xoff = 16 - R;
+  h->pitch = ((h->xoff + h->X) + 15) / 16 * 16;
+  h->plane = h->pitch * h->Y;
+  h->arr_bytes = (size_t)h->plane * (size_t)h->zl * sizeof(double);
+  h->nbuf = (kind == ST_25PT_WAVE && h->bt >= 2) ? 4 : 2;
+  for (int b = 0; b < h->nbuf; ++b) {
+    h->buf[b] = (double*)dev_alloc(h, h->arr_bytes);
+    if (!h->buf[b]) {
+      set_err("device allocation of %zu bytes failed (state buffer %d; %lld bytes held)", h->arr_bytes, b,
+              (long long)h->device_bytes);
+      return ST_E_NOMEM;
+    }
+  }
+  if (h->ncoef) {
+    const size_t cb = h->arr_bytes * (size_t)h->ncoef;
+    h->coef = (double*)dev_alloc(h, cb);
+    if (!h->coef) {
+      set_err("device allocation of %zu bytes failed (%d coefficient fields; %lld bytes held)", cb,
+              h->ncoef, (long long)h->device_bytes);
+      return ST_E_NOMEM;
+    }
+  }
+  h->lv0 = 0;
+  h->lv1 = 1;
+
+  if (o.nranks > 1) {
+    Nccl* n = nccl();
+    if (!n) { h->poisoned = true; return ST_E_NCCL; }
+    ncclUniqueId id;
+    memcpy(&id, o.nccl_id, sizeof id);
+    ncclResult_t r = n->CommInitRank(&h->comm, o.nranks, id, o.rank);
+    if (r != ncclSuccess) {
+      set_err("ncclCommInitRank: %s", n->GetErrorString(r));
+      h->comm = nullptr;
+      h->poisoned = true;
+      return ST_E_NCCL;
+    }
+  }
+  return ST_OK;
+}
+
+// Copy dense padded global host planes [store_z0, store_z1) into device buffer dst (raw pointer).
+cudaError_t upload_planes(stencil_ctx* h, double* raw, const double* host) {
+  const double* src = host + (size_t)h->store_z0 * h->X * h->Y;
+  return cudaMemcpy2DAsync(raw + h->xoff, h->pitch * sizeof(double), src, h->X * sizeof(double),
+                           h->X * sizeof(double), (size_t)h->Y * h->zl, cudaMemcpyHostToDevice,
+                           h->stream);
+}
+
+void fail_create(stencil_ctx* h) {
+  if (!h) return;
+  release(h);
+  delete h;
+}
+
+st::KParams base_params(stencil_ctx* h) {
+  st::KParams p{};
+  p.coef = h->coef_at();
+  p.cstride = h->plane * h->zl;
+  p.pitch = h->pitch;
+  p.plane = h->plane;
+  p.nx = (int)h->nx;
+  p.ny = (int)h->ny;
+  p.zl = (int)h->zl;
+  p.zi0 = (int)std::max<int64_t>(0, h->R - h->store_z0);
+  p.zi1 = (int)std::min<int64_t>(h->zl, h->nz + h->R - h->store_z0);
+  p.zo0 = (int)(h->slab_lo - h->store_z0);
+  p.zo1 = (int)(h->slab_hi - h->store_z0);
+  for (int i = 0; i < 6; ++i) p.s[i] = h->scal[i];
+  return p;
+}
+
+cudaEvent_t timing_begin(stencil_ctx* h, cudaEvent_t* end) {
+  if (!h->timing) return nullptr;
+  if (h->events_used == h->events.size()) {
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    h->events.emplace_back(a, b);
+  }
+  auto& pr = h->events[h->events_used++];
+  cudaEventRecord(pr.first, h->stream);
+  *end = pr.second;
+  return pr.first;
+}
+
+// NCCL halo exchange of `depth` planes of buffer b (Jacobi: the new level; wave: both levels).
+int exchange(stencil_ctx* h, int b, int64_t depth) {
+  if (h->nranks == 1 || depth <= 0) return ST_OK;
+  Nccl* n = nccl();
+  if (!n) { h->poisoned = true; return ST_E_NCCL; }
+  const int64_t lo = h->slab_lo - h->store_z0, hi = h->slab_hi - h->store_z0;
+  double* base = h->buf[b];
+  const size_t cnt = (size_t)(depth * h->plane);
+  ncclResult_t r = n->GroupStart();
+  if (h->rank > 0 && r == ncclSuccess) {
+    r = n->Send(base + lo * h->plane, cnt, ncclFloat64, h->rank - 1, h->comm, h->stream);
+    if (r == ncclSuccess)
+      r = n->Recv(base + (lo - depth) * h->plane, cnt, ncclFloat64, h->rank - 1, h->comm, h->stream);
+  }
+  if (h->rank < h->nranks - 1 && r == ncclSuccess) {
+    r = n->Send(base + (hi - depth) * h->plane, cnt, ncclFloat64, h->rank + 1, h->comm, h->stream);
+    if (r == ncclSuccess)
+      r = n->Recv(base + hi * h->plane, cnt, ncclFloat64, h->rank + 1, h->comm, h->stream);
+  }
+  ncclResult_t r2 = n->GroupEnd();
+  if (r == ncclSuccess) r = r2;
+  if (r != ncclSuccess) {
+    set_err("NCCL halo exchange: %s", n->GetErrorString(r));
+    h->poisoned = true;
+    return ST_E_NCCL;
+  }
+  return ST_OK;
+}
+
+// One block of b levels: launch, rotate roles, exchange halos.
+int run_block(stencil_ctx* h, int b) {
+  st::KParams p = base_params(h);
+  const bool wave = h->kind == ST_25PT_WAVE;
+  int new0, new1;
+  if (!wave) {
+    p.src = h->at(h->lv0);
+    p.dst = h->at(h->lv1);
+    new0 = h->lv1;
+    new1 = h->lv0;
+  } else if (b == 1) {
+    p.src = h->at(h->lv0);
+    p.srcu = h->at(h->lv1);
+    p.dst = h->at(h->lv1);  // Omega^{t+1} overwrites Omega^{t-1} in place
+    new0 = h->lv1;
+    new1 = h->lv0;
+  } else {
+    int spare[2], k = 0;
+    for (int i = 0; i < 4; ++i)
+      if (i != h->lv0 && i != h->lv1) spare[k++] = i;
+    p.src = h->at(h->lv0);
+    p.srcu = h->at(h->lv1);
+    p.dst = h->at(spare[0]);
+    p.dstu = h->at(spare[1]);
+    new0 = spare[0];
+    new1 = spare[1];
+  }
+  cudaEvent_t ev_end = nullptr;
+  cudaEvent_t ev_begin = timing_begin(h, &ev_end);
+  cudaError_t e;
+  if (h->variant == ST_VARIANT_NAIVE)
+    e = st::launch_naive(h->kind, p, h->stream, &h->last_launch);
+  else
+    e = st::launch_stream(h->kind, b, p, h->zchunk_req, h->num_sms, h->stream, &h->last_launch);
+  if (ev_begin) cudaEventRecord(ev_end, h->stream);
+  if (e != cudaSuccess) return cuda_fail(h, e, "kernel launch");
+  h->launches++;
+  h->lv0 = new0;
+  h->lv1 = new1;
+  h->steps += b;
+  int rc = exchange(h, h->lv0, (int64_t)h->R * b);
+  if (!rc && wave) rc = exchange(h, h->lv1, (int64_t)h->R * b);
+  return rc;
+}
+
+int check_handle(stencil_ctx* h) {
+  if (!h) { set_err("NULL handle"); return ST_E_INVAL; }
+  if (h->poisoned) { set_err("handle poisoned by an earlier CUDA/NCCL failure"); return ST_E_STATE; }
+  return ST_OK;
+}
+
+}  // namespace
+
+// ================================================================ C ABI
+extern "C" {
+
+void stencil_opts_default(st_opts* o) {
+  if (!o) return;
+  memset(o, 0, sizeof *o);
+  o->device = -1;
+  o->variant = ST_VARIANT_AUTO;
+  o->nranks = 1;
+}
+
+const char* stencil_last_error(void) { return g_err.c_str(); }
+
+const char* stencil_version(void) { return STENCIL_VERSION " (sm_100a)"; }
+
+int stencil_plan_slab(int64_t nz, int R, int nranks, int rank, int bt, int64_t* own_z0,
+                      int64_t* own_z1, int64_t* store_z0, int64_t* store_z1, int* bt_eff) {
+  if (!own_z0 || !own_z1 || !store_z0 || !store_z1) { set_err("NULL output"); return ST_E_INVAL; }
+  return plan_slab(nz, R, nranks, rank, bt, own_z0, own_z1, store_z0, store_z1, bt_eff, nullptr, nullptr);
+}
+
+int stencil_create(stencil_ctx** out, int kind, int64_t nx, int64_t ny, int64_t nz,
+                   const double* const* coeff, int n_coeff, const double* v0, const double* u0,
+                   const st_opts* opts) {
+  const int R = radius_of(kind);
+  if (R < 0) { set_err("bad kind %d", kind); return ST_E_INVAL; }
+  const int want = kind == 1 ? 2 : kind == 2 ? 7 : kind == 3 ? 6 : 13;
+  if (n_coeff != want) { set_err("kind %d needs n_coeff=%d (got %d)", kind, want, n_coeff); return ST_E_INVAL; }
+  if (!coeff || !v0) { set_err("NULL coeff or v0"); return ST_E_INVAL; }
+  for (int i = 0; i < n_coeff; ++i)
+    if (!coeff[i]) { set_err("coeff[%d] is NULL", i); return ST_E_INVAL; }
+  if (kind == ST_25PT_WAVE && !u0) { set_err("ST_25PT_WAVE needs u0"); return ST_E_INVAL; }
+  if (kind != ST_25PT_WAVE && u0) { set_err("u0 must be NULL for kind %d", kind); return ST_E_INVAL; }
+  stencil_ctx* h = nullptr;
+  int rc = create_common(out, kind, nx, ny, nz, opts, &h);
+  if (rc) { fail_create(h); return rc; }
+  const size_t hplane = (size_t)h->X * h->Y;
+  cudaError_t e;
+  for (int b = 0; b < h->nbuf && rc == ST_OK; ++b) {
+    e = upload_planes(h, h->buf[b], v0);
+    if (e != cudaSuccess) rc = cuda_fail(h, e, "upload state");
+  }
+  if (rc == ST_OK && kind == ST_25PT_WAVE) {
+    // level 1 = Omega^{-1}: interior from u0, ghosts from v0 (reading Q9).  Upload u0's
+    // planes, then restore ghosts from v0: ghost planes wholesale, ghost rows/columns by 2-D copies.
+    double* d = h->buf[h->lv1] + h->xoff;
+    for (int64_t z = 0; z < h->zl && rc == ST_OK; ++z) {
+      const int64_t gz = h->store_z0 + z;
+      const bool zghost = gz < R || gz >= nz + R;
+      const double* src = (zghost ? v0 : u0) + (size_t)gz * hplane;
+      e = cudaMemcpy2DAsync(d + z * h->plane, h->pitch * sizeof(double), src, h->X * sizeof(double),
+                            h->X * sizeof(double), h->Y, cudaMemcpyHostToDevice, h->stream);
+      if (e == cudaSuccess && !zghost) {
+        const double* g = v0 + (size_t)gz * hplane;
+        double* dz = d + z * h->plane;
+        // y-ghost rows (R at each end) and x-ghost columns (R at each end of every row)
+        e = cudaMemcpy2DAsync(dz, h->pitch * sizeof(double), g, h->X * sizeof(double), h->X * sizeof(double), R, cudaMemcpyHostToDevice, h->stream);
+        if (e == cudaSuccess)
+          e = cudaMemcpy2DAsync(dz + (h->Y - R) * h->pitch, h->pitch * sizeof(double), g + (h->Y - R) * h->X, h->X * sizeof(double), h->X * sizeof(double), R, cudaMemcpyHostToDevice, h->stream);
+        if (e == cudaSuccess)
+          e = cudaMemcpy2DAsync(dz, h->pitch * sizeof(double), g, h->X * sizeof(double), R * sizeof(double), h->Y, cudaMemcpyHostToDevice, h->stream);
+        if (e == cudaSuccess)
+          e = cudaMemcpy2DAsync(dz + h->X - R, h->pitch * sizeof(double), g + h->X - R, h->X * sizeof(double), R * sizeof(double), h->Y, cudaMemcpyHostToDevice, h->stream);
+      }
+      if (e != cudaSuccess) rc = cuda_fail(h, e, "upload wave level 1");
+    }
+  }
+  if (rc == ST_OK && h->ncoef) {
+    for (int i = 0; i < h->ncoef && rc == ST_OK; ++i) {
+      e = upload_planes(h, h->coef + (size_t)i * h->plane * h->zl, coeff[i]);
+      if (e != cudaSuccess) rc = cuda_fail(h, e, "upload coefficients");
+    }
+  } else if (rc == ST_OK) {
+    for (int i = 0; i < h->nscal; ++i) h->scal[i] = *coeff[i];
+  }
+  if (rc == ST_OK) {
+    e = cudaStreamSynchronize(h->stream);  // host arrays may be freed by the caller after return
+    if (e != cudaSuccess) rc = cuda_fail(h, e, "create synchronize");
+  }
+  if (rc) { fail_create(h); return rc; }
+  *out = h;
+  return ST_OK;
+}
+
+int stencil_create_seeded(stencil_ctx** out, int kind, int64_t nx, int64_t ny, int64_t nz,
+                          uint64_t seed, const double* scalars, const st_opts* opts) {
+  const int R = radius_of(kind);
+  if (R < 0) { set_err("bad kind %d", kind); return ST_E_INVAL; }
+  if (nscal_of(kind) == 0 && scalars) { set_err("variable kinds take no scalars"); return ST_E_INVAL; }
+  stencil_ctx* h = nullptr;
+  int rc = create_common(out, kind, nx, ny, nz, opts, &h);
+  if (rc) { fail_create(h); return rc; }
+  static const double d7c[2] = {0.4, 0.1};
+  const double d25w[6] = {3.0 * (-205.0 / 72.0), 8.0 / 5.0, -1.0 / 5.0, 8.0 / 315.0, -1.0 / 560.0, 0.1};
+  if (kind == ST_7PT_CONST) for (int i = 0; i < 2; ++i) h->scal[i] = scalars ? scalars[i] : d7c[i];
+  if (kind == ST_25PT_WAVE) for (int i = 0; i < 6; ++i) h->scal[i] = scalars ? scalars[i] : d25w[i];
+  const long long GZ = nz + 2 * R;
+  cudaError_t e = cudaSuccess;
+  for (int b = 0; b < h->nbuf && e == cudaSuccess; ++b) {
+    const int mode = (kind == ST_25PT_WAVE && b == h->lv1) ? 1 : 0;
+    e = st::launch_fill(h->buf[b] + h->xoff, h->pitch, h->plane, (int)h->zl, h->store_z0, h->X, h->Y,
+                        GZ, R, seed, 0, mode, 0.0, h->stream);
+  }
+  const double c = kind == ST_7PT_VAR ? 1.0 / 7.0 : 1.0 / 25.0;
+  for (int i = 0; i < h->ncoef && e == cudaSuccess; ++i)
+    e = st::launch_fill(h->coef + (size_t)i * h->plane * h->zl + h->xoff, h->pitch, h->plane, (int)h->zl,
+                        h->store_z0, h->X, h->Y, GZ, R, seed, 2 + i, 2, c, h->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+  if (e != cudaSuccess) {
+    rc = cuda_fail(h, e, "seeded fill");
+    fail_create(h);
+    return rc;
+  }
+  *out = h;
+  return ST_OK;
+}
+
+int stencil_run(stencil_ctx* h, int64_t T) {
+  int rc = check_handle(h);
+  if (rc) return rc;
+  if (T < 1) { set_err("T must be >= 1 (got %lld)", (long long)T); return ST_E_INVAL; }
+  Guard g(h);
+  if (!g.ok) { set_err("handle used concurrently"); return ST_E_STATE; }
+  const cudaError_t e = cudaSetDevice(h->device);
+  if (e != cudaSuccess) return cuda_fail(h, e, "cudaSetDevice");
+  const int bt = h->variant == ST_VARIANT_NAIVE ? 1 : h->bt;
+  int64_t left = T;
+  while (left > 0 && rc == ST_OK) {
+    const int b = (int)std::min<int64_t>(bt, left);
+    rc = run_block(h, b);
+    left -= b;
+  }
+  return rc;
+}
+
+int stencil_sync(stencil_ctx* h) {
+  int rc = check_handle(h);
+  if (rc) return rc;
+  cudaError_t e = cudaStreamSynchronize(h->stream);
+  if (e != cudaSuccess) return cuda_fail(h, e, "stream synchronize");
+  return ST_OK;
+}
+
+int stencil_read_planes(stencil_ctx* h, int level, int64_t z0, int64_t z1, double* out, int64_t out_elems) {
+  int rc = check_handle(h);
+  if (rc) return rc;
+  if (level < 0 || level > 1 || (level == 1 && h->kind != ST_25PT_WAVE)) {
+    set_err("level %d not readable for kind %d", level, h->kind);
+    return ST_E_INVAL;
+  }
+  if (!out || z0 < h->own_z0 || z1 > h->own_z1 || z0 > z1) {
+    set_err("planes [%lld,%lld) outside owned [%lld,%lld) or NULL out", (long long)z0, (long long)z1,
+            (long long)h->own_z0, (long long)h->own_z1);
+    return ST_E_INVAL;
+  }
+  const int64_t need = (z1 - z0) * h->X * h->Y;
+  if (out_elems < need) { set_err("out_elems %lld < %lld", (long long)out_elems, (long long)need); return ST_E_INVAL; }
+  Guard g(h);
+  if (!g.ok) { set_err("handle used concurrently"); return ST_E_STATE; }
+  if (z1 == z0) return ST_OK;
+  const double* src = h->at(level == 0 ? h->lv0 : h->lv1) + (z0 - h->store_z0) * h->plane;
+  cudaError_t e = cudaMemcpy2DAsync(out, h->X * sizeof(double), src, h->pitch * sizeof(double),
+                                    h->X * sizeof(double), (size_t)h->Y * (z1 - z0),
+                                    cudaMemcpyDeviceToHost, h->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+  if (e != cudaSuccess) return cuda_fail(h, e, "read");
+  return ST_OK;
+}
+
+int stencil_read(stencil_ctx* h, int level, double* out, int64_t out_elems) {
+  int rc = check_handle(h);
+  if (rc) return rc;
+  const int64_t total = (h->nz + 2 * h->R) * h->X * h->Y;
+  if (!out || out_elems < total) { set_err("out must hold %lld doubles", (long long)total); return ST_E_INVAL; }
+  return stencil_read_planes(h, level, h->own_z0, h->own_z1, out + h->own_z0 * h->X * h->Y,
+                             (h->own_z1 - h->own_z0) * h->X * h->Y);
+}
+
+int stencil_write(stencil_ctx* h, int level, const double* in, int64_t in_elems) {
+  int rc = check_handle(h);
+  if (rc) return rc;
+  if (level < 0 || level > 1 || (level == 1 && h->kind != ST_25PT_WAVE)) {
+    set_err("level %d not writable for kind %d", level, h->kind);
+    return ST_E_INVAL;
+  }
+  const int64_t total = (h->nz + 2 * h->R) * h->X * h->Y;
+  if (!in || in_elems < total) { set_err("in must hold %lld doubles", (long long)total); return ST_E_INVAL; }
+  Guard g(h);
+  if (!g.ok) { set_err("handle used concurrently"); return ST_E_STATE; }
+  cudaError_t e = upload_planes(h, h->buf[level == 0 ? h->lv0 : h->lv1], in);
+  if (e == cudaSuccess && level == 0 && h->kind != ST_25PT_WAVE)
+    e = upload_planes(h, h->buf[h->lv1], in);  // keep level 1's ghosts equal to the new ghosts
+  if (e == cudaSuccess && h->kind == ST_25PT_WAVE && h->nbuf == 4 && level == 0) {
+    for (int b = 0; b < 4 && e == cudaSuccess; ++b)
+      if (b != h->lv0 && b != h->lv1) e = upload_planes(h, h->buf[b], in);  // spare buffers' ghosts
+  }
+  if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+  if (e != cudaSuccess) return cuda_fail(h, e, "write");
+  return ST_OK;
+}
+
+int stencil_info(const stencil_ctx* h, st_info* o) {
+  if (!h || !o) { set_err("NULL handle or out"); return ST_E_INVAL; }
+  memset(o, 0, sizeof *o);
+  o->kind = h->kind; o->R = h->R; o->bt = h->variant == ST_VARIANT_NAIVE ? 1 : h->bt;
+  o->variant = h->variant; o->rank = h->rank; o->nranks = h->nranks;
+  o->tile_x = h->last_launch.tile_x; o->tile_y = h->last_launch.tile_y; o->zchunk = h->last_launch.zchunk;
+  o->nx = h->nx; o->ny = h->ny; o->nz = h->nz;
+  o->own_z0 = h->own_z0; o->own_z1 = h->own_z1;
+  o->pitch = h->pitch; o->plane = h->plane; o->local_planes = h->zl;
+  o->device_bytes = h->device_bytes; o->steps_done = h->steps; o->launches = h->launches;
+  return ST_OK;
+}
+
+int stencil_set_timing(stencil_ctx* h, int enable) {
+  int rc = check_handle(h);
+  if (rc) return rc;
+  h->timing = enable != 0;
+  return ST_OK;
+}
+
+int stencil_kernel_time(stencil_ctx* h, double* ms, int64_t* launches, int reset) {
+  int rc = check_handle(h);
+  if (rc) return rc;
+  cudaError_t e = cudaStreamSynchronize(h->stream);
+  if (e != cudaSuccess) return cuda_fail(h, e, "kernel_time synchronize");
+  double tot = 0.0;
+  for (size_t i = 0; i < h->events_used; ++i) {
+    float t = 0.f;
+    e = cudaEventElapsedTime(&t, h->events[i].first, h->events[i].second);
+    if (e != cudaSuccess) return cuda_fail(h, e, "cudaEventElapsedTime");
+    tot += t;
+  }
+  if (ms) *ms = tot;
+  if (launches) *launches = (int64_t)h->events_used;
+  if (reset) h->events_used = 0;
+  return ST_OK;
+}
+
+int stencil_destroy(stencil_ctx* h) {
+  if (!h) return ST_OK;
+  cudaSetDevice(h->device);
+  release(h);
+  delete h;
+  return ST_OK;
+}
+
+int stencil_nccl_unique_id(void* out, size_t out_bytes) {
+  if (!out || out_bytes < sizeof(ncclUniqueId)) { set_err("need %zu bytes", sizeof(ncclUniqueId)); return ST_E_INVAL; }
+  Nccl* n = nccl();
+  if (!n) return ST_E_NCCL;
+  ncclUniqueId id;
+  ncclResult_t r = n->GetUniqueId(&id);
+  if (r != ncclSuccess) { set_err("ncclGetUniqueId: %s", n->GetErrorString(r)); return ST_E_NCCL; }
+  memcpy(out, &id, sizeof id);
+  return ST_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,51 @@
+"""Helpers shared by the -m gpu tests: run the CUDA path through the C ABI and compare with oracle/."""
+import numpy as np
+
+import oracle
+import paper_1410_3060_b200 as st
+import synth
+
+WAVE = synth.K25W
+
+
+def interior(R):
+    return (slice(R, -R),) * 3
+
+
+def gpu_run(kind, nx, ny, nz, T, seed=synth.DEFAULT_SEED, variant=0, bt=0, zchunk=0, inputs=None,
+            scalars=None):
+    """Run the CUDA path; returns (Omega^T, Omega^{T-1} or None, info)."""
+    if inputs is None:
+        g = st.Grid(kind, nx, ny, nz, seed=seed, scalars=scalars, variant=variant, bt=bt, zchunk=zchunk)
+    else:
+        coeff = inputs.coef if inputs.coef else list(inputs.scalars)
+        u0 = inputs.U if kind == WAVE else None
+        g = st.Grid(kind, nx, ny, nz, v0=inputs.V, u0=u0, coeff=coeff, variant=variant, bt=bt,
+                    zchunk=zchunk)
+    with g:
+        if T > 0:
+            g.run(T)
+        new = g.read(0)
+        old = g.read(1) if kind == WAVE else None
+        info = g.info()
+    return new, old, info
+
+
+def rel_err(g, o, R):
+    I = interior(R)
+    d = np.max(np.abs(g[I] - o[I]))
+    return d / max(np.max(np.abs(o[I])), 1e-300)
+
+
+def assert_parity(kind, g_new, g_old, o_new, o_old, R, tol, inputs=None):
+    e = rel_err(g_new, o_new, R)
+    assert e <= tol, f"normwise relative error {e:.3e} > {tol:.1e}"
+    if kind == WAVE:
+        e1 = rel_err(g_old, o_old, R)
+        assert e1 <= tol, f"level-1 normwise relative error {e1:.3e} > {tol:.1e}"
+    if inputs is not None:  # G5: ghosts bitwise untouched
+        m = np.ones(g_new.shape, bool)
+        m[interior(R)] = False
+        assert np.array_equal(g_new[m], inputs.V[m])
+        if kind == WAVE:
+            assert np.array_equal(g_old[m], inputs.V[m])

@@ -1,0 +1,105 @@
+"""Parity at BASELINE.json's full sizes, in the launch configuration bench.py times (the library's
+default plan): configs[0] (C1) against a full oracle run; C2-C5 at full size on sampled cells that
+oracle.run_cone computes one by one (exact inside the cell's domain of dependence), and at full T
+via a property that holds at any size -- bitwise equality with the naive GPU sweep (G4)."""
+import numpy as np
+import pytest
+
+import oracle
+import paper_1410_3060_b200 as st
+import synth
+from synth import workloads
+from gpu_common import WAVE, assert_parity, gpu_run
+
+pytestmark = pytest.mark.gpu
+
+
+def sample_cells(w, n, seed=0):
+    R = synth.RADIUS[w.kind]
+    rng = np.random.default_rng(seed)
+    hi = (w.nz + R - 1, w.ny + R - 1, w.nx + R - 1)
+    cells = [(R, R, R), hi, (R, hi[1], (w.nx // 2) + R), ((w.nz // 2) + R, R + 1, hi[2] - 2)]
+    while len(cells) < n:
+        cells.append(tuple(int(rng.integers(R, h + 1)) for h in hi))
+    return cells[:n]
+
+
+def grid_values(g, cells, level=0):
+    out = []
+    for (z, y, x) in cells:
+        pl = g.read_planes(level, z, z + 1)
+        out.append(pl[0, y, x])
+    return np.array(out)
+
+
+def test_C1_full_oracle():
+    w = workloads.C1
+    inp = synth.make_inputs(w.kind, w.nx, w.ny, w.nz)
+    o_new, o_old = oracle.run(inp, w.T)
+    g_new, g_old, _ = gpu_run(w.kind, w.nx, w.ny, w.nz, w.T)
+    assert_parity(w.kind, g_new, g_old, o_new, o_old, inp.R, 1e-11, inputs=inp)
+
+
+@pytest.mark.parametrize("name", ["C2-7pt-var-512", "C3-25pt-wave-512", "C4-25pt-var-512"])
+def test_512_sampled_cells(name):
+    w = workloads.BY_NAME[name]
+    R = synth.RADIUS[w.kind]
+    # 7-point: the cone of the full T = 100 is small enough; 25-point: T = 10 (cone radius 40)
+    T = w.T if R == 1 else 10
+    ncell = 5 if R == 1 else 12
+    cells = sample_cells(w, ncell, seed=1)
+    o_new, o_old = oracle.run_cone(w.kind, w.nx, w.ny, w.nz, cells, T)
+    with st.Grid(w.kind, w.nx, w.ny, w.nz, seed=synth.DEFAULT_SEED) as g:
+        g.run(T)
+        g_new = grid_values(g, cells)
+        scale = np.max(np.abs(g.read_planes(0, w.nz // 2, w.nz // 2 + 1)))
+        if w.kind == WAVE:
+            g_old = grid_values(g, cells, 1)
+    # normwise against the field's magnitude (max over a mid plane), BASELINE.json's 1e-11
+    assert np.max(np.abs(g_new - o_new)) <= 1e-11 * scale
+    if w.kind == WAVE:
+        assert np.max(np.abs(g_old - o_old)) <= 1e-11 * scale
+
+
+@pytest.mark.parametrize("name", ["C2-7pt-var-512", "C3-25pt-wave-512", "C4-25pt-var-512"])
+def test_512_full_T_bitwise_vs_naive(name):
+    w = workloads.BY_NAME[name]
+    planes = [synth.RADIUS[w.kind], w.nz // 3, w.nz // 2 + 7, w.nz + synth.RADIUS[w.kind] - 1]
+    res = []
+    for variant in (st.ST_VARIANT_AUTO, st.ST_VARIANT_NAIVE):
+        with st.Grid(w.kind, w.nx, w.ny, w.nz, seed=synth.DEFAULT_SEED, variant=variant) as g:
+            g.run(w.T)
+            res.append([g.read_planes(0, z, z + 1) for z in planes])
+            if w.kind == WAVE:
+                res[-1] += [g.read_planes(1, z, z + 1) for z in planes]
+    for a, b in zip(*res):
+        assert np.array_equal(a, b)
+
+
+def _fits(bytes_needed):
+    import torch
+    free, _ = torch.cuda.mem_get_info()
+    return free > bytes_needed * 1.05
+
+
+def test_C5_full_size_sampled_and_bitwise():
+    w = workloads.C5
+    R = 4
+    need = 15 * (w.nx + 2 * R + 16) * (w.ny + 2 * R) * (w.nz + 2 * R) * 8
+    if not _fits(need):
+        pytest.skip("C5 does not fit this GPU")
+    cells = sample_cells(w, 8, seed=5)
+    o_new, _ = oracle.run_cone(w.kind, w.nx, w.ny, w.nz, cells, 6)
+    planes = [R, 300, w.nz + R - 1]
+    res = []
+    for variant in (st.ST_VARIANT_AUTO, st.ST_VARIANT_NAIVE):
+        with st.Grid(w.kind, w.nx, w.ny, w.nz, seed=synth.DEFAULT_SEED, variant=variant) as g:
+            g.run(6)
+            if variant == st.ST_VARIANT_AUTO:
+                g_new = grid_values(g, cells)
+                scale = np.max(np.abs(g.read_planes(0, w.nz // 2, w.nz // 2 + 1)))
+                assert np.max(np.abs(g_new - o_new)) <= 1e-11 * scale
+            g.run(w.T - 6)
+            res.append([g.read_planes(0, z, z + 1) for z in planes])
+    for a, b in zip(*res):
+        assert np.array_equal(a, b)

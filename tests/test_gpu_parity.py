@@ -1,0 +1,156 @@
+"""GPU parity (G1-G6): the CUDA path through the C ABI against oracle/ on the same seeded
+inputs, element by element, at sizes spanning several tiles with ragged tails; bitwise invariance of
+the GPU results across kernel variants; ghosts untouched; degenerate extents; error codes."""
+import numpy as np
+import pytest
+
+import oracle
+import paper_1410_3060_b200 as st
+import synth
+from gpu_common import WAVE, assert_parity, gpu_run, interior, rel_err
+
+pytestmark = pytest.mark.gpu
+
+KINDS = [synth.K7C, synth.K7V, synth.K25W, synth.K25V]
+# several tiles in x and y with ragged tails, several z-chunks (7-point tiles are 30..22 wide,
+# 25-point tiles 56 x 8)
+SHAPES = {synth.K7C: (61, 70, 45), synth.K7V: (61, 70, 45), synth.K25W: (130, 37, 41),
+          synth.K25V: (130, 37, 41)}
+
+
+def max_bt(kind):
+    return {synth.K7C: 6, synth.K7V: 4, synth.K25W: 1, synth.K25V: 1}[kind]
+
+
+@pytest.mark.parametrize("kind", KINDS)
+def test_seeded_fill_matches_host_generator(kind):
+    nx, ny, nz = 37, 20, 11
+    new, old, _ = gpu_run(kind, nx, ny, nz, 0, seed=77)
+    inp = synth.make_inputs(kind, nx, ny, nz, seed=77)
+    assert np.array_equal(new, inp.V)
+    if kind == WAVE:
+        assert np.array_equal(old, inp.U)
+
+
+@pytest.mark.parametrize("kind", KINDS)
+def test_create_from_host_equals_seeded(kind):
+    nx, ny, nz = 33, 19, 14
+    inp = synth.make_inputs(kind, nx, ny, nz, seed=5)
+    a = gpu_run(kind, nx, ny, nz, 7, seed=5)
+    b = gpu_run(kind, nx, ny, nz, 7, inputs=inp)
+    assert np.array_equal(a[0], b[0])
+    if kind == WAVE:
+        assert np.array_equal(a[1], b[1])
+
+
+@pytest.mark.parametrize("kind", KINDS)
+def test_parity_short_T_every_block_boundary(kind):
+    """G3: T in {1, 2, bt-1, bt, bt+1, 2bt+1} against the oracle, normwise <= 1e-13; G5 ghosts."""
+    nx, ny, nz = SHAPES[kind]
+    inp = synth.make_inputs(kind, nx, ny, nz, seed=3)
+    bts = sorted({1, 2, max_bt(kind)} & set(range(1, max_bt(kind) + 1)))
+    for bt in bts:
+        Ts = sorted({1, 2, max(1, bt - 1), bt, bt + 1, 2 * bt + 1})
+        o_new, o_old = inp.V.copy(), inp.U.copy()
+        done = 0
+        for T in Ts:
+            oracle.run_arrays(kind, nx, ny, nz, o_new, o_old, inp.coef, inp.scalars, T - done)
+            done = T
+            g_new, g_old, info = gpu_run(kind, nx, ny, nz, T, seed=3, bt=bt)
+            assert info["bt"] == bt
+            assert_parity(kind, g_new, g_old, o_new, o_old, inp.R, 1e-13, inputs=inp)
+
+
+@pytest.mark.parametrize("kind", KINDS)
+def test_parity_T20_default_plan(kind):
+    """G1 at moderate T with the library's default plan (the benchmarked one)."""
+    nx, ny, nz = SHAPES[kind]
+    inp = synth.make_inputs(kind, nx, ny, nz, seed=1)
+    T = 20
+    o_new, o_old = oracle.run(inp, T)
+    g_new, g_old, info = gpu_run(kind, nx, ny, nz, T, seed=1)
+    assert_parity(kind, g_new, g_old, o_new, o_old, inp.R, 1e-11, inputs=inp)
+
+
+@pytest.mark.parametrize("kind", [synth.K7C, synth.K7V, synth.K25V])
+def test_shadow_scaled_per_cell(kind):
+    """G2: |g - o| <= 1e-11 * S(p), S = oracle on |inputs| (non-negative coefficients), T = 60."""
+    n = (70, 66, 64) if synth.RADIUS[kind] == 1 else (72, 40, 48)
+    inp = synth.make_inputs(kind, *n, seed=2)
+    T = 60
+    o_new, _ = oracle.run(inp, T)
+    absinp = synth.Inputs(kind, *n, np.abs(inp.V), np.abs(inp.U), inp.coef, inp.scalars)
+    S, _ = oracle.run(absinp, T)
+    g_new, _, _ = gpu_run(kind, *n, T, seed=2)
+    I = interior(inp.R)
+    assert np.all(np.abs(g_new[I] - o_new[I]) <= 1e-11 * S[I])
+
+
+@pytest.mark.parametrize("kind", KINDS)
+def test_variants_bitwise_identical(kind):
+    """G4: naive == streaming (every bt, several z-chunks) bitwise."""
+    nx, ny, nz = SHAPES[kind]
+    T = 7
+    ref = gpu_run(kind, nx, ny, nz, T, seed=9, variant=st.ST_VARIANT_NAIVE)
+    for bt in range(1, max_bt(kind) + 1):
+        for zchunk in (0, 5, 1000):
+            got = gpu_run(kind, nx, ny, nz, T, seed=9, variant=st.ST_VARIANT_STREAM, bt=bt, zchunk=zchunk)
+            assert np.array_equal(got[0], ref[0]), (bt, zchunk)
+            if kind == WAVE:
+                assert np.array_equal(got[1], ref[1]), (bt, zchunk)
+
+
+@pytest.mark.parametrize("kind", KINDS)
+def test_degenerate_extents(kind):
+    """G6: extents 1, 2, 3, 5, 17 in every axis (nz < R*bt included), T not a multiple of bt."""
+    rng = np.random.default_rng(kind)
+    shapes = [(1, 1, 1), (2, 3, 1), (1, 5, 17), (17, 1, 2), (3, 17, 5), (5, 2, 3)]
+    shapes += [tuple(int(v) for v in rng.integers(1, 41, size=3)) for _ in range(3)]
+    for (nx, ny, nz) in shapes:
+        inp = synth.make_inputs(kind, nx, ny, nz, seed=4)
+        T = 5
+        o_new, o_old = oracle.run(inp, T)
+        for bt in sorted({1, max_bt(kind)}):
+            g_new, g_old, _ = gpu_run(kind, nx, ny, nz, T, seed=4, bt=bt)
+            assert_parity(kind, g_new, g_old, o_new, o_old, inp.R, 1e-13, inputs=inp)
+
+
+def test_checkpoint_resume_bitwise():
+    """run(T1); read; create from the read state; run(T2) == run(T1 + T2), bitwise (all kinds)."""
+    for kind in KINDS:
+        nx, ny, nz = SHAPES[kind]
+        inp = synth.make_inputs(kind, nx, ny, nz, seed=6)
+        full = gpu_run(kind, nx, ny, nz, 9, seed=6)
+        a_new, a_old, _ = gpu_run(kind, nx, ny, nz, 4, seed=6)
+        res = synth.Inputs(kind, nx, ny, nz, a_new, a_old if kind == WAVE else a_new.copy(), inp.coef,
+                           inp.scalars)
+        b = gpu_run(kind, nx, ny, nz, 5, inputs=res)
+        assert np.array_equal(b[0], full[0])
+        if kind == WAVE:
+            assert np.array_equal(b[1], full[1])
+
+
+def test_error_codes_on_gpu():
+    with pytest.raises(st.StencilError) as ei:
+        st.Grid(synth.K7C, 0, 4, 4, seed=1)
+    assert ei.value.code == st.ST_E_INVAL
+    g = st.Grid(synth.K7V, 8, 8, 8, seed=1)
+    with pytest.raises(st.StencilError) as ei:
+        g.run(0)
+    assert ei.value.code == st.ST_E_INVAL
+    with pytest.raises(st.StencilError) as ei:
+        g.read(1)  # level 1 is scratch for Jacobi kinds
+    assert ei.value.code == st.ST_E_INVAL
+    with pytest.raises(st.StencilError) as ei:
+        st.stencil_read(g.h, 0, np.zeros(10))
+    assert ei.value.code == st.ST_E_INVAL
+    info = g.info()
+    assert info["device_bytes"] > 0 and info["steps_done"] == 0
+    g.run(3)
+    g.sync()
+    assert g.info()["steps_done"] == 3
+    g.close()
+    with pytest.raises(st.StencilError) as ei:
+        st.Grid(synth.K25V, 4000, 4000, 4000, seed=1)  # 15 x 32 GB: does not fit
+    assert ei.value.code == st.ST_E_NOMEM
+    assert "bytes" in st.stencil_last_error()
