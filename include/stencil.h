@@ -71,8 +71,12 @@ enum {
 enum {
   ST_VARIANT_AUTO = 0,   /* library's choice for the kind and shape (the benchmarked plan) */
   ST_VARIANT_NAIVE = 1,  /* one thread per point, one launch per time step (the GPU naive sweep) */
-  ST_VARIANT_STREAM = 2  /* 2.5-D z-streaming; with bt > 1 the time-skewed wavefront of
-                            bt fused levels over overlapped xy tiles (P:569-602 transposed) */
+  ST_VARIANT_STREAM = 2, /* 2.5-D z-streaming; with bt > 1 the time-skewed wavefront of
+                            bt fused levels over overlapped xy tiles (P:569-602 transposed);
+                            loads through registers, one CTA per tile and z-chunk */
+  ST_VARIANT_PIPE = 3    /* the same wavefront with TMA-fed shared-memory rings: a producer warp
+                            streams planes and coefficient fields ahead with cp.async.bulk.tensor +
+                            mbarriers; persistent CTAs.  The default. */
 };
 
 /* Device allocator: return a device pointer to >= bytes (256-byte aligned) or NULL. */
@@ -83,7 +87,8 @@ typedef struct {
   int device;          /* CUDA ordinal; -1 = the current device */
   int variant;         /* ST_VARIANT_*; 0 = auto */
   int bt;              /* time-block depth (levels fused per launch); 0 = auto; >= 1 otherwise */
-  int tile_x, tile_y;  /* reserved for tile overrides; 0 = auto */
+  int tile_cfg;        /* kernel tile configuration index of the variant (0 = default) */
+  int reserved;        /* must be 0 */
   int zchunk;          /* planes per CTA z-chunk; 0 = auto */
   int rank, nranks;    /* z-slab decomposition over nranks processes (one GPU each); 1 = single */
   const void *nccl_id; /* nranks > 1: 128-byte ncclUniqueId made by rank 0 (stencil_nccl_unique_id)

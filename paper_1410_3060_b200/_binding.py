@@ -15,7 +15,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libstencil.so")
 
 ST_7PT_CONST, ST_7PT_VAR, ST_25PT_WAVE, ST_25PT_VAR = 1, 2, 3, 4
-ST_VARIANT_AUTO, ST_VARIANT_NAIVE, ST_VARIANT_STREAM = 0, 1, 2
+ST_VARIANT_AUTO, ST_VARIANT_NAIVE, ST_VARIANT_STREAM, ST_VARIANT_PIPE = 0, 1, 2, 3
 ST_OK, ST_E_INVAL, ST_E_NOMEM, ST_E_CUDA, ST_E_NCCL, ST_E_STATE = 0, -1, -2, -3, -4, -5
 RADIUS = {1: 1, 2: 1, 3: 4, 4: 4}
 N_COEFF = {1: 2, 2: 7, 3: 6, 4: 13}
@@ -33,7 +33,7 @@ FREE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void
 
 class StOpts(ctypes.Structure):
     _fields_ = [("device", ctypes.c_int), ("variant", ctypes.c_int), ("bt", ctypes.c_int),
-                ("tile_x", ctypes.c_int), ("tile_y", ctypes.c_int), ("zchunk", ctypes.c_int),
+                ("tile_cfg", ctypes.c_int), ("reserved", ctypes.c_int), ("zchunk", ctypes.c_int),
                 ("rank", ctypes.c_int), ("nranks", ctypes.c_int), ("nccl_id", ctypes.c_void_p),
                 ("stream", ctypes.c_void_p), ("alloc", ALLOC_FN), ("free", FREE_FN),
                 ("alloc_user", ctypes.c_void_p)]
@@ -251,14 +251,14 @@ class Grid:
     """
 
     def __init__(self, kind, nx, ny, nz, *, seed=None, scalars=None, v0=None, u0=None, coeff=None,
-                 variant=ST_VARIANT_AUTO, bt=0, zchunk=0, rank=0, nranks=1, nccl_id=None,
+                 variant=ST_VARIANT_AUTO, bt=0, zchunk=0, tile_cfg=0, rank=0, nranks=1, nccl_id=None,
                  device=None, stream=None, torch_memory=True):
         import torch
         self.kind, self.nx, self.ny, self.nz = kind, nx, ny, nz
         self.R = RADIUS[kind]
         o = stencil_opts_default()
         o.device = torch.cuda.current_device() if device is None else device
-        o.variant, o.bt, o.zchunk = variant, bt, zchunk
+        o.variant, o.bt, o.zchunk, o.tile_cfg = variant, bt, zchunk, tile_cfg
         o.rank, o.nranks = rank, nranks
         self._id = None
         if nranks > 1:

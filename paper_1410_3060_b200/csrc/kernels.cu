@@ -22,28 +22,6 @@
 
 namespace st {
 
-template <int KIND, int R>
-__device__ __forceinline__ double apply_point(double c, double u, const double (&m)[3][R],
-                                              const double (&pl)[3][R], const double* W,
-                                              const KParams& p) {
-  if constexpr (KIND == K7C) {
-    return point_7c(c, m, pl, p.s[0], p.s[1]);
-  } else if constexpr (KIND == K7V) {
-    double w[7];
-#pragma unroll
-    for (int i = 0; i < 7; ++i) w[i] = W[i];
-    return point_7v(c, m, pl, w);
-  } else if constexpr (KIND == K25V) {
-    double w[13];
-#pragma unroll
-    for (int i = 0; i < 13; ++i) w[i] = W[i];
-    return point_25v(c, m, pl, w);
-  } else {
-    const double s[6] = {p.s[0], p.s[1], p.s[2], p.s[3], p.s[4], p.s[5]};
-    return point_25w(c, u, m, pl, s);
-  }
-}
-
 // ------------------------------------------------------------------------------------------------
 // naive: one thread per interior point of planes [zo0, zo1), one time step.
 template <int KIND>
@@ -68,7 +46,7 @@ __global__ void __launch_bounds__(256) naive_kernel(const KParams p) {
 #pragma unroll
   for (int k = 0; k < NC; ++k) W[k] = p.coef[k * p.cstride + i];
   const double u = Traits<KIND>::WAVE ? p.srcu[i] : 0.0;
-  p.dst[i] = apply_point<KIND, R>(p.src[i], u, m, pl, W, p);
+  p.dst[i] = apply_point<KIND, R>(p.src[i], u, m, pl, W, p.s);
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -191,7 +169,7 @@ __global__ void __launch_bounds__(FX * FYT) stream_kernel(const KParams p) {
           }
           double u = 0.0;
           if constexpr (WAVE) u = (k == 1) ? uq[j][0] : ring[k >= 2 ? k - 2 : 0][j][0];
-          v = apply_point<KIND, R>(ring[k - 1][j][R], u, m, pl, W, p);
+          v = apply_point<KIND, R>(ring[k - 1][j][R], u, m, pl, W, p.s);
         }
         if (k < BT) {
 #pragma unroll

@@ -22,6 +22,12 @@ struct KParams {
   int zo0, zo1;        // local planes this launch writes at the last level: [zo0, zo1)
   int zchunk;          // output planes per CTA along z (grid.z = ceil((zo1 - zo0) / zchunk))
   double s[6];         // scalar weights (7c: w1, w2; wave: w0, w1..w4, alpha)
+  // TMA-pipelined kernel only: 16-byte-aligned allocation bases (element (z, y, x) of a padded array
+  // is raw[z*plane + y*pitch + x + xoff]) for the tensor maps.
+  const double* src_raw;
+  const double* srcu_raw;
+  const double* coef_raw;
+  int xoff;
 };
 
 struct LaunchInfo {
@@ -40,6 +46,14 @@ cudaError_t launch_naive(int kind, const KParams& p, cudaStream_t stream, Launch
 cudaError_t launch_stream(int kind, int b, const KParams& p, int zchunk_req, int num_sms,
                           cudaStream_t stream, LaunchInfo* info);
 int max_stream_bt(int kind);
+
+// b fused levels of the TMA-pipelined, warp-specialised z-streaming kernel (ST_VARIANT_PIPE):
+// a producer warp streams planes of Omega^t and the coefficient fields into shared-memory rings
+// with cp.async.bulk.tensor + mbarriers; consumer warps run the same wavefront as stream_kernel.
+// cfg selects a tile configuration (0 = default for the kind and b).  Persistent: one CTA per SM.
+cudaError_t launch_pipe(int kind, int b, const KParams& p, int zchunk_req, int num_sms, int cfg,
+                        cudaStream_t stream, LaunchInfo* info);
+int max_pipe_bt(int kind);
 
 // Seeded fill of the local planes of one array (synth/synth.h).  mode 0: U[-1,1) from `stream`
 // everywhere; mode 1: U[-1,1), interior cells from stream 1 and the rest from stream 0 (wave

@@ -67,4 +67,28 @@ __device__ __forceinline__ double point_25w(double c, double u, const double (&m
   return __fma_rn(s[5], L, __dsub_rn(__dmul_rn(2.0, c), u));
 }
 
+// Dispatch on the kind; W = the coefficient values at the point (variable kinds), u = O^{t-1} (wave),
+// ps = scalar weights.
+template <int KIND, int R>
+__device__ __forceinline__ double apply_point(double c, double u, const double (&m)[3][R],
+                                              const double (&pl)[3][R], const double* W,
+                                              const double (&ps)[6]) {
+  if constexpr (KIND == K7C) {
+    return point_7c(c, m, pl, ps[0], ps[1]);
+  } else if constexpr (KIND == K7V) {
+    double w[7];
+#pragma unroll
+    for (int i = 0; i < 7; ++i) w[i] = W[i];
+    return point_7v(c, m, pl, w);
+  } else if constexpr (KIND == K25V) {
+    double w[13];
+#pragma unroll
+    for (int i = 0; i < 13; ++i) w[i] = W[i];
+    return point_25v(c, m, pl, w);
+  } else {
+    const double s[6] = {ps[0], ps[1], ps[2], ps[3], ps[4], ps[5]};
+    return point_25w(c, u, m, pl, s);
+  }
+}
+
 }  // namespace st

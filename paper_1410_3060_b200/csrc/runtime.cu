@@ -83,7 +83,7 @@ struct stencil_ctx {
   int64_t nx = 0, ny = 0, nz = 0;
   int rank = 0, nranks = 1;
   int device = 0, num_sms = 148;
-  int variant = ST_VARIANT_STREAM, bt = 1, zchunk_req = 0;
+  int variant = ST_VARIANT_PIPE, bt = 1, zchunk_req = 0, tile_cfg = 0;
   cudaStream_t stream = nullptr;
   st_alloc_fn alloc = nullptr;
   st_free_fn free_fn = nullptr;
@@ -222,8 +222,9 @@ int create_common(stencil_ctx** out, int kind, int64_t nx, int64_t ny, int64_t n
   if (R < 0) { set_err("bad kind %d", kind); return ST_E_INVAL; }
   if (nx < 1 || ny < 1 || nz < 1) { set_err("extents must be >= 1 (got %lld %lld %lld)", (long long)nx, (long long)ny, (long long)nz); return ST_E_INVAL; }
   if (nx > (1 << 30) || ny > (1 << 30)) { set_err("extent too large"); return ST_E_INVAL; }
-  if (o.bt < 0 || o.variant < 0 || o.variant > ST_VARIANT_STREAM || o.zchunk < 0) {
-    set_err("bad options (bt=%d variant=%d zchunk=%d)", o.bt, o.variant, o.zchunk);
+  if (o.bt < 0 || o.variant < 0 || o.variant > ST_VARIANT_PIPE || o.zchunk < 0 || o.tile_cfg < 0 ||
+      o.reserved != 0) {
+    set_err("bad options (bt=%d variant=%d zchunk=%d tile_cfg=%d)", o.bt, o.variant, o.zchunk, o.tile_cfg);
     return ST_E_INVAL;
   }
   if (o.nranks < 1 || o.rank < 0 || o.rank >= o.nranks) { set_err("bad rank %d of %d", o.rank, o.nranks); return ST_E_INVAL; }
@@ -251,12 +252,15 @@ int create_common(stencil_ctx** out, int kind, int64_t nx, int64_t ny, int64_t n
   h->stream = (cudaStream_t)o.stream;
   h->alloc = o.alloc; h->free_fn = o.free; h->alloc_user = o.alloc_user;
   h->zchunk_req = o.zchunk;
+  h->tile_cfg = o.tile_cfg;
   CK(cudaSetDevice(dev), "cudaSetDevice");
   CK(cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, dev), "device attribute");
 
-  h->variant = o.variant == ST_VARIANT_AUTO ? ST_VARIANT_STREAM : o.variant;
+  h->variant = o.variant == ST_VARIANT_AUTO ? ST_VARIANT_PIPE : o.variant;
   int bt = h->variant == ST_VARIANT_NAIVE ? 1 : (o.bt ? o.bt : default_bt(kind));
-  bt = std::min(bt, std::max(1, st::max_stream_bt(kind)));
+  const int bt_cap = h->variant == ST_VARIANT_PIPE ? st::max_pipe_bt(kind)
+                   : h->variant == ST_VARIANT_STREAM ? st::max_stream_bt(kind) : 1;
+  bt = std::min(bt, std::max(1, bt_cap));
   int bt_eff = 1;
   int rc = plan_slab(nz, R, o.nranks, o.rank, bt, &h->own_z0, &h->own_z1, &h->store_z0, &h->store_z1,
                      &bt_eff, &h->slab_lo, &h->slab_hi);
@@ -387,6 +391,10 @@ int run_block(stencil_ctx* h, int b) {
   st::KParams p = base_params(h);
   const bool wave = h->kind == ST_25PT_WAVE;
   int new0, new1;
+  p.src_raw = h->buf[h->lv0];
+  p.srcu_raw = h->buf[h->lv1];
+  p.coef_raw = h->coef;
+  p.xoff = (int)h->xoff;
   if (!wave) {
     p.src = h->at(h->lv0);
     p.dst = h->at(h->lv1);
@@ -414,8 +422,10 @@ int run_block(stencil_ctx* h, int b) {
   cudaError_t e;
   if (h->variant == ST_VARIANT_NAIVE)
     e = st::launch_naive(h->kind, p, h->stream, &h->last_launch);
-  else
+  else if (h->variant == ST_VARIANT_STREAM)
     e = st::launch_stream(h->kind, b, p, h->zchunk_req, h->num_sms, h->stream, &h->last_launch);
+  else
+    e = st::launch_pipe(h->kind, b, p, h->zchunk_req, h->num_sms, h->tile_cfg, h->stream, &h->last_launch);
   if (ev_begin) cudaEventRecord(ev_end, h->stream);
   if (e != cudaSuccess) return cuda_fail(h, e, "kernel launch");
   h->launches++;

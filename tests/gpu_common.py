@@ -13,15 +13,16 @@ def interior(R):
 
 
 def gpu_run(kind, nx, ny, nz, T, seed=synth.DEFAULT_SEED, variant=0, bt=0, zchunk=0, inputs=None,
-            scalars=None):
+            scalars=None, tile_cfg=0):
     """Run the CUDA path; returns (Omega^T, Omega^{T-1} or None, info)."""
     if inputs is None:
-        g = st.Grid(kind, nx, ny, nz, seed=seed, scalars=scalars, variant=variant, bt=bt, zchunk=zchunk)
+        g = st.Grid(kind, nx, ny, nz, seed=seed, scalars=scalars, variant=variant, bt=bt, zchunk=zchunk,
+                    tile_cfg=tile_cfg)
     else:
         coeff = inputs.coef if inputs.coef else list(inputs.scalars)
         u0 = inputs.U if kind == WAVE else None
         g = st.Grid(kind, nx, ny, nz, v0=inputs.V, u0=u0, coeff=coeff, variant=variant, bt=bt,
-                    zchunk=zchunk)
+                    zchunk=zchunk, tile_cfg=tile_cfg)
     with g:
         if T > 0:
             g.run(T)

@@ -18,8 +18,13 @@ SHAPES = {synth.K7C: (61, 70, 45), synth.K7V: (61, 70, 45), synth.K25W: (130, 37
           synth.K25V: (130, 37, 41)}
 
 
-def max_bt(kind):
-    return {synth.K7C: 6, synth.K7V: 4, synth.K25W: 1, synth.K25V: 1}[kind]
+def max_bt(kind, variant=st.ST_VARIANT_PIPE):
+    if variant == st.ST_VARIANT_STREAM:
+        return {synth.K7C: 6, synth.K7V: 4, synth.K25W: 1, synth.K25V: 1}[kind]
+    return {synth.K7C: 8, synth.K7V: 3, synth.K25W: 1, synth.K25V: 1}[kind]
+
+
+N_CFG = {synth.K7C: 1, synth.K7V: 2, synth.K25W: 2, synth.K25V: 1}  # pipe tile configurations
 
 
 @pytest.mark.parametrize("kind", KINDS)
@@ -88,16 +93,20 @@ def test_shadow_scaled_per_cell(kind):
 
 @pytest.mark.parametrize("kind", KINDS)
 def test_variants_bitwise_identical(kind):
-    """G4: naive == streaming (every bt, several z-chunks) bitwise."""
+    """G4: naive == streaming == TMA-pipelined (every bt, tile configs, several z-chunks) bitwise."""
     nx, ny, nz = SHAPES[kind]
     T = 7
     ref = gpu_run(kind, nx, ny, nz, T, seed=9, variant=st.ST_VARIANT_NAIVE)
-    for bt in range(1, max_bt(kind) + 1):
-        for zchunk in (0, 5, 1000):
-            got = gpu_run(kind, nx, ny, nz, T, seed=9, variant=st.ST_VARIANT_STREAM, bt=bt, zchunk=zchunk)
-            assert np.array_equal(got[0], ref[0]), (bt, zchunk)
-            if kind == WAVE:
-                assert np.array_equal(got[1], ref[1]), (bt, zchunk)
+    plans = [(st.ST_VARIANT_STREAM, bt, zc, 0) for bt in range(1, max_bt(kind, st.ST_VARIANT_STREAM) + 1)
+             for zc in (0, 5, 1000)]
+    plans += [(st.ST_VARIANT_PIPE, bt, zc, cfg) for bt in range(1, max_bt(kind) + 1) for zc in (0, 5, 1000)
+              for cfg in range(N_CFG[kind])]
+    for variant, bt, zchunk, cfg in plans:
+        got = gpu_run(kind, nx, ny, nz, T, seed=9, variant=variant, bt=bt, zchunk=zchunk, tile_cfg=cfg)
+        assert got[2]["bt"] == bt
+        assert np.array_equal(got[0], ref[0]), (variant, bt, zchunk, cfg)
+        if kind == WAVE:
+            assert np.array_equal(got[1], ref[1]), (variant, bt, zchunk, cfg)
 
 
 @pytest.mark.parametrize("kind", KINDS)
@@ -110,8 +119,9 @@ def test_degenerate_extents(kind):
         inp = synth.make_inputs(kind, nx, ny, nz, seed=4)
         T = 5
         o_new, o_old = oracle.run(inp, T)
-        for bt in sorted({1, max_bt(kind)}):
-            g_new, g_old, _ = gpu_run(kind, nx, ny, nz, T, seed=4, bt=bt)
+        for variant, bt in sorted({(st.ST_VARIANT_PIPE, 1), (st.ST_VARIANT_PIPE, max_bt(kind)),
+                                   (st.ST_VARIANT_STREAM, max_bt(kind, st.ST_VARIANT_STREAM))}):
+            g_new, g_old, _ = gpu_run(kind, nx, ny, nz, T, seed=4, bt=bt, variant=variant)
             assert_parity(kind, g_new, g_old, o_new, o_old, inp.R, 1e-13, inputs=inp)
 
 
