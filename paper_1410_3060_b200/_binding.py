@@ -236,7 +236,10 @@ def _torch_allocator():
                 return None
 
         def _free(ptr, nbytes, stream, user):
-            torch.cuda.caching_allocator_delete(ptr)
+            try:
+                torch.cuda.caching_allocator_delete(ptr)
+            except Exception:  # interpreter shutdown or a dead context: nothing left to free
+                pass
 
         _torch_alloc_cb = ALLOC_FN(_alloc)
         _torch_free_cb = FREE_FN(_free)

@@ -27,6 +27,8 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
+#include <cstring>
 #include <mutex>
 
 namespace st {
@@ -81,14 +83,16 @@ struct Item {
   int gx0, gy0, zc0, zc1, s_begin, s_end;
 };
 
-template <int R, int BT, int OX, int OY>
+// Item origin = the level-1 extent origin: output origin minus R*H (H = BT - 1 halo levels).
+template <int R, int H, int OX, int OY>
 __device__ __forceinline__ Item decode(int item, int ntx, int nty, const KParams& p) {
+  constexpr int BT = H + 1;
   const int per = ntx * nty;
   const int zc = item / per, t = item - zc * per;
   const int ty = t / ntx, tx = t - ty * ntx;
   Item it;
-  it.gx0 = tx * OX + R - R * BT;
-  it.gy0 = ty * OY + R - R * BT;
+  it.gx0 = tx * OX + R - R * H;
+  it.gy0 = ty * OY + R - R * H;
   it.zc0 = p.zo0 + zc * p.zchunk;
   it.zc1 = min(p.zo1, it.zc0 + p.zchunk);
   it.s_begin = max(0, it.zc0 - BT * R);
@@ -98,48 +102,57 @@ __device__ __forceinline__ Item decode(int item, int ntx, int nty, const KParams
 
 }  // namespace
 
-// FX x FY footprint, consumer threads own CY-cell vertical strips; DV / DC = ring depths.
-template <int KIND, int BT, int FX, int FY, int CY, int DV, int DC>
+// Consumer threads cover the level-1 extent E1 = TX x TY of a tile (TX threads per row, TY/CY strips
+// of CY cells each): every consumer cell is computed at level 1, and the level-BT output tile is
+// OX x OY = (TX - 2R(BT-1)) x (TY - 2R(BT-1)).  The Omega^t box (footprint) is E1 grown by R on each
+// side; the coefficient (or wave U) box is E1 itself.  DV / DC = ring depths (planes).
+template <int KIND, int BT, int TX, int TY, int CY, int DV, int DC>
 struct PipeCfg {
   using TR = Traits<KIND>;
   static constexpr int R = TR::R, NC = TR::NCOEF, RL = 2 * R + 1;
   static constexpr bool WAVE = TR::WAVE;
-  static constexpr int NS = FY / CY;
-  static constexpr int NCONS = FX * NS;
+  static constexpr int NS = TY / CY;
+  static constexpr int NCONS = TX * NS;
   static constexpr int THREADS = NCONS + 32;
-  static constexpr int EX = FX - 2 * R, EY = FY - 2 * R;
-  static constexpr int OX = FX - 2 * R * BT, OY = FY - 2 * R * BT;
+  static constexpr int FX = TX + 2 * R, FY = TY + 2 * R;         // Omega^t footprint
+  static constexpr int OX = TX - 2 * R * (BT - 1), OY = TY - 2 * R * (BT - 1);
   static constexpr int NCF = WAVE ? 1 : NC;  // fields in the C ring (coefficients, or U for the wave)
   static constexpr bool HAS_C = NCF > 0;
-  static constexpr int VELEMS = FX * FY, CELEMS = EX * EY * NCF;
-  static constexpr int CSLOT = (CELEMS + 15) / 16 * 16;  // C-ring slot stride: 128-byte aligned
-  static constexpr int NPL = BT - 1;  // shared level planes (double-buffered)
-  static constexpr size_t SMEM = sizeof(double) * ((size_t)DV * VELEMS + (HAS_C ? (size_t)DC * CSLOT : 0) +
-                                                   (size_t)NPL * 2 * VELEMS) +
+  // TMA boxes start on an even fp64 column (tiled TMA needs 16-byte aligned x coordinates), so the
+  // boxes are 2 columns wider than the data and the data sit at a per-item shift of 0 or 1.
+  static constexpr int FXB = FX + 2, EXB = TX + 2;
+  static constexpr int VELEMS = FXB * FY, CFIELD = EXB * TY, CELEMS = CFIELD * NCF;
+  static constexpr int VSLOT = (VELEMS + 15) / 16 * 16;  // ring slot strides: TMA destinations
+  static constexpr int CSLOT = (CELEMS + 15) / 16 * 16;  // must be 128-byte aligned
+  static constexpr int PELEMS = TX * TY;                  // one level plane (levels 1..BT-1)
+  static constexpr int NPL = BT - 1;                      // shared level planes (double-buffered)
+  static constexpr size_t SMEM = sizeof(double) * ((size_t)DV * VSLOT + (HAS_C ? (size_t)DC * CSLOT : 0) +
+                                                   (size_t)NPL * 2 * PELEMS) +
                                  sizeof(uint64_t) * 2 * (DV + DC) + 128;
-  static_assert(FY % CY == 0, "strips");
-  static_assert(OX > 0 && OY > 0, "footprint too small for BT");
+  static_assert(TY % CY == 0, "strips");
+  static_assert(OX > 0 && OY > 0, "tile too small for BT");
   static_assert(NCONS % 32 == 0, "whole consumer warps");
   static_assert(DV >= R + 2, "V ring too shallow");
   static_assert(!HAS_C || DC >= (WAVE ? 0 : (BT - 1) * R) + 2, "C ring too shallow");
-  static_assert((EX * 8) % 16 == 0 && (FX * 8) % 16 == 0, "TMA box rows must be 16-byte multiples");
+  static_assert((EXB * 8) % 16 == 0 && (FXB * 8) % 16 == 0, "TMA box rows must be 16-byte multiples");
+  static_assert(FXB <= 256 && FY <= 256 && EXB <= 256, "TMA box dimension limit");
 };
 
-template <int KIND, int BT, int FX, int FY, int CY, int DV, int DC>
-__global__ void __launch_bounds__(PipeCfg<KIND, BT, FX, FY, CY, DV, DC>::THREADS, 1)
+template <int KIND, int BT, int TX, int TY, int CY, int DV, int DC>
+__global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CY, DV, DC>::THREADS, 1)
     pipe_kernel(const __grid_constant__ CUtensorMap mapV, const __grid_constant__ CUtensorMap mapC,
                 const KParams p, int ntx, int nty, int items) {
-  using C = PipeCfg<KIND, BT, FX, FY, CY, DV, DC>;
-  constexpr int R = C::R, NC = C::NC, RL = C::RL, EX = C::EX, NCONS = C::NCONS;
+  using C = PipeCfg<KIND, BT, TX, TY, CY, DV, DC>;
+  constexpr int R = C::R, NC = C::NC, RL = C::RL, NCONS = C::NCONS, FXB = C::FXB, EXB = C::EXB;
   constexpr bool WAVE = C::WAVE, HAS_C = C::HAS_C;
   constexpr int OX = C::OX, OY = C::OY;
   constexpr int CLAG = WAVE ? 0 : (BT - 1) * R;  // steps a C-ring plane stays in use
 
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double* sV = reinterpret_cast<double*>(smem_raw);
-  double* sC = sV + (size_t)DV * C::VELEMS;
+  double* sC = sV + (size_t)DV * C::VSLOT;
   double* sP = sC + (HAS_C ? (size_t)DC * C::CSLOT : 0);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + (size_t)C::NPL * 2 * C::VELEMS);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + (size_t)C::NPL * 2 * C::PELEMS);
   uint64_t* fullV = bars;
   uint64_t* emptyV = bars + DV;
   uint64_t* fullC = bars + 2 * DV;
@@ -160,20 +173,22 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, FX, FY, CY, DV, DC>::THREADS
       if (HAS_C) asm volatile("prefetch.tensormap [%0];" ::"l"(&mapC) : "memory");
       uint32_t iv = 0;
       for (int item = blockIdx.x; item < items; item += gridDim.x) {
-        const Item it = decode<R, BT, OX, OY>(item, ntx, nty, p);
+        const Item it = decode<R, BT - 1, OX, OY>(item, ntx, nty, p);
+        const int xv = (it.gx0 - R + p.xoff) & ~1;  // footprint box
+        const int xc = (it.gx0 + p.xoff) & ~1;      // level-1 extent box
         for (int s = it.s_begin; s <= it.s_end; ++s, ++iv) {
           const uint32_t sv = iv % DV, nv = iv / DV;
           mbar_wait(&emptyV[sv], (nv & 1) ^ 1);
           mbar_expect_tx(&fullV[sv], C::VELEMS * sizeof(double));
-          tma_load_3d(sV + (size_t)sv * C::VELEMS, &mapV, &fullV[sv], it.gx0 + p.xoff, it.gy0, s);
+          tma_load_3d(sV + (size_t)sv * C::VSLOT, &mapV, &fullV[sv], xv, it.gy0 - R, s);
           if constexpr (HAS_C) {
             const uint32_t sc = iv % DC, nc = iv / DC;
             mbar_wait(&emptyC[sc], (nc & 1) ^ 1);
             mbar_expect_tx(&fullC[sc], C::CELEMS * sizeof(double));
             if constexpr (WAVE)
-              tma_load_3d(sC + (size_t)sc * C::CSLOT, &mapC, &fullC[sc], it.gx0 + R + p.xoff, it.gy0 + R, s - R);
+              tma_load_3d(sC + (size_t)sc * C::CSLOT, &mapC, &fullC[sc], xc, it.gy0, s - R);
             else
-              tma_load_4d(sC + (size_t)sc * C::CSLOT, &mapC, &fullC[sc], it.gx0 + R + p.xoff, it.gy0 + R, s - R, 0);
+              tma_load_4d(sC + (size_t)sc * C::CSLOT, &mapC, &fullC[sc], xc, it.gy0, s - R, 0);
           }
         }
       }
@@ -182,17 +197,18 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, FX, FY, CY, DV, DC>::THREADS
   }
 
   // ---------------------------------------------------------------- consumers
-  const int lx = tid % FX;
-  const int ly0 = (tid / FX) * CY;
+  const int lx = tid % TX;           // column in the level-1 extent
+  const int ly0 = (tid / TX) * CY;   // first row of this thread's strip
   const int lane = tid & 31;
-  const int X = p.nx + 2 * R, Y = p.ny + 2 * R;
-  (void)X; (void)Y;
   uint32_t iv = 0;
 
   for (int item = blockIdx.x; item < items; item += gridDim.x) {
-    const Item it = decode<R, BT, OX, OY>(item, ntx, nty, p);
+    const Item it = decode<R, BT - 1, OX, OY>(item, ntx, nty, p);
     const int gx = it.gx0 + lx;
     const bool xin = gx >= R && gx < p.nx + R;
+    const int shv = (it.gx0 - R + p.xoff) & 1;  // column shift of the footprint boxes
+    const int shc = (it.gx0 + p.xoff) & 1;      // column shift of the C boxes
+    const int lxv = lx + R + shv;               // this column inside a footprint box row
     bool inter[CY], outc[CY];
     unsigned lvl[CY];
     long long col[CY];
@@ -203,7 +219,8 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, FX, FY, CY, DV, DC>::THREADS
       lvl[j] = 0;
 #pragma unroll
       for (int k = 1; k <= BT; ++k)
-        if (lx >= k * R && lx < FX - k * R && ly >= k * R && ly < FY - k * R) lvl[j] |= 1u << k;
+        if (lx >= (k - 1) * R && lx < TX - (k - 1) * R && ly >= (k - 1) * R && ly < TY - (k - 1) * R)
+          lvl[j] |= 1u << k;
       outc[j] = inter[j] && ((lvl[j] >> BT) & 1u);
       col[j] = (long long)gy * p.pitch + gx;
     }
@@ -221,10 +238,10 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, FX, FY, CY, DV, DC>::THREADS
       // Level 0: plane s of Omega^t -> register rings.
       const uint32_t sv = iv % DV;
       mbar_wait(&fullV[sv], (iv / DV) & 1);
-      const double* Vs = sV + (size_t)sv * C::VELEMS;
+      const double* Vs = sV + (size_t)sv * C::VSLOT;
 #pragma unroll
       for (int j = 0; j < CY; ++j) {
-        const double v = Vs[(ly0 + j) * FX + lx];
+        const double v = Vs[(ly0 + j + R) * FXB + lxv];
 #pragma unroll
         for (int i = 0; i < RL - 1; ++i) ring[0][j][i] = ring[0][j][i + 1];
         ring[0][j][RL - 1] = v;
@@ -234,15 +251,22 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, FX, FY, CY, DV, DC>::THREADS
 #pragma unroll
       for (int k = 1; k <= BT; ++k) {
         const int c = s - k * R;
+        // x/y neighbour source: level 1 reads the footprint box of plane s - R (row stride FXB,
+        // cell (lx, ly) at [(ly + R) * FXB + lxv]); level k >= 2 a shared level plane (TX x TY).
         const double* Src;
+        int stride, base;
         if (k == 1) {
-          Src = sV + (size_t)((iv - R) % DV) * C::VELEMS;
+          Src = sV + (size_t)((iv - R) % DV) * C::VSLOT;
+          stride = FXB;
+          base = R * FXB + lxv;
         } else {
-          double* P = sP + (size_t)((k - 2) * 2 + buf) * C::VELEMS;
+          double* P = sP + (size_t)((k - 2) * 2 + buf) * C::PELEMS;
 #pragma unroll
-          for (int j = 0; j < CY; ++j) P[(ly0 + j) * FX + lx] = ring[k - 1][j][R];
+          for (int j = 0; j < CY; ++j) P[(ly0 + j) * TX + lx] = ring[k - 1][j][R];
           named_sync(1, NCONS);
           Src = P;
+          stride = TX;
+          base = lx;
         }
         // planes below s_begin + k*R are not valid at level k (unless the stream starts at plane 0)
         const bool zv = c >= p.zi0 && c < p.zi1 && (it.s_begin == 0 || c >= it.s_begin + k * R);
@@ -251,8 +275,9 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, FX, FY, CY, DV, DC>::THREADS
         if (zv) {
 #pragma unroll
           for (int i = 0; i < CY + 2 * R; ++i) {
-            const int row = min(max(ly0 - R + i, 0), FY - 1);
-            ys[i] = Src[row * FX + lx];
+            int row = ly0 - R + i;
+            if (k > 1) row = min(max(row, 0), TY - 1);  // level planes have no halo rows
+            ys[i] = Src[row * stride + base];
           }
         }
 #pragma unroll
@@ -261,7 +286,7 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, FX, FY, CY, DV, DC>::THREADS
           if (zv && inter[j] && ((lvl[j] >> k) & 1u)) {
             const int ly = ly0 + j;
             double m[3][R], pl[3][R];
-            const double* row = Src + ly * FX + lx;
+            const double* row = Src + ly * stride + base;
 #pragma unroll
             for (int r = 1; r <= R; ++r) {
               m[0][r - 1] = row[-r];
@@ -271,11 +296,11 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, FX, FY, CY, DV, DC>::THREADS
               m[2][r - 1] = ring[k - 1][j][R - r];
               pl[2][r - 1] = ring[k - 1][j][R + r];
             }
-            const int ci = (ly - R) * EX + (lx - R);
+            const int ci = ly * EXB + lx + shc;
             double W[NC > 0 ? NC : 1];
             if constexpr (NC > 0) {
 #pragma unroll
-              for (int f = 0; f < NC; ++f) W[f] = Ck[f * (C::CELEMS / C::NCF) + ci];
+              for (int f = 0; f < NC; ++f) W[f] = Ck[f * C::CFIELD + ci];
             }
             double u = 0.0;
             if constexpr (WAVE) u = (k == 1) ? Ck[ci] : ring[k >= 2 ? k - 2 : 0][j][0];
@@ -291,7 +316,7 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, FX, FY, CY, DV, DC>::THREADS
             if constexpr (WAVE && BT >= 2) __stcs(p.dstu + o, ring[BT - 1][j][R]);
           }
         }
-        if (k == 1 && iv >= iv_b + R) {  // V plane of step iv - R fully consumed
+        if (k == 1 && iv >= iv_b + R) {  // footprint plane of step iv - R fully consumed
           __syncwarp();
           if (lane == 0) mbar_arrive(&emptyV[(iv - R) % DV]);
         }
@@ -336,16 +361,24 @@ bool make_map(CUtensorMap* m, const double* base, int rank, long long pitch, lon
   cuuint64_t strides[3] = {(cuuint64_t)pitch * 8, (cuuint64_t)plane * 8, (cuuint64_t)fstride * 8};
   cuuint32_t box[4] = {(cuuint32_t)bx, (cuuint32_t)by, 1, (cuuint32_t)bf};
   cuuint32_t es[4] = {1, 1, 1, 1};
+  // L2 promotion: experiment knob STENCIL_TMA_PROMO = 0 (none), 1 (64B), 2 (128B), 3 (256B)
+  static int promo = [] {
+    const char* e = getenv("STENCIL_TMA_PROMO");
+    return e ? atoi(e) : 0;
+  }();
+  const CUtensorMapL2promotion pr = promo == 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                                   : promo == 2 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                                   : promo == 3 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+                                                : CU_TENSOR_MAP_L2_PROMOTION_NONE;
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, rank, const_cast<double*>(base), dims, strides, box, es,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, pr, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
 
-template <int KIND, int BT, int FX, int FY, int CY, int DV, int DC>
+template <int KIND, int BT, int TX, int TY, int CY, int DV, int DC>
 cudaError_t run_pipe(const KParams& p0, int zchunk_req, int num_sms, cudaStream_t stream, LaunchInfo* info) {
-  using C = PipeCfg<KIND, BT, FX, FY, CY, DV, DC>;
-  auto kern = pipe_kernel<KIND, BT, FX, FY, CY, DV, DC>;
+  using C = PipeCfg<KIND, BT, TX, TY, CY, DV, DC>;
+  auto kern = pipe_kernel<KIND, BT, TX, TY, CY, DV, DC>;
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
@@ -359,24 +392,30 @@ cudaError_t run_pipe(const KParams& p0, int zchunk_req, int num_sms, cudaStream_
   const long long tiles = (long long)ntx * nty;
   int zchunk = zchunk_req;
   if (zchunk <= 0) {
-    // >= ~8 work items per CTA for load balance, chunks >= 12x the 2*BT*R fill/drain planes
     int occ0 = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ0, kern, C::THREADS, C::SMEM);
-    const long long chunks = std::max<long long>(1, (8LL * std::max(1, occ0) * num_sms + tiles - 1) / tiles);
-    zchunk = (int)((planes + chunks - 1) / chunks);
-    zchunk = std::max(zchunk, std::min(planes, 24 * BT * C::R));
+    const long long slots = (long long)std::max(1, occ0) * num_sms;
+    const int min_chunk = 24 * BT * C::R;  // keeps the 2*BT*R fill/drain planes of a chunk < ~8 %
+    if (tiles * ((planes + min_chunk - 1) / min_chunk) >= 2 * slots) {
+      // large grid: ~8 work items per CTA for load balance, chunks >= min_chunk planes
+      const long long chunks = std::max<long long>(1, (8 * slots + tiles - 1) / tiles);
+      zchunk = std::max((int)((planes + chunks - 1) / chunks), std::min(planes, min_chunk));
+    } else {
+      // small grid (latency-bound): about one work item per CTA slot
+      zchunk = (int)std::max<long long>(2, (planes * tiles + slots - 1) / slots);
+    }
   }
   p.zchunk = zchunk;
   const int nzc = (planes + zchunk - 1) / zchunk;
   const long long items = tiles * nzc;
   CUtensorMap mapV, mapC;
   memset(&mapC, 0, sizeof mapC);
-  if (!make_map(&mapV, p.src_raw, 3, p.pitch, p.ny + 2 * C::R, p.zl, 1, p.plane, 0, FX, FY, 1))
+  if (!make_map(&mapV, p.src_raw, 3, p.pitch, p.ny + 2 * C::R, p.zl, 1, p.plane, 0, C::FXB, C::FY, 1))
     return cudaErrorInvalidValue;
   if (C::HAS_C) {
-    bool ok = C::WAVE ? make_map(&mapC, p.srcu_raw, 3, p.pitch, p.ny + 2 * C::R, p.zl, 1, p.plane, 0, C::EX, C::EY, 1)
+    bool ok = C::WAVE ? make_map(&mapC, p.srcu_raw, 3, p.pitch, p.ny + 2 * C::R, p.zl, 1, p.plane, 0, C::EXB, TY, 1)
                       : make_map(&mapC, p.coef_raw, 4, p.pitch, p.ny + 2 * C::R, p.zl, C::NC, p.plane, p.cstride,
-                                 C::EX, C::EY, C::NC);
+                                 C::EXB, TY, C::NC);
     if (!ok) return cudaErrorInvalidValue;
   }
   int occ = 1;
@@ -402,11 +441,13 @@ int max_pipe_bt(int kind) {
   }
 }
 
-// Tile configurations: <KIND, BT, FX, FY, CY, DV, DC>.  Shared memory per CTA (see PipeCfg::SMEM)
-// stays below the 227 KB opt-in limit; DESIGN.md §5 lists the budget of each.
+// Tile configurations <KIND, BT, TX, TY, CY, DV, DC> (level-1 extent TX x TY, strips of CY cells,
+// ring depths).  Shared memory per CTA stays below the 227 KB opt-in limit (DESIGN.md §5 lists each
+// budget).  At BT = 1 the coefficient box equals the output tile, and TX = 32 / 64 puts its rows on
+// 128-byte lines (the interior column x = R is 128-byte aligned in the device layout).
 cudaError_t launch_pipe(int kind, int b, const KParams& p, int zchunk_req, int num_sms, int cfg,
                         cudaStream_t stream, LaunchInfo* info) {
-#define PIPE(K, B, FX, FY, CY, DV, DC) return run_pipe<K, B, FX, FY, CY, DV, DC>(p, zchunk_req, num_sms, stream, info)
+#define PIPE(K, B, TX, TY, CY, DV, DC) return run_pipe<K, B, TX, TY, CY, DV, DC>(p, zchunk_req, num_sms, stream, info)
   switch (kind) {
     case K7C:
       switch (b) {
@@ -426,20 +467,23 @@ cudaError_t launch_pipe(int kind, int b, const KParams& p, int zchunk_req, int n
           if (cfg == 1) PIPE(K7V, 1, 32, 32, 4, 4, 2);
           PIPE(K7V, 1, 32, 32, 4, 4, 3);
         case 2:
-          if (cfg == 1) PIPE(K7V, 2, 32, 24, 4, 4, 4);
-          PIPE(K7V, 2, 32, 32, 4, 4, 3);
+          if (cfg == 1) PIPE(K7V, 2, 32, 24, 4, 4, 3);
+          PIPE(K7V, 2, 32, 28, 4, 4, 3);
         case 3:
-          PIPE(K7V, 3, 32, 24, 4, 4, 4);
+          PIPE(K7V, 3, 32, 20, 4, 4, 4);
       }
       break;
     case K25W:
       if (b == 1) {
-        if (cfg == 1) PIPE(K25W, 1, 64, 32, 8, 8, 4);
-        PIPE(K25W, 1, 64, 16, 4, 6, 3);
+        if (cfg == 1) PIPE(K25W, 1, 32, 32, 4, 7, 3);
+        PIPE(K25W, 1, 64, 16, 4, 7, 3);
       }
       break;
     case K25V:
-      if (b == 1) PIPE(K25V, 1, 64, 16, 4, 8, 3);
+      if (b == 1) {
+        if (cfg == 1) PIPE(K25V, 1, 32, 16, 4, 6, 3);
+        PIPE(K25V, 1, 64, 8, 2, 6, 3);
+      }
       break;
   }
 #undef PIPE

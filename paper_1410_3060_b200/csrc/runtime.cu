@@ -175,7 +175,7 @@ void release(stencil_ctx* h) {
 
 int default_bt(int kind) {
   switch (kind) {
-    case ST_7PT_CONST: return 4;
+    case ST_7PT_CONST: return 4;  // tools/sweep.py on B200
     case ST_7PT_VAR: return 2;
     default: return 1;
   }

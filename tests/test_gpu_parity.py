@@ -12,8 +12,8 @@ from gpu_common import WAVE, assert_parity, gpu_run, interior, rel_err
 pytestmark = pytest.mark.gpu
 
 KINDS = [synth.K7C, synth.K7V, synth.K25W, synth.K25V]
-# several tiles in x and y with ragged tails, several z-chunks (7-point tiles are 30..22 wide,
-# 25-point tiles 56 x 8)
+# several tiles in x and y with ragged tails, several z-chunks (7-point output tiles 32x32 .. 16x16,
+# 25-point output tiles 64 x 8 / 32 x 16 / 64 x 16; streaming variant 30 x 30 .. 22 x 22, 56 x 8)
 SHAPES = {synth.K7C: (61, 70, 45), synth.K7V: (61, 70, 45), synth.K25W: (130, 37, 41),
           synth.K25V: (130, 37, 41)}
 
@@ -24,7 +24,7 @@ def max_bt(kind, variant=st.ST_VARIANT_PIPE):
     return {synth.K7C: 8, synth.K7V: 3, synth.K25W: 1, synth.K25V: 1}[kind]
 
 
-N_CFG = {synth.K7C: 1, synth.K7V: 2, synth.K25W: 2, synth.K25V: 1}  # pipe tile configurations
+N_CFG = {synth.K7C: 1, synth.K7V: 2, synth.K25W: 2, synth.K25V: 2}  # pipe tile configurations
 
 
 @pytest.mark.parametrize("kind", KINDS)
