@@ -88,7 +88,10 @@ typedef struct {
   int variant;         /* ST_VARIANT_*; 0 = auto */
   int bt;              /* time-block depth (levels fused per launch); 0 = auto; >= 1 otherwise */
   int tile_cfg;        /* kernel tile configuration index of the variant (0 = default) */
-  int reserved;        /* must be 0 */
+  int local_slabs;     /* z-slabs held by this handle: 1 (one slab per process and GPU; neighbours
+                          exchange halos with NCCL), or nranks with rank = 0 ("loopback": all slabs
+                          on this handle's device, halos exchanged by device copies -- the multi-GPU
+                          plan on one GPU) */
   int zchunk;          /* planes per CTA z-chunk; 0 = auto */
   int rank, nranks;    /* z-slab decomposition over nranks processes (one GPU each); 1 = single */
   const void *nccl_id; /* nranks > 1: 128-byte ncclUniqueId made by rank 0 (stencil_nccl_unique_id)
@@ -100,18 +103,19 @@ typedef struct {
 } st_opts;
 
 typedef struct {
-  int kind, R, bt, variant, rank, nranks;
-  int tile_x, tile_y, zchunk;     /* output tile of the streaming kernel; z planes per CTA */
+  int kind, R, bt, variant, rank, nranks, local_slabs;
+  int tile_x, tile_y, zchunk;     /* output tile of the last launch; z planes per work item */
   int64_t nx, ny, nz;             /* global interior extents */
-  int64_t own_z0, own_z1;         /* padded planes [own_z0, own_z1) this rank owns (global index) */
+  int64_t own_z0, own_z1;         /* padded planes [own_z0, own_z1) this handle owns (global index) */
   int64_t pitch, plane;           /* device row pitch and plane stride, in doubles */
-  int64_t local_planes;           /* padded planes stored on this rank (owned + halo) */
+  int64_t local_planes;           /* padded planes stored by this handle (owned + halos) */
   int64_t device_bytes;           /* device memory held by the handle */
   int64_t steps_done;             /* time steps applied since creation (Omega^steps_done is level 0) */
   int64_t launches;               /* kernel launches enqueued since creation / last stats reset */
 } st_info;
 
-/* Fill *o with defaults: device -1, auto variant/bt/tiles, single rank, NULL stream, cudaMalloc. */
+/* Fill *o with defaults: device -1, auto variant/bt/tiles, single rank (local_slabs 1), NULL stream,
+ * cudaMalloc. */
 void stencil_opts_default(st_opts *o);
 
 /*

@@ -33,15 +33,15 @@ FREE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void
 
 class StOpts(ctypes.Structure):
     _fields_ = [("device", ctypes.c_int), ("variant", ctypes.c_int), ("bt", ctypes.c_int),
-                ("tile_cfg", ctypes.c_int), ("reserved", ctypes.c_int), ("zchunk", ctypes.c_int),
+                ("tile_cfg", ctypes.c_int), ("local_slabs", ctypes.c_int), ("zchunk", ctypes.c_int),
                 ("rank", ctypes.c_int), ("nranks", ctypes.c_int), ("nccl_id", ctypes.c_void_p),
                 ("stream", ctypes.c_void_p), ("alloc", ALLOC_FN), ("free", FREE_FN),
                 ("alloc_user", ctypes.c_void_p)]
 
 
 class StInfo(ctypes.Structure):
-    _fields_ = [(n, ctypes.c_int) for n in ("kind", "R", "bt", "variant", "rank", "nranks", "tile_x",
-                                             "tile_y", "zchunk")] + \
+    _fields_ = [(n, ctypes.c_int) for n in ("kind", "R", "bt", "variant", "rank", "nranks", "local_slabs",
+                                             "tile_x", "tile_y", "zchunk")] + \
                [(n, ctypes.c_int64) for n in ("nx", "ny", "nz", "own_z0", "own_z1", "pitch", "plane",
                                                "local_planes", "device_bytes", "steps_done", "launches")]
 
@@ -255,6 +255,7 @@ class Grid:
 
     def __init__(self, kind, nx, ny, nz, *, seed=None, scalars=None, v0=None, u0=None, coeff=None,
                  variant=ST_VARIANT_AUTO, bt=0, zchunk=0, tile_cfg=0, rank=0, nranks=1, nccl_id=None,
+                 local_slabs=1,
                  device=None, stream=None, torch_memory=True):
         import torch
         self.kind, self.nx, self.ny, self.nz = kind, nx, ny, nz
@@ -262,9 +263,9 @@ class Grid:
         o = stencil_opts_default()
         o.device = torch.cuda.current_device() if device is None else device
         o.variant, o.bt, o.zchunk, o.tile_cfg = variant, bt, zchunk, tile_cfg
-        o.rank, o.nranks = rank, nranks
+        o.rank, o.nranks, o.local_slabs = rank, nranks, local_slabs
         self._id = None
-        if nranks > 1:
+        if nranks > 1 and local_slabs == 1:
             self._id = ctypes.create_string_buffer(bytes(nccl_id), 128)
             o.nccl_id = ctypes.cast(self._id, ctypes.c_void_p)
         if stream is None:

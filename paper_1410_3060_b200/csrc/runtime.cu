@@ -2,8 +2,13 @@
 //
 // Plan (§8(e)): device layout, time-block schedule
 // (ceil(T/bt) launches, last one T mod bt levels, reading Q16), buffer-role rotation of the
-// two time levels, z-slab decomposition with R*bt-deep halos exchanged with NCCL
-// send/recv after every block.
+// two time levels, z-slab decomposition with R*bt-deep halos.
+//
+// A handle owns one or more consecutive z-slabs of the global grid ("slabs").  After every fused block
+// of b levels the R*b boundary planes of the new level are exchanged between neighbouring slabs:
+//   * slabs of the same handle (opts.local_slabs = nranks, one process, one GPU): device-to-device
+//     copies on the handle's stream ("loopback"; the same plan as multi-GPU, testable on one GPU);
+//   * slabs of different processes (one slab per process and GPU): NCCL send/recv in one group.
 #include "../../include/stencil.h"
 #include "kernels.cuh"
 
@@ -20,7 +25,7 @@
 #include <vector>
 
 #ifndef STENCIL_VERSION
-#define STENCIL_VERSION "0.1.0"
+#define STENCIL_VERSION "0.2.0"
 #endif
 
 namespace {
@@ -75,13 +80,22 @@ Nccl* nccl() {
   return &n;
 }
 
+// One z-slab: global padded planes [store_z0, store_z1) stored, [own_z0, own_z1) owned,
+// interior planes [lo, hi) computed.
+struct Slab {
+  int rank = 0;
+  int64_t own_z0 = 0, own_z1 = 0, store_z0 = 0, store_z1 = 0, zl = 0, lo = 0, hi = 0;
+  double* buf[4] = {nullptr, nullptr, nullptr, nullptr};  // raw (un-offset) state buffers
+  double* coef = nullptr;                                  // raw coefficient slab
+};
+
 }  // namespace
 
 // ---------------------------------------------------------------- the handle
 struct stencil_ctx {
   int kind = 0, R = 0, ncoef = 0, nscal = 0;
   int64_t nx = 0, ny = 0, nz = 0;
-  int rank = 0, nranks = 1;
+  int rank = 0, nranks = 1, local = 1;  // first local slab's rank, total slabs, slabs on this handle
   int device = 0, num_sms = 148;
   int variant = ST_VARIANT_PIPE, bt = 1, zchunk_req = 0, tile_cfg = 0;
   cudaStream_t stream = nullptr;
@@ -89,20 +103,14 @@ struct stencil_ctx {
   st_free_fn free_fn = nullptr;
   void* alloc_user = nullptr;
 
-  // layout (elements)
+  // layout (elements), common to all slabs
   int64_t X = 0, Y = 0, pitch = 0, plane = 0, xoff = 0;
-  int64_t own_z0 = 0, own_z1 = 0, store_z0 = 0, store_z1 = 0, zl = 0;
-  int64_t slab_lo = 0, slab_hi = 0;  // this rank's interior planes (global padded) [lo, hi)
-  size_t arr_bytes = 0;
-
-  // device memory
-  std::vector<std::pair<void*, size_t>> allocs;
-  double* buf[4] = {nullptr, nullptr, nullptr, nullptr};  // raw (un-offset) state buffers
+  std::vector<Slab> slabs;
   int nbuf = 2;
-  int lv0 = 0, lv1 = 1;   // buffer index of Omega^t and Omega^{t-1}
-  double* coef = nullptr;  // raw coefficient slab (ncoef fields of zl planes)
+  int lv0 = 0, lv1 = 1;  // buffer index of Omega^t and Omega^{t-1} (same in every slab)
   double scal[6] = {0, 0, 0, 0, 0, 0};
 
+  std::vector<std::pair<void*, size_t>> allocs;
   int64_t steps = 0;
   int64_t launches = 0;
   int64_t device_bytes = 0;
@@ -110,15 +118,15 @@ struct stencil_ctx {
   std::atomic<int> busy{0};
   st::LaunchInfo last_launch{};
 
-  // timing
   bool timing = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> events;
   size_t events_used = 0;
 
   ncclComm_t comm = nullptr;
 
-  double* at(int b) const { return buf[b] + xoff; }        // element (0,0,0) of buffer b
-  double* coef_at() const { return coef ? coef + xoff : nullptr; }
+  double* at(const Slab& s, int b) const { return s.buf[b] + xoff; }
+  int64_t own_z0() const { return slabs.front().own_z0; }
+  int64_t own_z1() const { return slabs.back().own_z1; }
 };
 
 namespace {
@@ -181,8 +189,7 @@ int default_bt(int kind) {
   }
 }
 
-int plan_slab(int64_t nz, int R, int nranks, int rank, int bt, int64_t* own_z0, int64_t* own_z1,
-              int64_t* store_z0, int64_t* store_z1, int* bt_eff, int64_t* slab_lo, int64_t* slab_hi) {
+int plan_slab(int64_t nz, int R, int nranks, int rank, int bt, Slab* s, int* bt_eff) {
   if (nz < 1 || R < 1 || nranks < 1 || rank < 0 || rank >= nranks || nz < nranks || bt < 0) {
     set_err("plan_slab: bad arguments (nz=%lld R=%d nranks=%d rank=%d bt=%d)", (long long)nz, R,
             nranks, rank, bt);
@@ -200,17 +207,19 @@ int plan_slab(int64_t nz, int R, int nranks, int rank, int bt, int64_t* own_z0, 
   const int64_t lo = R + rank * base + std::min<int64_t>(rank, rem);
   const int64_t hi = lo + base + (rank < rem ? 1 : 0);
   const int64_t H = (int64_t)R * b;
-  *own_z0 = rank == 0 ? 0 : lo;
-  *own_z1 = rank == nranks - 1 ? nz + 2 * R : hi;
-  *store_z0 = rank == 0 ? 0 : lo - H;
-  *store_z1 = rank == nranks - 1 ? nz + 2 * R : hi + H;
+  s->rank = rank;
+  s->lo = lo;
+  s->hi = hi;
+  s->own_z0 = rank == 0 ? 0 : lo;
+  s->own_z1 = rank == nranks - 1 ? nz + 2 * R : hi;
+  s->store_z0 = rank == 0 ? 0 : lo - H;
+  s->store_z1 = rank == nranks - 1 ? nz + 2 * R : hi + H;
+  s->zl = s->store_z1 - s->store_z0;
   if (bt_eff) *bt_eff = b;
-  if (slab_lo) *slab_lo = lo;
-  if (slab_hi) *slab_hi = hi;
   return ST_OK;
 }
 
-// Common part of both create calls: validation, device, plan, allocation.
+// Common part of both create calls: validation, device, plan, allocation, communicator.
 int create_common(stencil_ctx** out, int kind, int64_t nx, int64_t ny, int64_t nz,
                   const st_opts* opts_in, stencil_ctx** hp) {
   if (!out) { set_err("out is NULL"); return ST_E_INVAL; }
@@ -222,14 +231,19 @@ int create_common(stencil_ctx** out, int kind, int64_t nx, int64_t ny, int64_t n
   if (R < 0) { set_err("bad kind %d", kind); return ST_E_INVAL; }
   if (nx < 1 || ny < 1 || nz < 1) { set_err("extents must be >= 1 (got %lld %lld %lld)", (long long)nx, (long long)ny, (long long)nz); return ST_E_INVAL; }
   if (nx > (1 << 30) || ny > (1 << 30)) { set_err("extent too large"); return ST_E_INVAL; }
-  if (o.bt < 0 || o.variant < 0 || o.variant > ST_VARIANT_PIPE || o.zchunk < 0 || o.tile_cfg < 0 ||
-      o.reserved != 0) {
+  if (o.bt < 0 || o.variant < 0 || o.variant > ST_VARIANT_PIPE || o.zchunk < 0 || o.tile_cfg < 0) {
     set_err("bad options (bt=%d variant=%d zchunk=%d tile_cfg=%d)", o.bt, o.variant, o.zchunk, o.tile_cfg);
     return ST_E_INVAL;
   }
   if (o.nranks < 1 || o.rank < 0 || o.rank >= o.nranks) { set_err("bad rank %d of %d", o.rank, o.nranks); return ST_E_INVAL; }
+  const int local = o.local_slabs < 1 ? 1 : o.local_slabs;
+  if (!(local == 1 || (local == o.nranks && o.rank == 0))) {
+    set_err("local_slabs must be 1 (one slab per process) or nranks with rank 0 (got %d of %d)", local, o.nranks);
+    return ST_E_INVAL;
+  }
   if (nz < o.nranks) { set_err("nz=%lld < nranks=%d", (long long)nz, o.nranks); return ST_E_INVAL; }
-  if (o.nranks > 1 && !o.nccl_id) { set_err("nranks > 1 needs nccl_id"); return ST_E_INVAL; }
+  const bool use_nccl = o.nranks > 1 && local == 1;
+  if (use_nccl && !o.nccl_id) { set_err("nranks > 1 with one slab per process needs nccl_id"); return ST_E_INVAL; }
 
   int ndev = 0;
   cudaError_t e = cudaGetDeviceCount(&ndev);
@@ -247,7 +261,7 @@ int create_common(stencil_ctx** out, int kind, int64_t nx, int64_t ny, int64_t n
   *hp = h;
   h->kind = kind; h->R = R; h->ncoef = ncoef_of(kind); h->nscal = nscal_of(kind);
   h->nx = nx; h->ny = ny; h->nz = nz;
-  h->rank = o.rank; h->nranks = o.nranks;
+  h->rank = o.rank; h->nranks = o.nranks; h->local = local;
   h->device = dev;
   h->stream = (cudaStream_t)o.stream;
   h->alloc = o.alloc; h->free_fn = o.free; h->alloc_user = o.alloc_user;
@@ -261,12 +275,13 @@ int create_common(stencil_ctx** out, int kind, int64_t nx, int64_t ny, int64_t n
   const int bt_cap = h->variant == ST_VARIANT_PIPE ? st::max_pipe_bt(kind)
                    : h->variant == ST_VARIANT_STREAM ? st::max_stream_bt(kind) : 1;
   bt = std::min(bt, std::max(1, bt_cap));
-  int bt_eff = 1;
-  int rc = plan_slab(nz, R, o.nranks, o.rank, bt, &h->own_z0, &h->own_z1, &h->store_z0, &h->store_z1,
-                     &bt_eff, &h->slab_lo, &h->slab_hi);
-  if (rc) return rc;
-  h->bt = bt_eff;
-  h->zl = h->store_z1 - h->store_z0;
+  h->slabs.resize(local);
+  for (int i = 0; i < local; ++i) {
+    int bt_eff = 1;
+    int rc = plan_slab(nz, R, o.nranks, o.rank + i, bt, &h->slabs[i], &bt_eff);
+    if (rc) return rc;
+    h->bt = bt_eff;
+  }
 
   // Device layout: interior column x = R lands on a 128-byte boundary; rows padded to 16 doubles.
   h->X = nx + 2 * R;
@@ -274,29 +289,31 @@ int create_common(stencil_ctx** out, int kind, int64_t nx, int64_t ny, int64_t n
   h->xoff = 16 - R;
   h->pitch = ((h->xoff + h->X) + 15) / 16 * 16;
   h->plane = h->pitch * h->Y;
-  h->arr_bytes = (size_t)h->plane * (size_t)h->zl * sizeof(double);
   h->nbuf = (kind == ST_25PT_WAVE && h->bt >= 2) ? 4 : 2;
-  for (int b = 0; b < h->nbuf; ++b) {
-    h->buf[b] = (double*)dev_alloc(h, h->arr_bytes);
-    if (!h->buf[b]) {
-      set_err("device allocation of %zu bytes failed (state buffer %d; %lld bytes held)", h->arr_bytes, b,
-              (long long)h->device_bytes);
-      return ST_E_NOMEM;
+  for (auto& s : h->slabs) {
+    const size_t bytes = (size_t)h->plane * (size_t)s.zl * sizeof(double);
+    for (int b = 0; b < h->nbuf; ++b) {
+      s.buf[b] = (double*)dev_alloc(h, bytes);
+      if (!s.buf[b]) {
+        set_err("device allocation of %zu bytes failed (state buffer %d of slab %d; %lld bytes held)", bytes,
+                b, s.rank, (long long)h->device_bytes);
+        return ST_E_NOMEM;
+      }
     }
-  }
-  if (h->ncoef) {
-    const size_t cb = h->arr_bytes * (size_t)h->ncoef;
-    h->coef = (double*)dev_alloc(h, cb);
-    if (!h->coef) {
-      set_err("device allocation of %zu bytes failed (%d coefficient fields; %lld bytes held)", cb,
-              h->ncoef, (long long)h->device_bytes);
-      return ST_E_NOMEM;
+    if (h->ncoef) {
+      const size_t cb = bytes * (size_t)h->ncoef;
+      s.coef = (double*)dev_alloc(h, cb);
+      if (!s.coef) {
+        set_err("device allocation of %zu bytes failed (%d coefficient fields of slab %d; %lld bytes held)", cb,
+                h->ncoef, s.rank, (long long)h->device_bytes);
+        return ST_E_NOMEM;
+      }
     }
   }
   h->lv0 = 0;
   h->lv1 = 1;
 
-  if (o.nranks > 1) {
+  if (use_nccl) {
     Nccl* n = nccl();
     if (!n) { h->poisoned = true; return ST_E_NCCL; }
     ncclUniqueId id;
@@ -312,12 +329,11 @@ int create_common(stencil_ctx** out, int kind, int64_t nx, int64_t ny, int64_t n
   return ST_OK;
 }
 
-// Copy dense padded global host planes [store_z0, store_z1) into device buffer dst (raw pointer).
-cudaError_t upload_planes(stencil_ctx* h, double* raw, const double* host) {
-  const double* src = host + (size_t)h->store_z0 * h->X * h->Y;
+// Copy dense padded global host planes [store_z0, store_z1) of slab s into its device buffer raw.
+cudaError_t upload_planes(stencil_ctx* h, const Slab& s, double* raw, const double* host) {
+  const double* src = host + (size_t)s.store_z0 * h->X * h->Y;
   return cudaMemcpy2DAsync(raw + h->xoff, h->pitch * sizeof(double), src, h->X * sizeof(double),
-                           h->X * sizeof(double), (size_t)h->Y * h->zl, cudaMemcpyHostToDevice,
-                           h->stream);
+                           h->X * sizeof(double), (size_t)h->Y * s.zl, cudaMemcpyHostToDevice, h->stream);
 }
 
 void fail_create(stencil_ctx* h) {
@@ -326,20 +342,22 @@ void fail_create(stencil_ctx* h) {
   delete h;
 }
 
-st::KParams base_params(stencil_ctx* h) {
+st::KParams base_params(stencil_ctx* h, const Slab& s) {
   st::KParams p{};
-  p.coef = h->coef_at();
-  p.cstride = h->plane * h->zl;
+  p.coef = s.coef ? s.coef + h->xoff : nullptr;
+  p.cstride = h->plane * s.zl;
   p.pitch = h->pitch;
   p.plane = h->plane;
   p.nx = (int)h->nx;
   p.ny = (int)h->ny;
-  p.zl = (int)h->zl;
-  p.zi0 = (int)std::max<int64_t>(0, h->R - h->store_z0);
-  p.zi1 = (int)std::min<int64_t>(h->zl, h->nz + h->R - h->store_z0);
-  p.zo0 = (int)(h->slab_lo - h->store_z0);
-  p.zo1 = (int)(h->slab_hi - h->store_z0);
+  p.zl = (int)s.zl;
+  p.zi0 = (int)std::max<int64_t>(0, h->R - s.store_z0);
+  p.zi1 = (int)std::min<int64_t>(s.zl, h->nz + h->R - s.store_z0);
+  p.zo0 = (int)(s.lo - s.store_z0);
+  p.zo1 = (int)(s.hi - s.store_z0);
   for (int i = 0; i < 6; ++i) p.s[i] = h->scal[i];
+  p.coef_raw = s.coef;
+  p.xoff = (int)h->xoff;
   return p;
 }
 
@@ -357,14 +375,33 @@ cudaEvent_t timing_begin(stencil_ctx* h, cudaEvent_t* end) {
   return pr.first;
 }
 
-// NCCL halo exchange of `depth` planes of buffer b (Jacobi: the new level; wave: both levels).
+// Halo exchange of `depth` planes of buffer b after a block.
 int exchange(stencil_ctx* h, int b, int64_t depth) {
   if (h->nranks == 1 || depth <= 0) return ST_OK;
+  const size_t cnt = (size_t)(depth * h->plane);
+  if (h->local > 1) {
+    // loopback: slabs i and i+1 of this handle share the boundary between slab i's top owned planes
+    // [hi_i - depth, hi_i) and slab i+1's bottom owned planes [lo_{i+1}, lo_{i+1} + depth).
+    for (size_t i = 0; i + 1 < h->slabs.size(); ++i) {
+      Slab& a = h->slabs[i];
+      Slab& c = h->slabs[i + 1];
+      double* A = a.buf[b];
+      double* Cb = c.buf[b];
+      cudaError_t e = cudaMemcpyAsync(Cb + (c.lo - depth - c.store_z0) * h->plane,
+                                      A + (a.hi - depth - a.store_z0) * h->plane, cnt * sizeof(double),
+                                      cudaMemcpyDeviceToDevice, h->stream);
+      if (e == cudaSuccess)
+        e = cudaMemcpyAsync(A + (a.hi - a.store_z0) * h->plane, Cb + (c.lo - c.store_z0) * h->plane,
+                            cnt * sizeof(double), cudaMemcpyDeviceToDevice, h->stream);
+      if (e != cudaSuccess) return cuda_fail(h, e, "loopback halo copy");
+    }
+    return ST_OK;
+  }
   Nccl* n = nccl();
   if (!n) { h->poisoned = true; return ST_E_NCCL; }
-  const int64_t lo = h->slab_lo - h->store_z0, hi = h->slab_hi - h->store_z0;
-  double* base = h->buf[b];
-  const size_t cnt = (size_t)(depth * h->plane);
+  Slab& s = h->slabs.front();
+  const int64_t lo = s.lo - s.store_z0, hi = s.hi - s.store_z0;
+  double* base = s.buf[b];
   ncclResult_t r = n->GroupStart();
   if (h->rank > 0 && r == ncclSuccess) {
     r = n->Send(base + lo * h->plane, cnt, ncclFloat64, h->rank - 1, h->comm, h->stream);
@@ -386,49 +423,48 @@ int exchange(stencil_ctx* h, int b, int64_t depth) {
   return ST_OK;
 }
 
-// One block of b levels: launch, rotate roles, exchange halos.
+// One block of b levels on every slab: launch, rotate roles, exchange halos.
 int run_block(stencil_ctx* h, int b) {
-  st::KParams p = base_params(h);
   const bool wave = h->kind == ST_25PT_WAVE;
-  int new0, new1;
-  p.src_raw = h->buf[h->lv0];
-  p.srcu_raw = h->buf[h->lv1];
-  p.coef_raw = h->coef;
-  p.xoff = (int)h->xoff;
+  int new0, new1, d0, d1 = -1;
   if (!wave) {
-    p.src = h->at(h->lv0);
-    p.dst = h->at(h->lv1);
+    d0 = h->lv1;
     new0 = h->lv1;
     new1 = h->lv0;
   } else if (b == 1) {
-    p.src = h->at(h->lv0);
-    p.srcu = h->at(h->lv1);
-    p.dst = h->at(h->lv1);  // Omega^{t+1} overwrites Omega^{t-1} in place
+    d0 = h->lv1;  // Omega^{t+1} overwrites Omega^{t-1} in place
     new0 = h->lv1;
     new1 = h->lv0;
   } else {
     int spare[2], k = 0;
     for (int i = 0; i < 4; ++i)
       if (i != h->lv0 && i != h->lv1) spare[k++] = i;
-    p.src = h->at(h->lv0);
-    p.srcu = h->at(h->lv1);
-    p.dst = h->at(spare[0]);
-    p.dstu = h->at(spare[1]);
+    d0 = spare[0];
+    d1 = spare[1];
     new0 = spare[0];
     new1 = spare[1];
   }
-  cudaEvent_t ev_end = nullptr;
-  cudaEvent_t ev_begin = timing_begin(h, &ev_end);
-  cudaError_t e;
-  if (h->variant == ST_VARIANT_NAIVE)
-    e = st::launch_naive(h->kind, p, h->stream, &h->last_launch);
-  else if (h->variant == ST_VARIANT_STREAM)
-    e = st::launch_stream(h->kind, b, p, h->zchunk_req, h->num_sms, h->stream, &h->last_launch);
-  else
-    e = st::launch_pipe(h->kind, b, p, h->zchunk_req, h->num_sms, h->tile_cfg, h->stream, &h->last_launch);
-  if (ev_begin) cudaEventRecord(ev_end, h->stream);
-  if (e != cudaSuccess) return cuda_fail(h, e, "kernel launch");
-  h->launches++;
+  for (auto& s : h->slabs) {
+    st::KParams p = base_params(h, s);
+    p.src = h->at(s, h->lv0);
+    p.srcu = h->at(s, h->lv1);
+    p.dst = h->at(s, d0);
+    p.dstu = d1 >= 0 ? h->at(s, d1) : nullptr;
+    p.src_raw = s.buf[h->lv0];
+    p.srcu_raw = s.buf[h->lv1];
+    cudaEvent_t ev_end = nullptr;
+    cudaEvent_t ev_begin = timing_begin(h, &ev_end);
+    cudaError_t e;
+    if (h->variant == ST_VARIANT_NAIVE)
+      e = st::launch_naive(h->kind, p, h->stream, &h->last_launch);
+    else if (h->variant == ST_VARIANT_STREAM)
+      e = st::launch_stream(h->kind, b, p, h->zchunk_req, h->num_sms, h->stream, &h->last_launch);
+    else
+      e = st::launch_pipe(h->kind, b, p, h->zchunk_req, h->num_sms, h->tile_cfg, h->stream, &h->last_launch);
+    if (ev_begin) cudaEventRecord(ev_end, h->stream);
+    if (e != cudaSuccess) return cuda_fail(h, e, "kernel launch");
+    h->launches++;
+  }
   h->lv0 = new0;
   h->lv1 = new1;
   h->steps += b;
@@ -454,6 +490,7 @@ void stencil_opts_default(st_opts* o) {
   o->device = -1;
   o->variant = ST_VARIANT_AUTO;
   o->nranks = 1;
+  o->local_slabs = 1;
 }
 
 const char* stencil_last_error(void) { return g_err.c_str(); }
@@ -463,7 +500,14 @@ const char* stencil_version(void) { return STENCIL_VERSION " (sm_100a)"; }
 int stencil_plan_slab(int64_t nz, int R, int nranks, int rank, int bt, int64_t* own_z0,
                       int64_t* own_z1, int64_t* store_z0, int64_t* store_z1, int* bt_eff) {
   if (!own_z0 || !own_z1 || !store_z0 || !store_z1) { set_err("NULL output"); return ST_E_INVAL; }
-  return plan_slab(nz, R, nranks, rank, bt, own_z0, own_z1, store_z0, store_z1, bt_eff, nullptr, nullptr);
+  Slab s;
+  int rc = plan_slab(nz, R, nranks, rank, bt, &s, bt_eff);
+  if (rc) return rc;
+  *own_z0 = s.own_z0;
+  *own_z1 = s.own_z1;
+  *store_z0 = s.store_z0;
+  *store_z1 = s.store_z1;
+  return ST_OK;
 }
 
 int stencil_create(stencil_ctx** out, int kind, int64_t nx, int64_t ny, int64_t nz,
@@ -482,44 +526,40 @@ int stencil_create(stencil_ctx** out, int kind, int64_t nx, int64_t ny, int64_t 
   int rc = create_common(out, kind, nx, ny, nz, opts, &h);
   if (rc) { fail_create(h); return rc; }
   const size_t hplane = (size_t)h->X * h->Y;
-  cudaError_t e;
-  for (int b = 0; b < h->nbuf && rc == ST_OK; ++b) {
-    e = upload_planes(h, h->buf[b], v0);
-    if (e != cudaSuccess) rc = cuda_fail(h, e, "upload state");
-  }
-  if (rc == ST_OK && kind == ST_25PT_WAVE) {
-    // level 1 = Omega^{-1}: interior from u0, ghosts from v0 (reading Q9).  Upload u0's
-    // planes, then restore ghosts from v0: ghost planes wholesale, ghost rows/columns by 2-D copies.
-    double* d = h->buf[h->lv1] + h->xoff;
-    for (int64_t z = 0; z < h->zl && rc == ST_OK; ++z) {
-      const int64_t gz = h->store_z0 + z;
-      const bool zghost = gz < R || gz >= nz + R;
-      const double* src = (zghost ? v0 : u0) + (size_t)gz * hplane;
-      e = cudaMemcpy2DAsync(d + z * h->plane, h->pitch * sizeof(double), src, h->X * sizeof(double),
-                            h->X * sizeof(double), h->Y, cudaMemcpyHostToDevice, h->stream);
-      if (e == cudaSuccess && !zghost) {
-        const double* g = v0 + (size_t)gz * hplane;
+  cudaError_t e = cudaSuccess;
+  for (auto& s : h->slabs) {
+    for (int b = 0; b < h->nbuf && e == cudaSuccess; ++b) e = upload_planes(h, s, s.buf[b], v0);
+    if (e == cudaSuccess && kind == ST_25PT_WAVE) {
+      // level 1 = Omega^{-1}: interior from u0, ghosts from v0 (reading Q9).  Upload u0's
+      // planes, then restore ghosts from v0: ghost planes wholesale, ghost rows/columns by 2-D copies.
+      double* d = s.buf[h->lv1] + h->xoff;
+      const size_t P = h->pitch * sizeof(double), HX = h->X * sizeof(double);
+      for (int64_t z = 0; z < s.zl && e == cudaSuccess; ++z) {
+        const int64_t gz = s.store_z0 + z;
+        const bool zghost = gz < R || gz >= nz + R;
+        const double* src = (zghost ? v0 : u0) + (size_t)gz * hplane;
         double* dz = d + z * h->plane;
-        // y-ghost rows (R at each end) and x-ghost columns (R at each end of every row)
-        e = cudaMemcpy2DAsync(dz, h->pitch * sizeof(double), g, h->X * sizeof(double), h->X * sizeof(double), R, cudaMemcpyHostToDevice, h->stream);
-        if (e == cudaSuccess)
-          e = cudaMemcpy2DAsync(dz + (h->Y - R) * h->pitch, h->pitch * sizeof(double), g + (h->Y - R) * h->X, h->X * sizeof(double), h->X * sizeof(double), R, cudaMemcpyHostToDevice, h->stream);
-        if (e == cudaSuccess)
-          e = cudaMemcpy2DAsync(dz, h->pitch * sizeof(double), g, h->X * sizeof(double), R * sizeof(double), h->Y, cudaMemcpyHostToDevice, h->stream);
-        if (e == cudaSuccess)
-          e = cudaMemcpy2DAsync(dz + h->X - R, h->pitch * sizeof(double), g + h->X - R, h->X * sizeof(double), R * sizeof(double), h->Y, cudaMemcpyHostToDevice, h->stream);
+        e = cudaMemcpy2DAsync(dz, P, src, HX, HX, h->Y, cudaMemcpyHostToDevice, h->stream);
+        if (e == cudaSuccess && !zghost) {
+          const double* g = v0 + (size_t)gz * hplane;
+          e = cudaMemcpy2DAsync(dz, P, g, HX, HX, R, cudaMemcpyHostToDevice, h->stream);
+          if (e == cudaSuccess)
+            e = cudaMemcpy2DAsync(dz + (h->Y - R) * h->pitch, P, g + (h->Y - R) * h->X, HX, HX, R,
+                                  cudaMemcpyHostToDevice, h->stream);
+          if (e == cudaSuccess)
+            e = cudaMemcpy2DAsync(dz, P, g, HX, R * sizeof(double), h->Y, cudaMemcpyHostToDevice, h->stream);
+          if (e == cudaSuccess)
+            e = cudaMemcpy2DAsync(dz + h->X - R, P, g + h->X - R, HX, R * sizeof(double), h->Y,
+                                  cudaMemcpyHostToDevice, h->stream);
+        }
       }
-      if (e != cudaSuccess) rc = cuda_fail(h, e, "upload wave level 1");
     }
+    for (int i = 0; i < h->ncoef && e == cudaSuccess; ++i)
+      e = upload_planes(h, s, s.coef + (size_t)i * h->plane * s.zl, coeff[i]);
   }
-  if (rc == ST_OK && h->ncoef) {
-    for (int i = 0; i < h->ncoef && rc == ST_OK; ++i) {
-      e = upload_planes(h, h->coef + (size_t)i * h->plane * h->zl, coeff[i]);
-      if (e != cudaSuccess) rc = cuda_fail(h, e, "upload coefficients");
-    }
-  } else if (rc == ST_OK) {
+  if (e != cudaSuccess) rc = cuda_fail(h, e, "upload");
+  if (rc == ST_OK && !h->ncoef)
     for (int i = 0; i < h->nscal; ++i) h->scal[i] = *coeff[i];
-  }
   if (rc == ST_OK) {
     e = cudaStreamSynchronize(h->stream);  // host arrays may be freed by the caller after return
     if (e != cudaSuccess) rc = cuda_fail(h, e, "create synchronize");
@@ -542,16 +582,18 @@ int stencil_create_seeded(stencil_ctx** out, int kind, int64_t nx, int64_t ny, i
   if (kind == ST_7PT_CONST) for (int i = 0; i < 2; ++i) h->scal[i] = scalars ? scalars[i] : d7c[i];
   if (kind == ST_25PT_WAVE) for (int i = 0; i < 6; ++i) h->scal[i] = scalars ? scalars[i] : d25w[i];
   const long long GZ = nz + 2 * R;
-  cudaError_t e = cudaSuccess;
-  for (int b = 0; b < h->nbuf && e == cudaSuccess; ++b) {
-    const int mode = (kind == ST_25PT_WAVE && b == h->lv1) ? 1 : 0;
-    e = st::launch_fill(h->buf[b] + h->xoff, h->pitch, h->plane, (int)h->zl, h->store_z0, h->X, h->Y,
-                        GZ, R, seed, 0, mode, 0.0, h->stream);
-  }
   const double c = kind == ST_7PT_VAR ? 1.0 / 7.0 : 1.0 / 25.0;
-  for (int i = 0; i < h->ncoef && e == cudaSuccess; ++i)
-    e = st::launch_fill(h->coef + (size_t)i * h->plane * h->zl + h->xoff, h->pitch, h->plane, (int)h->zl,
-                        h->store_z0, h->X, h->Y, GZ, R, seed, 2 + i, 2, c, h->stream);
+  cudaError_t e = cudaSuccess;
+  for (auto& s : h->slabs) {
+    for (int b = 0; b < h->nbuf && e == cudaSuccess; ++b) {
+      const int mode = (kind == ST_25PT_WAVE && b == h->lv1) ? 1 : 0;
+      e = st::launch_fill(s.buf[b] + h->xoff, h->pitch, h->plane, (int)s.zl, s.store_z0, h->X, h->Y, GZ, R,
+                          seed, 0, mode, 0.0, h->stream);
+    }
+    for (int i = 0; i < h->ncoef && e == cudaSuccess; ++i)
+      e = st::launch_fill(s.coef + (size_t)i * h->plane * s.zl + h->xoff, h->pitch, h->plane, (int)s.zl,
+                          s.store_z0, h->X, h->Y, GZ, R, seed, 2 + i, 2, c, h->stream);
+  }
   if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
   if (e != cudaSuccess) {
     rc = cuda_fail(h, e, "seeded fill");
@@ -595,20 +637,27 @@ int stencil_read_planes(stencil_ctx* h, int level, int64_t z0, int64_t z1, doubl
     set_err("level %d not readable for kind %d", level, h->kind);
     return ST_E_INVAL;
   }
-  if (!out || z0 < h->own_z0 || z1 > h->own_z1 || z0 > z1) {
+  if (!out || z0 < h->own_z0() || z1 > h->own_z1() || z0 > z1) {
     set_err("planes [%lld,%lld) outside owned [%lld,%lld) or NULL out", (long long)z0, (long long)z1,
-            (long long)h->own_z0, (long long)h->own_z1);
+            (long long)h->own_z0(), (long long)h->own_z1());
     return ST_E_INVAL;
   }
-  const int64_t need = (z1 - z0) * h->X * h->Y;
-  if (out_elems < need) { set_err("out_elems %lld < %lld", (long long)out_elems, (long long)need); return ST_E_INVAL; }
+  const int64_t hplane = h->X * h->Y;
+  if (out_elems < (z1 - z0) * hplane) {
+    set_err("out_elems %lld < %lld", (long long)out_elems, (long long)((z1 - z0) * hplane));
+    return ST_E_INVAL;
+  }
   Guard g(h);
   if (!g.ok) { set_err("handle used concurrently"); return ST_E_STATE; }
-  if (z1 == z0) return ST_OK;
-  const double* src = h->at(level == 0 ? h->lv0 : h->lv1) + (z0 - h->store_z0) * h->plane;
-  cudaError_t e = cudaMemcpy2DAsync(out, h->X * sizeof(double), src, h->pitch * sizeof(double),
-                                    h->X * sizeof(double), (size_t)h->Y * (z1 - z0),
-                                    cudaMemcpyDeviceToHost, h->stream);
+  cudaError_t e = cudaSuccess;
+  for (auto& s : h->slabs) {
+    const int64_t a = std::max(z0, s.own_z0), b = std::min(z1, s.own_z1);
+    if (a >= b) continue;
+    const double* src = h->at(s, level == 0 ? h->lv0 : h->lv1) + (a - s.store_z0) * h->plane;
+    e = cudaMemcpy2DAsync(out + (a - z0) * hplane, h->X * sizeof(double), src, h->pitch * sizeof(double),
+                          h->X * sizeof(double), (size_t)h->Y * (b - a), cudaMemcpyDeviceToHost, h->stream);
+    if (e != cudaSuccess) break;
+  }
   if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
   if (e != cudaSuccess) return cuda_fail(h, e, "read");
   return ST_OK;
@@ -617,10 +666,11 @@ int stencil_read_planes(stencil_ctx* h, int level, int64_t z0, int64_t z1, doubl
 int stencil_read(stencil_ctx* h, int level, double* out, int64_t out_elems) {
   int rc = check_handle(h);
   if (rc) return rc;
-  const int64_t total = (h->nz + 2 * h->R) * h->X * h->Y;
+  const int64_t hplane = h->X * h->Y;
+  const int64_t total = (h->nz + 2 * h->R) * hplane;
   if (!out || out_elems < total) { set_err("out must hold %lld doubles", (long long)total); return ST_E_INVAL; }
-  return stencil_read_planes(h, level, h->own_z0, h->own_z1, out + h->own_z0 * h->X * h->Y,
-                             (h->own_z1 - h->own_z0) * h->X * h->Y);
+  return stencil_read_planes(h, level, h->own_z0(), h->own_z1(), out + h->own_z0() * hplane,
+                             (h->own_z1() - h->own_z0()) * hplane);
 }
 
 int stencil_write(stencil_ctx* h, int level, const double* in, int64_t in_elems) {
@@ -634,12 +684,14 @@ int stencil_write(stencil_ctx* h, int level, const double* in, int64_t in_elems)
   if (!in || in_elems < total) { set_err("in must hold %lld doubles", (long long)total); return ST_E_INVAL; }
   Guard g(h);
   if (!g.ok) { set_err("handle used concurrently"); return ST_E_STATE; }
-  cudaError_t e = upload_planes(h, h->buf[level == 0 ? h->lv0 : h->lv1], in);
-  if (e == cudaSuccess && level == 0 && h->kind != ST_25PT_WAVE)
-    e = upload_planes(h, h->buf[h->lv1], in);  // keep level 1's ghosts equal to the new ghosts
-  if (e == cudaSuccess && h->kind == ST_25PT_WAVE && h->nbuf == 4 && level == 0) {
-    for (int b = 0; b < 4 && e == cudaSuccess; ++b)
-      if (b != h->lv0 && b != h->lv1) e = upload_planes(h, h->buf[b], in);  // spare buffers' ghosts
+  cudaError_t e = cudaSuccess;
+  for (auto& s : h->slabs) {
+    if (e == cudaSuccess) e = upload_planes(h, s, s.buf[level == 0 ? h->lv0 : h->lv1], in);
+    if (e == cudaSuccess && level == 0 && h->kind != ST_25PT_WAVE)
+      e = upload_planes(h, s, s.buf[h->lv1], in);  // keep level 1's ghosts equal to the new ghosts
+    if (e == cudaSuccess && h->kind == ST_25PT_WAVE && h->nbuf == 4 && level == 0)
+      for (int b = 0; b < 4 && e == cudaSuccess; ++b)
+        if (b != h->lv0 && b != h->lv1) e = upload_planes(h, s, s.buf[b], in);  // spare buffers' ghosts
   }
   if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
   if (e != cudaSuccess) return cuda_fail(h, e, "write");
@@ -650,11 +702,14 @@ int stencil_info(const stencil_ctx* h, st_info* o) {
   if (!h || !o) { set_err("NULL handle or out"); return ST_E_INVAL; }
   memset(o, 0, sizeof *o);
   o->kind = h->kind; o->R = h->R; o->bt = h->variant == ST_VARIANT_NAIVE ? 1 : h->bt;
-  o->variant = h->variant; o->rank = h->rank; o->nranks = h->nranks;
+  o->variant = h->variant; o->rank = h->rank; o->nranks = h->nranks; o->local_slabs = h->local;
   o->tile_x = h->last_launch.tile_x; o->tile_y = h->last_launch.tile_y; o->zchunk = h->last_launch.zchunk;
   o->nx = h->nx; o->ny = h->ny; o->nz = h->nz;
-  o->own_z0 = h->own_z0; o->own_z1 = h->own_z1;
-  o->pitch = h->pitch; o->plane = h->plane; o->local_planes = h->zl;
+  o->own_z0 = h->own_z0(); o->own_z1 = h->own_z1();
+  o->pitch = h->pitch; o->plane = h->plane;
+  int64_t zl = 0;
+  for (auto& s : h->slabs) zl += s.zl;
+  o->local_planes = zl;
   o->device_bytes = h->device_bytes; o->steps_done = h->steps; o->launches = h->launches;
   return ST_OK;
 }

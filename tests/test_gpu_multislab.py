@@ -1,0 +1,74 @@
+"""The multi-GPU z-slab plan on one GPU: a handle holding all P slabs
+("loopback": halos exchanged by device copies after every fused block, the same plan and kernels as the
+NCCL path) must reproduce the single-slab run bitwise (G4 across slab counts) and match the oracle."""
+import numpy as np
+import pytest
+
+import oracle
+import paper_1410_3060_b200 as st
+import synth
+from gpu_common import WAVE, assert_parity
+
+pytestmark = pytest.mark.gpu
+
+
+def run(kind, n, T, **kw):
+    with st.Grid(kind, *n, seed=31, **kw) as g:
+        g.run(T)
+        new = g.read(0)
+        old = g.read(1) if kind == WAVE else None
+        info = g.info()
+    return new, old, info
+
+
+CASES = [
+    (synth.K7C, (40, 33, 37), 11),
+    (synth.K7V, (40, 33, 37), 9),
+    (synth.K25W, (70, 20, 41), 6),
+    (synth.K25V, (70, 20, 41), 6),
+]
+
+
+@pytest.mark.parametrize("kind,n,T", CASES)
+@pytest.mark.parametrize("P", [2, 3, 5])
+def test_loopback_slabs_bitwise_equal_single(kind, n, T, P):
+    ref = run(kind, n, T)
+    for variant, bt in ((st.ST_VARIANT_PIPE, 0), (st.ST_VARIANT_PIPE, 2 if synth.RADIUS[kind] == 1 else 1),
+                        (st.ST_VARIANT_STREAM, 1), (st.ST_VARIANT_NAIVE, 0)):
+        got = run(kind, n, T, nranks=P, local_slabs=P, variant=variant, bt=bt)
+        assert got[2]["nranks"] == P and got[2]["local_slabs"] == P
+        assert np.array_equal(got[0], ref[0]), (variant, bt)
+        if kind == WAVE:
+            assert np.array_equal(got[1], ref[1]), (variant, bt)
+
+
+@pytest.mark.parametrize("kind,n,T", CASES)
+def test_loopback_slabs_oracle_parity(kind, n, T):
+    inp = synth.make_inputs(kind, *n, seed=31)
+    o_new, o_old = oracle.run(inp, T)
+    g_new, g_old, info = run(kind, n, T, nranks=4, local_slabs=4)
+    assert_parity(kind, g_new, g_old, o_new, o_old, inp.R, 1e-12, inputs=inp)
+
+
+def test_bt_clamped_to_thinnest_slab():
+    # 25-point, nz = 16 over 4 slabs of 4 planes: R*bt <= 4 forces bt = 1
+    new, _, info = run(synth.K25V, (20, 20, 16), 3, nranks=4, local_slabs=4, bt=1)
+    assert info["bt"] == 1
+    # 7-point, nz = 9 over 3 slabs of 3 planes: bt clamped to 3
+    _, _, info = run(synth.K7C, (20, 20, 9), 5, nranks=3, local_slabs=3, bt=8)
+    assert info["bt"] == 3
+
+
+def test_weak_shape_medium():
+    """7v 128 x 128 x (64 * 4) over 4 slabs, T = 20, default plan: bitwise equal to one slab."""
+    n = (128, 128, 256)
+    a = run(synth.K7V, n, 20)
+    b = run(synth.K7V, n, 20, nranks=4, local_slabs=4)
+    assert np.array_equal(a[0], b[0])
+
+
+def test_invalid_slab_options():
+    with pytest.raises(st.StencilError):
+        st.Grid(synth.K7V, 8, 8, 8, seed=1, nranks=2, local_slabs=3)
+    with pytest.raises(st.StencilError):
+        st.Grid(synth.K25V, 8, 8, 12, seed=1, nranks=4, local_slabs=4)  # 3-plane slabs < R = 4

@@ -1,0 +1,99 @@
+"""The N > 1 path's host logic on CPU: z-slab plan (stencil_plan_slab) + per-block halo exchange of depth
+R*b, run with world_size 2 (and 3) over torch.distributed `gloo` processes.  Each rank advances its slab
+with the oracle on its stored planes (halo planes act as fixed ghosts during a block, exact for the
+owned planes by the R-per-step cone argument) and exchanges the R*b boundary planes of the new levels
+after every block -- the schedule runtime.cu runs with NCCL.  The concatenated owned planes must equal
+the global oracle run bitwise (the same point formula in the same order)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle
+import paper_1410_3060_b200 as st
+import synth
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _exchange(arr, plan, rank, world, depth, R):
+    """Swap `depth` boundary planes with z-neighbours (gloo send/recv), in place on the stored box."""
+    z0 = plan["store_z0"]
+    lo = plan["own_z0"] if rank > 0 else R
+    hi = plan["own_z1"] if rank < world - 1 else None
+    reqs = []
+    bufs = []
+    if rank > 0:
+        send = torch.from_numpy(np.ascontiguousarray(arr[lo - z0: lo - z0 + depth]))
+        recv = torch.empty_like(send)
+        reqs += [dist.isend(send, rank - 1), dist.irecv(recv, rank - 1)]
+        bufs.append((lo - z0 - depth, recv))
+    if rank < world - 1:
+        send = torch.from_numpy(np.ascontiguousarray(arr[hi - z0 - depth: hi - z0]))
+        recv = torch.empty_like(send)
+        reqs += [dist.isend(send, rank + 1), dist.irecv(recv, rank + 1)]
+        bufs.append((hi - z0, recv))
+    for r in reqs:
+        r.wait()
+    for off, recv in bufs:
+        arr[off: off + depth] = recv.numpy()
+
+
+def _worker(rank, world, port, kind, n, T, bt, out_dir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        nx, ny, nz = n
+        R = synth.RADIUS[kind]
+        plan = st.stencil_plan_slab(nz, R, world, rank, bt)
+        b_eff = plan["bt"]
+        dims = synth.padded_dims(kind, nx, ny, nz)
+        box = ((plan["store_z0"], plan["store_z1"]), (0, dims[1]), (0, dims[2]))
+        inp = synth.make_inputs(kind, nx, ny, nz, seed=21, box=box)
+        V, U = inp.V, inp.U
+        nz_box = V.shape[0] - 2 * R
+        left = T
+        while left > 0:
+            b = min(b_eff, left)
+            oracle.run_arrays(kind, nx, ny, nz_box, V, U, inp.coef, inp.scalars, b, 1)
+            _exchange(V, plan, rank, world, R * b, R)
+            if kind == synth.K25W:
+                _exchange(U, plan, rank, world, R * b, R)
+            left -= b
+        z0 = plan["store_z0"]
+        own = V[plan["own_z0"] - z0: plan["own_z1"] - z0]
+        own_u = U[plan["own_z0"] - z0: plan["own_z1"] - z0]
+        np.save(os.path.join(out_dir, f"r{rank}_v.npy"), own)
+        np.save(os.path.join(out_dir, f"r{rank}_u.npy"), own_u)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("kind,n,T,bt,world", [
+    (synth.K7V, (9, 8, 21), 7, 3, 2),
+    (synth.K7C, (7, 6, 13), 9, 4, 3),
+    (synth.K25V, (9, 10, 26), 5, 2, 2),
+    (synth.K25W, (9, 8, 27), 5, 3, 3),
+])
+def test_slab_schedule_gloo_equals_global(tmp_path, kind, n, T, bt, world):
+    port = _free_port()
+    mp.spawn(_worker, args=(world, port, kind, n, T, bt, str(tmp_path)), nprocs=world, join=True)
+    inp = synth.make_inputs(kind, *n, seed=21)
+    ref_v, ref_u = oracle.run(inp, T, nthreads=1)
+    got_v = np.concatenate([np.load(tmp_path / f"r{r}_v.npy") for r in range(world)])
+    assert got_v.shape == ref_v.shape
+    assert np.array_equal(got_v, ref_v)
+    if kind == synth.K25W:
+        got_u = np.concatenate([np.load(tmp_path / f"r{r}_u.npy") for r in range(world)])
+        assert np.array_equal(got_u, ref_u)
