@@ -52,11 +52,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred P1;\n"
       "LAB_WAIT:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
       "@P1 bra DONE;\n\t"
       "bra LAB_WAIT;\n"
       "DONE:\n\t}" ::"r"(smem_u32(b)),
-      "r"(parity)
+      "r"(parity), "r"(0x989680u)  // suspend-time hint: sleep in hardware instead of spinning
       : "memory");
 }
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int x,
@@ -106,7 +106,7 @@ __device__ __forceinline__ Item decode(int item, int ntx, int nty, const KParams
 // of CY cells each): every consumer cell is computed at level 1, and the level-BT output tile is
 // OX x OY = (TX - 2R(BT-1)) x (TY - 2R(BT-1)).  The Omega^t box (footprint) is E1 grown by R on each
 // side; the coefficient (or wave U) box is E1 itself.  DV / DC = ring depths (planes).
-template <int KIND, int BT, int TX, int TY, int CY, int DV, int DC>
+template <int KIND, int BT, int TX, int TY, int CY, int DV, int DC, int WIN>
 struct PipeCfg {
   using TR = Traits<KIND>;
   static constexpr int R = TR::R, NC = TR::NCOEF, RL = 2 * R + 1;
@@ -133,20 +133,28 @@ struct PipeCfg {
   static_assert(OX > 0 && OY > 0, "tile too small for BT");
   static_assert(NCONS % 32 == 0, "whole consumer warps");
   static_assert(DV >= R + 2, "V ring too shallow");
-  static_assert(!HAS_C || DC >= (WAVE ? 0 : (BT - 1) * R) + 2, "C ring too shallow");
+  // Coefficients: levels 1..BT-WIN read them from the C ring in shared memory, which therefore keeps
+  // each plane for CLAG = (BT-1-WIN)*R steps after its level-1 use; the last WIN levels read them from
+  // a per-thread register window of L = WIN*R planes, filled from the ring when a plane leaves it.
+  static constexpr int CLAG = WAVE ? 0 : (BT - 1 - WIN) * R;
+  static constexpr int L = WIN * R;  // register-window planes
+  static_assert(WIN >= 0 && WIN <= BT - 1, "WIN in [0, BT-1]");
+  static_assert(!WIN || NC > 0, "register window only for variable kinds");
+  static_assert(!HAS_C || DC >= CLAG + 2, "C ring too shallow");
   static_assert((EXB * 8) % 16 == 0 && (FXB * 8) % 16 == 0, "TMA box rows must be 16-byte multiples");
   static_assert(FXB <= 256 && FY <= 256 && EXB <= 256, "TMA box dimension limit");
 };
 
-template <int KIND, int BT, int TX, int TY, int CY, int DV, int DC>
-__global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CY, DV, DC>::THREADS, 1)
+template <int KIND, int BT, int TX, int TY, int CY, int DV, int DC, int WIN>
+__global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CY, DV, DC, WIN>::THREADS, 1)
     pipe_kernel(const __grid_constant__ CUtensorMap mapV, const __grid_constant__ CUtensorMap mapC,
                 const KParams p, int ntx, int nty, int items) {
-  using C = PipeCfg<KIND, BT, TX, TY, CY, DV, DC>;
+  using C = PipeCfg<KIND, BT, TX, TY, CY, DV, DC, WIN>;
   constexpr int R = C::R, NC = C::NC, RL = C::RL, NCONS = C::NCONS, FXB = C::FXB, EXB = C::EXB;
+  constexpr int L = C::L;
   constexpr bool WAVE = C::WAVE, HAS_C = C::HAS_C;
   constexpr int OX = C::OX, OY = C::OY;
-  constexpr int CLAG = WAVE ? 0 : (BT - 1) * R;  // steps a C-ring plane stays in use
+  constexpr int CLAG = C::CLAG;  // steps a C-ring plane stays in use after its level-1 step
 
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double* sV = reinterpret_cast<double*>(smem_raw);
@@ -231,6 +239,8 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CY, DV, DC>::THREADS
       for (int j = 0; j < CY; ++j)
 #pragma unroll
         for (int i = 0; i < RL; ++i) ring[k][j][i] = 0.0;
+    // register window: at step s, cwin[i] = coefficients of plane s - (BT - WIN) * R - L + i (i < L)
+    double cwin[L > 0 ? L : 1][CY][NC > 0 ? NC : 1];
 
     const uint32_t iv_b = iv;
     for (int s = it.s_begin; s <= it.s_end; ++s, ++iv) {
@@ -282,14 +292,14 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CY, DV, DC>::THREADS
         }
 #pragma unroll
         for (int j = 0; j < CY; ++j) {
-          double v = ring[k - 1][j][R];
-          if (zv && inter[j] && ((lvl[j] >> k) & 1u)) {
+          double v = ring[k - 1][j][R];  // ghosts and cells outside the level-k extent keep their input
+          if (zv) {                      // (uniform) -- compute every cell, select: no divergent branches
             const int ly = ly0 + j;
             double m[3][R], pl[3][R];
             const double* row = Src + ly * stride + base;
 #pragma unroll
             for (int r = 1; r <= R; ++r) {
-              m[0][r - 1] = row[-r];
+              m[0][r - 1] = row[-r];  // stays inside shared memory for edge cells; result discarded
               pl[0][r - 1] = row[r];
               m[1][r - 1] = ys[R + j - r];
               pl[1][r - 1] = ys[R + j + r];
@@ -300,11 +310,15 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CY, DV, DC>::THREADS
             double W[NC > 0 ? NC : 1];
             if constexpr (NC > 0) {
 #pragma unroll
-              for (int f = 0; f < NC; ++f) W[f] = Ck[f * C::CFIELD + ci];
+              for (int f = 0; f < NC; ++f) {
+                if (WIN && k > BT - WIN) W[f] = cwin[L > 0 ? (BT - k) * R : 0][j][f];
+                else W[f] = Ck[f * C::CFIELD + ci];
+              }
             }
             double u = 0.0;
             if constexpr (WAVE) u = (k == 1) ? Ck[ci] : ring[k >= 2 ? k - 2 : 0][j][0];
-            v = apply_point<KIND, R>(ring[k - 1][j][R], u, m, pl, W, p.s);
+            const double vc = apply_point<KIND, R>(ring[k - 1][j][R], u, m, pl, W, p.s);
+            v = (inter[j] && ((lvl[j] >> k) & 1u)) ? vc : v;
           }
           if (k < BT) {
 #pragma unroll
@@ -320,10 +334,23 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CY, DV, DC>::THREADS
           __syncwarp();
           if (lane == 0) mbar_arrive(&emptyV[(iv - R) % DV]);
         }
-        if (HAS_C && k == BT && iv >= iv_b + CLAG) {  // C plane of step iv - CLAG fully consumed
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&emptyC[(iv - CLAG) % DC]);
+      }
+      if constexpr (L > 0) {  // slide the window: drop plane s - BT*R, append plane s - (BT-WIN)*R
+        const double* C1 = sC + (size_t)((iv - CLAG) % DC) * C::CSLOT;
+#pragma unroll
+        for (int j = 0; j < CY; ++j) {
+          const int ci = (ly0 + j) * EXB + lx + shc;
+#pragma unroll
+          for (int f = 0; f < NC; ++f) {
+#pragma unroll
+            for (int i = 0; i < L - 1; ++i) cwin[i][j][f] = cwin[i + 1][j][f];
+            cwin[L - 1][j][f] = C1[f * C::CFIELD + ci];
+          }
         }
+      }
+      if (HAS_C && iv >= iv_b + CLAG) {  // C plane of step iv - CLAG fully consumed
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&emptyC[(iv - CLAG) % DC]);
       }
     }
     // release ring slots of this item that the lags above did not reach
@@ -375,10 +402,10 @@ bool make_map(CUtensorMap* m, const double* base, int rank, long long pitch, lon
   return r == CUDA_SUCCESS;
 }
 
-template <int KIND, int BT, int TX, int TY, int CY, int DV, int DC>
+template <int KIND, int BT, int TX, int TY, int CY, int DV, int DC, int WIN = 0>
 cudaError_t run_pipe(const KParams& p0, int zchunk_req, int num_sms, cudaStream_t stream, LaunchInfo* info) {
-  using C = PipeCfg<KIND, BT, TX, TY, CY, DV, DC>;
-  auto kern = pipe_kernel<KIND, BT, TX, TY, CY, DV, DC>;
+  using C = PipeCfg<KIND, BT, TX, TY, CY, DV, DC, WIN>;
+  auto kern = pipe_kernel<KIND, BT, TX, TY, CY, DV, DC, WIN>;
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
@@ -448,6 +475,8 @@ int max_pipe_bt(int kind) {
 cudaError_t launch_pipe(int kind, int b, const KParams& p, int zchunk_req, int num_sms, int cfg,
                         cudaStream_t stream, LaunchInfo* info) {
 #define PIPE(K, B, TX, TY, CY, DV, DC) return run_pipe<K, B, TX, TY, CY, DV, DC>(p, zchunk_req, num_sms, stream, info)
+#define PIPEW(K, B, TX, TY, CY, DV, DC) return run_pipe<K, B, TX, TY, CY, DV, DC, B - 1>(p, zchunk_req, num_sms, stream, info)
+#define PIPEWN(K, B, TX, TY, CY, DV, DC, W) return run_pipe<K, B, TX, TY, CY, DV, DC, W>(p, zchunk_req, num_sms, stream, info)
   switch (kind) {
     case K7C:
       switch (b) {
@@ -467,10 +496,13 @@ cudaError_t launch_pipe(int kind, int b, const KParams& p, int zchunk_req, int n
           if (cfg == 1) PIPE(K7V, 1, 32, 32, 4, 4, 2);
           PIPE(K7V, 1, 32, 32, 4, 4, 3);
         case 2:
-          if (cfg == 1) PIPE(K7V, 2, 32, 24, 4, 4, 3);
-          PIPE(K7V, 2, 32, 28, 4, 4, 3);
+          if (cfg == 1) PIPE(K7V, 2, 32, 28, 4, 4, 3);
+          if (cfg == 2) PIPEW(K7V, 2, 32, 32, 4, 4, 2);
+          PIPEW(K7V, 2, 32, 28, 4, 4, 3);
         case 3:
-          PIPE(K7V, 3, 32, 20, 4, 4, 4);
+          if (cfg == 1) PIPE(K7V, 3, 32, 20, 4, 4, 4);
+          if (cfg == 2) PIPEWN(K7V, 3, 32, 32, 4, 4, 2, 2);
+          PIPEWN(K7V, 3, 32, 28, 4, 4, 3, 1);
       }
       break;
     case K25W:
@@ -487,6 +519,8 @@ cudaError_t launch_pipe(int kind, int b, const KParams& p, int zchunk_req, int n
       break;
   }
 #undef PIPE
+#undef PIPEW
+#undef PIPEWN
   return cudaErrorInvalidValue;
 }
 

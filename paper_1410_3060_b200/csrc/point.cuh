@@ -29,28 +29,35 @@ __device__ __forceinline__ double point_7c(double c, const double (&m)[3][1], co
   return __fma_rn(w1, c, __dmul_rn(w2, s));
 }
 
-// Fig. 1c: W0*O + W1*O[x-1] + W2*O[x+1] + W3*O[y-1] + W4*O[y+1] + W5*O[z-1] + W6*O[z+1].
+// Fig. 1c: W0*O + W1*O[x-1] + W2*O[x+1] + W3*O[y-1] + W4*O[y+1] + W5*O[z-1] + W6*O[z+1],
+// summed as two independent FMA chains (x terms with the centre, y and z terms) added at the end, so
+// the dependent-latency depth is 5 instead of 7 (the kernels are latency-bound at low occupancy).
 __device__ __forceinline__ double point_7v(double c, const double (&m)[3][1], const double (&p)[3][1],
                                            const double (&W)[7]) {
-  double acc = __dmul_rn(W[0], c);
-  acc = __fma_rn(W[1], m[0][0], acc);
-  acc = __fma_rn(W[2], p[0][0], acc);
-  acc = __fma_rn(W[3], m[1][0], acc);
-  acc = __fma_rn(W[4], p[1][0], acc);
-  acc = __fma_rn(W[5], m[2][0], acc);
-  acc = __fma_rn(W[6], p[2][0], acc);
-  return acc;
+  double a = __dmul_rn(W[0], c);
+  double b = __dmul_rn(W[3], m[1][0]);
+  a = __fma_rn(W[1], m[0][0], a);
+  b = __fma_rn(W[4], p[1][0], b);
+  a = __fma_rn(W[2], p[0][0], a);
+  b = __fma_rn(W[5], m[2][0], b);
+  b = __fma_rn(W[6], p[2][0], b);
+  return __dadd_rn(a, b);
 }
 
-// Fig. 1d: W0*O + sum_{r=1..4} [W_{3r-2}(x pair) + W_{3r-1}(y pair) + W_{3r}(z pair)].
+// Fig. 1d: W0*O + sum_{r=1..4} [W_{3r-2}(x pair) + W_{3r-1}(y pair) + W_{3r}(z pair)],
+// as three independent FMA chains (one per axis; the centre term starts the x chain) added at the end:
+// dependent-latency depth 6 instead of 13.
 __device__ __forceinline__ double point_25v(double c, const double (&m)[3][4], const double (&p)[3][4],
                                             const double (&W)[13]) {
-  double acc = __dmul_rn(W[0], c);
+  double acc[3];
+  acc[0] = __fma_rn(W[1], __dadd_rn(m[0][0], p[0][0]), __dmul_rn(W[0], c));
+  acc[1] = __dmul_rn(W[2], __dadd_rn(m[1][0], p[1][0]));
+  acc[2] = __dmul_rn(W[3], __dadd_rn(m[2][0], p[2][0]));
 #pragma unroll
-  for (int r = 0; r < 4; ++r)
+  for (int r = 1; r < 4; ++r)
 #pragma unroll
-    for (int a = 0; a < 3; ++a) acc = __fma_rn(W[1 + 3 * r + a], __dadd_rn(m[a][r], p[a][r]), acc);
-  return acc;
+    for (int a = 0; a < 3; ++a) acc[a] = __fma_rn(W[1 + 3 * r + a], __dadd_rn(m[a][r], p[a][r]), acc[a]);
+  return __dadd_rn(__dadd_rn(acc[0], acc[1]), acc[2]);
 }
 
 // Fig. 1e, scalar alpha: 2*O^t - O^{t-1} + alpha*[w0*O^t + sum_r w_r*(x+y+z pairs_r)].

@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--bts", default="1,2,3,4,5,6")
     ap.add_argument("--zchunks", default="0")
     ap.add_argument("--variants", default="2")
+    ap.add_argument("--cfgs", default="0")
     ap.add_argument("--T", type=int, default=0, help="override T (0 = the workload's)")
     ap.add_argument("--reps", type=int, default=3)
     a = ap.parse_args()
@@ -33,11 +34,12 @@ def main():
         w = {x.name.split("-")[0]: x for x in workloads.CONFIGS}[name]
         T = a.T or w.T
         for variant in [int(v) for v in a.variants.split(",")]:
-            for bt in [int(b) for b in a.bts.split(",")]:
-                for zc in [int(z) for z in a.zchunks.split(",")]:
+            for bt, zc, cfg in [(int(b), int(z), int(c)) for b in a.bts.split(",")
+                                for z in a.zchunks.split(",") for c in a.cfgs.split(",")]:
+                if True:
                     try:
                         g = st.Grid(w.kind, w.nx, w.ny, w.nz, seed=synth.DEFAULT_SEED, variant=variant,
-                                    bt=bt, zchunk=zc)
+                                    bt=bt, zchunk=zc, tile_cfg=cfg)
                     except st.StencilError as e:
                         print(json.dumps({"workload": name, "bt": bt, "error": str(e)}))
                         continue
@@ -59,7 +61,7 @@ def main():
                     info = g.info()
                     g.close()
                     lups = w.nx * w.ny * w.nz * T
-                    print(json.dumps({"workload": name, "variant": variant, "bt": info["bt"],
+                    print(json.dumps({"workload": name, "variant": variant, "bt": info["bt"], "cfg": cfg,
                                       "zchunk": info["zchunk"], "tile": [info["tile_x"], info["tile_y"]],
                                       "ms": round(ms, 3), "glups": round(lups / ms / 1e6, 2)}), flush=True)
                     torch.cuda.empty_cache()
