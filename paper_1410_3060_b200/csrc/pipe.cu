@@ -205,6 +205,7 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CY, DV, DC, WIN>::TH
   }
 
   // ---------------------------------------------------------------- consumers
+  const double ps[6] = {p.s[0], p.s[1], p.s[2], p.s[3], p.s[4], p.s[5]};  // scalars in registers
   const int lx = tid % TX;           // column in the level-1 extent
   const int ly0 = (tid / TX) * CY;   // first row of this thread's strip
   const int lane = tid & 31;
@@ -317,7 +318,7 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CY, DV, DC, WIN>::TH
             }
             double u = 0.0;
             if constexpr (WAVE) u = (k == 1) ? Ck[ci] : ring[k >= 2 ? k - 2 : 0][j][0];
-            const double vc = apply_point<KIND, R>(ring[k - 1][j][R], u, m, pl, W, p.s);
+            const double vc = apply_point<KIND, R>(ring[k - 1][j][R], u, m, pl, W, ps);
             v = (inter[j] && ((lvl[j] >> k) & 1u)) ? vc : v;
           }
           if (k < BT) {
@@ -508,6 +509,7 @@ cudaError_t launch_pipe(int kind, int b, const KParams& p, int zchunk_req, int n
     case K25W:
       if (b == 1) {
         if (cfg == 1) PIPE(K25W, 1, 32, 32, 4, 7, 3);
+        if (cfg == 2) PIPE(K25W, 1, 32, 56, 8, 7, 3);
         PIPE(K25W, 1, 64, 16, 4, 7, 3);
       }
       break;
