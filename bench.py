@@ -261,9 +261,11 @@ def main():
                                     + (block_bytes_per_cell(w.kind, rem) if rem else 0))
     launches_per_step = nblocks_full + (1 if rem else 0)
     avg_launch_ms = kern_ms / max(1, kern_launches)
-    bytes_per_launch = per_step_bytes / launches_per_step
+    # achieved = algorithmic bytes of the timed launches / their summed device time (equivalently bytes
+    # per launch / average launch time when every launch is a full block; with z-slabs each block is
+    # an edge + interior pair of launches)
     peak, peak_src = load_peaks()
-    achieved = bytes_per_launch / (avg_launch_ms / 1e3) / 1e9
+    achieved = per_step_bytes * args.steps / (kern_ms / 1e3) / 1e9 if kern_ms else 0.0
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": load_traffic(w.name, bt), "peak_source": peak_src,
                 "bytes_per_cell_per_launch": block_bytes_per_cell(w.kind, bt), "bt": bt,

@@ -28,6 +28,7 @@ struct KParams {
   const double* srcu_raw;
   const double* coef_raw;
   int xoff;
+  int dbg;  // experiment knob (STENCIL_DBG): bit 0 = skip all compute in the pipe kernel
 };
 
 struct LaunchInfo {

@@ -106,7 +106,7 @@ __device__ __forceinline__ Item decode(int item, int ntx, int nty, const KParams
 // of CY cells each): every consumer cell is computed at level 1, and the level-BT output tile is
 // OX x OY = (TX - 2R(BT-1)) x (TY - 2R(BT-1)).  The Omega^t box (footprint) is E1 grown by R on each
 // side; the coefficient (or wave U) box is E1 itself.  DV / DC = ring depths (planes).
-template <int KIND, int BT, int TX, int TY, int CY, int DV, int DC, int WIN>
+template <int KIND, int BT, int TX, int TY, int CY, int DV, int DC, int WIN, int MINB>
 struct PipeCfg {
   using TR = Traits<KIND>;
   static constexpr int R = TR::R, NC = TR::NCOEF, RL = 2 * R + 1;
@@ -145,11 +145,11 @@ struct PipeCfg {
   static_assert(FXB <= 256 && FY <= 256 && EXB <= 256, "TMA box dimension limit");
 };
 
-template <int KIND, int BT, int TX, int TY, int CY, int DV, int DC, int WIN>
-__global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CY, DV, DC, WIN>::THREADS, 1)
+template <int KIND, int BT, int TX, int TY, int CY, int DV, int DC, int WIN, int MINB>
+__global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CY, DV, DC, WIN, MINB>::THREADS, MINB)
     pipe_kernel(const __grid_constant__ CUtensorMap mapV, const __grid_constant__ CUtensorMap mapC,
                 const KParams p, int ntx, int nty, int items) {
-  using C = PipeCfg<KIND, BT, TX, TY, CY, DV, DC, WIN>;
+  using C = PipeCfg<KIND, BT, TX, TY, CY, DV, DC, WIN, MINB>;
   constexpr int R = C::R, NC = C::NC, RL = C::RL, NCONS = C::NCONS, FXB = C::FXB, EXB = C::EXB;
   constexpr int L = C::L;
   constexpr bool WAVE = C::WAVE, HAS_C = C::HAS_C;
@@ -280,7 +280,7 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CY, DV, DC, WIN>::TH
           base = lx;
         }
         // planes below s_begin + k*R are not valid at level k (unless the stream starts at plane 0)
-        const bool zv = c >= p.zi0 && c < p.zi1 && (it.s_begin == 0 || c >= it.s_begin + k * R);
+        const bool zv = !(p.dbg & 1) && c >= p.zi0 && c < p.zi1 && (it.s_begin == 0 || c >= it.s_begin + k * R);
         const double* Ck = sC + (size_t)((iv - (k - 1) * R) % DC) * C::CSLOT;
         double ys[CY + 2 * R];
         if (zv) {
@@ -403,10 +403,10 @@ bool make_map(CUtensorMap* m, const double* base, int rank, long long pitch, lon
   return r == CUDA_SUCCESS;
 }
 
-template <int KIND, int BT, int TX, int TY, int CY, int DV, int DC, int WIN = 0>
+template <int KIND, int BT, int TX, int TY, int CY, int DV, int DC, int WIN = 0, int MINB = 1>
 cudaError_t run_pipe(const KParams& p0, int zchunk_req, int num_sms, cudaStream_t stream, LaunchInfo* info) {
-  using C = PipeCfg<KIND, BT, TX, TY, CY, DV, DC, WIN>;
-  auto kern = pipe_kernel<KIND, BT, TX, TY, CY, DV, DC, WIN>;
+  using C = PipeCfg<KIND, BT, TX, TY, CY, DV, DC, WIN, MINB>;
+  auto kern = pipe_kernel<KIND, BT, TX, TY, CY, DV, DC, WIN, MINB>;
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
@@ -478,6 +478,7 @@ cudaError_t launch_pipe(int kind, int b, const KParams& p, int zchunk_req, int n
 #define PIPE(K, B, TX, TY, CY, DV, DC) return run_pipe<K, B, TX, TY, CY, DV, DC>(p, zchunk_req, num_sms, stream, info)
 #define PIPEW(K, B, TX, TY, CY, DV, DC) return run_pipe<K, B, TX, TY, CY, DV, DC, B - 1>(p, zchunk_req, num_sms, stream, info)
 #define PIPEWN(K, B, TX, TY, CY, DV, DC, W) return run_pipe<K, B, TX, TY, CY, DV, DC, W>(p, zchunk_req, num_sms, stream, info)
+#define PIPE2(K, B, TX, TY, CY, DV, DC, W) return run_pipe<K, B, TX, TY, CY, DV, DC, W, 2>(p, zchunk_req, num_sms, stream, info)
   switch (kind) {
     case K7C:
       switch (b) {
@@ -495,14 +496,21 @@ cudaError_t launch_pipe(int kind, int b, const KParams& p, int zchunk_req, int n
       switch (b) {
         case 1:
           if (cfg == 1) PIPE(K7V, 1, 32, 32, 4, 4, 2);
+          if (cfg == 3) PIPE2(K7V, 1, 32, 14, 2, 4, 3, 0);
           PIPE(K7V, 1, 32, 32, 4, 4, 3);
         case 2:
           if (cfg == 1) PIPE(K7V, 2, 32, 28, 4, 4, 3);
           if (cfg == 2) PIPEW(K7V, 2, 32, 32, 4, 4, 2);
+          if (cfg == 3) PIPE2(K7V, 2, 32, 14, 2, 4, 3, 1);
           PIPEW(K7V, 2, 32, 28, 4, 4, 3);
         case 3:
           if (cfg == 1) PIPE(K7V, 3, 32, 20, 4, 4, 4);
           if (cfg == 2) PIPEWN(K7V, 3, 32, 32, 4, 4, 2, 2);
+          if (cfg == 3) PIPE2(K7V, 3, 32, 14, 2, 4, 2, 2);
+          if (cfg == 4) PIPE2(K7V, 3, 32, 12, 2, 4, 2, 2);
+          if (cfg == 5) PIPE2(K7V, 3, 32, 14, 2, 4, 3, 1);
+          if (cfg == 6) PIPEWN(K7V, 3, 32, 20, 4, 4, 4, 1);
+          if (cfg == 7) PIPEWN(K7V, 3, 32, 24, 4, 5, 3, 1);
           PIPEWN(K7V, 3, 32, 28, 4, 4, 3, 1);
       }
       break;
@@ -510,6 +518,7 @@ cudaError_t launch_pipe(int kind, int b, const KParams& p, int zchunk_req, int n
       if (b == 1) {
         if (cfg == 1) PIPE(K25W, 1, 32, 32, 4, 7, 3);
         if (cfg == 2) PIPE(K25W, 1, 32, 56, 8, 7, 3);
+        if (cfg == 3) PIPE2(K25W, 1, 32, 14, 2, 7, 3, 0);
         PIPE(K25W, 1, 64, 16, 4, 7, 3);
       }
       break;
@@ -523,6 +532,7 @@ cudaError_t launch_pipe(int kind, int b, const KParams& p, int zchunk_req, int n
 #undef PIPE
 #undef PIPEW
 #undef PIPEWN
+#undef PIPE2
   return cudaErrorInvalidValue;
 }
 

@@ -18,6 +18,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -123,6 +124,12 @@ struct stencil_ctx {
   size_t events_used = 0;
 
   ncclComm_t comm = nullptr;
+  // halo-first overlap (nranks > 1): the exchange runs on comm_stream after the edge kernels
+  // (ev_edge) while the interior kernels run on `stream`; ev_halo marks the exchange's completion.
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t ev_edge = nullptr, ev_halo = nullptr;
+  bool halo_pending = false;
+  bool overlap = true;  // STENCIL_NO_OVERLAP=1: bulk-synchronous schedule (one launch, then exchange)
 
   double* at(const Slab& s, int b) const { return s.buf[b] + xoff; }
   int64_t own_z0() const { return slabs.front().own_z0; }
@@ -179,6 +186,11 @@ void release(stencil_ctx* h) {
   h->events.clear();
   if (h->comm && nccl()) nccl()->CommDestroy(h->comm);
   h->comm = nullptr;
+  if (h->comm_stream) cudaStreamSynchronize(h->comm_stream), cudaStreamDestroy(h->comm_stream);
+  if (h->ev_edge) cudaEventDestroy(h->ev_edge);
+  if (h->ev_halo) cudaEventDestroy(h->ev_halo);
+  h->comm_stream = nullptr;
+  h->ev_edge = h->ev_halo = nullptr;
 }
 
 int default_bt(int kind) {
@@ -313,6 +325,13 @@ int create_common(stencil_ctx** out, int kind, int64_t nx, int64_t ny, int64_t n
   h->lv0 = 0;
   h->lv1 = 1;
 
+  if (o.nranks > 1) {
+    CK(cudaStreamCreateWithFlags(&h->comm_stream, cudaStreamNonBlocking), "comm stream");
+    CK(cudaEventCreateWithFlags(&h->ev_edge, cudaEventDisableTiming), "event");
+    CK(cudaEventCreateWithFlags(&h->ev_halo, cudaEventDisableTiming), "event");
+    const char* no = getenv("STENCIL_NO_OVERLAP");
+    h->overlap = !(no && atoi(no));
+  }
   if (use_nccl) {
     Nccl* n = nccl();
     if (!n) { h->poisoned = true; return ST_E_NCCL; }
@@ -358,6 +377,8 @@ st::KParams base_params(stencil_ctx* h, const Slab& s) {
   for (int i = 0; i < 6; ++i) p.s[i] = h->scal[i];
   p.coef_raw = s.coef;
   p.xoff = (int)h->xoff;
+  static const int dbg = getenv("STENCIL_DBG") ? atoi(getenv("STENCIL_DBG")) : 0;
+  p.dbg = dbg;
   return p;
 }
 
@@ -376,7 +397,7 @@ cudaEvent_t timing_begin(stencil_ctx* h, cudaEvent_t* end) {
 }
 
 // Halo exchange of `depth` planes of buffer b after a block.
-int exchange(stencil_ctx* h, int b, int64_t depth) {
+int exchange(stencil_ctx* h, int b, int64_t depth, cudaStream_t cs) {
   if (h->nranks == 1 || depth <= 0) return ST_OK;
   const size_t cnt = (size_t)(depth * h->plane);
   if (h->local > 1) {
@@ -389,10 +410,10 @@ int exchange(stencil_ctx* h, int b, int64_t depth) {
       double* Cb = c.buf[b];
       cudaError_t e = cudaMemcpyAsync(Cb + (c.lo - depth - c.store_z0) * h->plane,
                                       A + (a.hi - depth - a.store_z0) * h->plane, cnt * sizeof(double),
-                                      cudaMemcpyDeviceToDevice, h->stream);
+                                      cudaMemcpyDeviceToDevice, cs);
       if (e == cudaSuccess)
         e = cudaMemcpyAsync(A + (a.hi - a.store_z0) * h->plane, Cb + (c.lo - c.store_z0) * h->plane,
-                            cnt * sizeof(double), cudaMemcpyDeviceToDevice, h->stream);
+                            cnt * sizeof(double), cudaMemcpyDeviceToDevice, cs);
       if (e != cudaSuccess) return cuda_fail(h, e, "loopback halo copy");
     }
     return ST_OK;
@@ -404,14 +425,14 @@ int exchange(stencil_ctx* h, int b, int64_t depth) {
   double* base = s.buf[b];
   ncclResult_t r = n->GroupStart();
   if (h->rank > 0 && r == ncclSuccess) {
-    r = n->Send(base + lo * h->plane, cnt, ncclFloat64, h->rank - 1, h->comm, h->stream);
+    r = n->Send(base + lo * h->plane, cnt, ncclFloat64, h->rank - 1, h->comm, cs);
     if (r == ncclSuccess)
-      r = n->Recv(base + (lo - depth) * h->plane, cnt, ncclFloat64, h->rank - 1, h->comm, h->stream);
+      r = n->Recv(base + (lo - depth) * h->plane, cnt, ncclFloat64, h->rank - 1, h->comm, cs);
   }
   if (h->rank < h->nranks - 1 && r == ncclSuccess) {
-    r = n->Send(base + (hi - depth) * h->plane, cnt, ncclFloat64, h->rank + 1, h->comm, h->stream);
+    r = n->Send(base + (hi - depth) * h->plane, cnt, ncclFloat64, h->rank + 1, h->comm, cs);
     if (r == ncclSuccess)
-      r = n->Recv(base + hi * h->plane, cnt, ncclFloat64, h->rank + 1, h->comm, h->stream);
+      r = n->Recv(base + hi * h->plane, cnt, ncclFloat64, h->rank + 1, h->comm, cs);
   }
   ncclResult_t r2 = n->GroupEnd();
   if (r == ncclSuccess) r = r2;
@@ -423,7 +444,41 @@ int exchange(stencil_ctx* h, int b, int64_t depth) {
   return ST_OK;
 }
 
-// One block of b levels on every slab: launch, rotate roles, exchange halos.
+// Launch the kernel of the handle's variant for b levels over output planes [z0, z1) (global padded
+// indices) of slab s.
+int launch_range(stencil_ctx* h, Slab& s, int b, int d0, int d1, int64_t z0, int64_t z1) {
+  if (z1 <= z0) return ST_OK;
+  st::KParams p = base_params(h, s);
+  p.zo0 = (int)(z0 - s.store_z0);
+  p.zo1 = (int)(z1 - s.store_z0);
+  p.src = h->at(s, h->lv0);
+  p.srcu = h->at(s, h->lv1);
+  p.dst = h->at(s, d0);
+  p.dstu = d1 >= 0 ? h->at(s, d1) : nullptr;
+  p.src_raw = s.buf[h->lv0];
+  p.srcu_raw = s.buf[h->lv1];
+  cudaEvent_t ev_end = nullptr;
+  cudaEvent_t ev_begin = timing_begin(h, &ev_end);
+  cudaError_t e;
+  if (h->variant == ST_VARIANT_NAIVE)
+    e = st::launch_naive(h->kind, p, h->stream, &h->last_launch);
+  else if (h->variant == ST_VARIANT_STREAM)
+    e = st::launch_stream(h->kind, b, p, h->zchunk_req, h->num_sms, h->stream, &h->last_launch);
+  else
+    e = st::launch_pipe(h->kind, b, p, h->zchunk_req, h->num_sms, h->tile_cfg, h->stream, &h->last_launch);
+  if (ev_begin) cudaEventRecord(ev_end, h->stream);
+  if (e != cudaSuccess) return cuda_fail(h, e, "kernel launch");
+  h->launches++;
+  return ST_OK;
+}
+
+// One block of b levels on every slab, then the halo exchange of the new level(s).
+// Multi-slab schedule ("halo-first"): the edge kernels compute the R*b boundary planes of
+// each slab that has a neighbour, the exchange of those planes starts on comm_stream, and the interior
+// kernel (planes [lo + R*b, hi - R*b)) runs on the compute stream meanwhile.  The interior kernel reads
+// only owned planes of the old level and writes only interior planes of the new one, so it touches
+// neither the planes being sent nor the halo planes being received.  The next block waits for the
+// exchange (ev_halo).
 int run_block(stencil_ctx* h, int b) {
   const bool wave = h->kind == ST_25PT_WAVE;
   int new0, new1, d0, d1 = -1;
@@ -444,32 +499,51 @@ int run_block(stencil_ctx* h, int b) {
     new0 = spare[0];
     new1 = spare[1];
   }
-  for (auto& s : h->slabs) {
-    st::KParams p = base_params(h, s);
-    p.src = h->at(s, h->lv0);
-    p.srcu = h->at(s, h->lv1);
-    p.dst = h->at(s, d0);
-    p.dstu = d1 >= 0 ? h->at(s, d1) : nullptr;
-    p.src_raw = s.buf[h->lv0];
-    p.srcu_raw = s.buf[h->lv1];
-    cudaEvent_t ev_end = nullptr;
-    cudaEvent_t ev_begin = timing_begin(h, &ev_end);
-    cudaError_t e;
-    if (h->variant == ST_VARIANT_NAIVE)
-      e = st::launch_naive(h->kind, p, h->stream, &h->last_launch);
-    else if (h->variant == ST_VARIANT_STREAM)
-      e = st::launch_stream(h->kind, b, p, h->zchunk_req, h->num_sms, h->stream, &h->last_launch);
-    else
-      e = st::launch_pipe(h->kind, b, p, h->zchunk_req, h->num_sms, h->tile_cfg, h->stream, &h->last_launch);
-    if (ev_begin) cudaEventRecord(ev_end, h->stream);
-    if (e != cudaSuccess) return cuda_fail(h, e, "kernel launch");
-    h->launches++;
+  int rc = ST_OK;
+  const int64_t depth = (int64_t)h->R * b;
+  if (h->nranks == 1) {
+    for (auto& s : h->slabs)
+      if ((rc = launch_range(h, s, b, d0, d1, s.lo, s.hi))) return rc;
+  } else {
+    cudaError_t e = cudaSuccess;
+    if (h->halo_pending) e = cudaStreamWaitEvent(h->stream, h->ev_halo, 0);  // previous block's halos
+    if (e != cudaSuccess) return cuda_fail(h, e, "wait halo");
+    if (!h->overlap) {
+      for (auto& s : h->slabs)
+        if ((rc = launch_range(h, s, b, d0, d1, s.lo, s.hi))) return rc;
+    } else {
+      // edge planes first (a slab thinner than two edges is computed whole)
+      for (auto& s : h->slabs) {
+        const bool below = s.rank > 0, above = s.rank < h->nranks - 1;
+        const int64_t ilo = s.lo + (below ? depth : 0), ihi = s.hi - (above ? depth : 0);
+        if (ilo >= ihi) {
+          if ((rc = launch_range(h, s, b, d0, d1, s.lo, s.hi))) return rc;
+          continue;
+        }
+        if (below && (rc = launch_range(h, s, b, d0, d1, s.lo, ilo))) return rc;
+        if (above && (rc = launch_range(h, s, b, d0, d1, ihi, s.hi))) return rc;
+      }
+    }
+    e = cudaEventRecord(h->ev_edge, h->stream);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(h->comm_stream, h->ev_edge, 0);
+    if (e != cudaSuccess) return cuda_fail(h, e, "edge event");
+    rc = exchange(h, new0, depth, h->comm_stream);
+    if (!rc && wave) rc = exchange(h, new1, depth, h->comm_stream);
+    if (rc) return rc;
+    e = cudaEventRecord(h->ev_halo, h->comm_stream);
+    if (e != cudaSuccess) return cuda_fail(h, e, "halo event");
+    h->halo_pending = true;
+    if (h->overlap) {
+      for (auto& s : h->slabs) {
+        const bool below = s.rank > 0, above = s.rank < h->nranks - 1;
+        const int64_t ilo = s.lo + (below ? depth : 0), ihi = s.hi - (above ? depth : 0);
+        if (ilo < ihi && (rc = launch_range(h, s, b, d0, d1, ilo, ihi))) return rc;
+      }
+    }
   }
   h->lv0 = new0;
   h->lv1 = new1;
   h->steps += b;
-  int rc = exchange(h, h->lv0, (int64_t)h->R * b);
-  if (!rc && wave) rc = exchange(h, h->lv1, (int64_t)h->R * b);
   return rc;
 }
 
@@ -618,6 +692,11 @@ int stencil_run(stencil_ctx* h, int64_t T) {
     const int b = (int)std::min<int64_t>(bt, left);
     rc = run_block(h, b);
     left -= b;
+  }
+  if (rc == ST_OK && h->halo_pending) {  // later work on the caller's stream sees the halos
+    const cudaError_t e2 = cudaStreamWaitEvent(h->stream, h->ev_halo, 0);
+    if (e2 != cudaSuccess) return cuda_fail(h, e2, "join comm stream");
+    h->halo_pending = false;
   }
   return rc;
 }

@@ -67,6 +67,17 @@ def test_weak_shape_medium():
     assert np.array_equal(a[0], b[0])
 
 
+@pytest.mark.parametrize("kind,n,T", CASES)
+def test_overlap_schedule_equals_bulk_synchronous(kind, n, T, monkeypatch):
+    """Halo-first schedule (edge kernels, exchange on a comm stream, interior kernel) == one launch per
+    slab followed by the exchange (STENCIL_NO_OVERLAP=1), bitwise."""
+    a = run(kind, n, T, nranks=3, local_slabs=3)
+    monkeypatch.setenv("STENCIL_NO_OVERLAP", "1")
+    b = run(kind, n, T, nranks=3, local_slabs=3)
+    assert np.array_equal(a[0], b[0])
+    assert a[2]["launches"] > b[2]["launches"]  # the split schedule launches edge + interior kernels
+
+
 def test_invalid_slab_options():
     with pytest.raises(st.StencilError):
         st.Grid(synth.K7V, 8, 8, 8, seed=1, nranks=2, local_slabs=3)
