@@ -218,19 +218,19 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CY, DV, DC, WIN, MIN
     const int shv = (it.gx0 - R + p.xoff) & 1;  // column shift of the footprint boxes
     const int shc = (it.gx0 + p.xoff) & 1;      // column shift of the C boxes
     const int lxv = lx + R + shv;               // this column inside a footprint box row
-    bool inter[CY], outc[CY];
-    unsigned lvl[CY];
+    bool outc[CY];
+    unsigned act[CY];  // bit k: cell is interior and inside the level-k extent (computed at level k)
     long long col[CY];
 #pragma unroll
     for (int j = 0; j < CY; ++j) {
       const int ly = ly0 + j, gy = it.gy0 + ly;
-      inter[j] = xin && gy >= R && gy < p.ny + R;
-      lvl[j] = 0;
+      const bool inter = xin && gy >= R && gy < p.ny + R;
+      act[j] = 0;
 #pragma unroll
       for (int k = 1; k <= BT; ++k)
-        if (lx >= (k - 1) * R && lx < TX - (k - 1) * R && ly >= (k - 1) * R && ly < TY - (k - 1) * R)
-          lvl[j] |= 1u << k;
-      outc[j] = inter[j] && ((lvl[j] >> BT) & 1u);
+        if (inter && lx >= (k - 1) * R && lx < TX - (k - 1) * R && ly >= (k - 1) * R && ly < TY - (k - 1) * R)
+          act[j] |= 1u << k;
+      outc[j] = (act[j] >> BT) & 1u;
       col[j] = (long long)gy * p.pitch + gx;
     }
     double ring[BT][CY][RL];
@@ -274,53 +274,52 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CY, DV, DC, WIN, MIN
           double* P = sP + (size_t)((k - 2) * 2 + buf) * C::PELEMS;
 #pragma unroll
           for (int j = 0; j < CY; ++j) P[(ly0 + j) * TX + lx] = ring[k - 1][j][R];
-          named_sync(1, NCONS);
+          if (!(p.dbg & 2)) named_sync(1, NCONS);
           Src = P;
           stride = TX;
           base = lx;
         }
-        // planes below s_begin + k*R are not valid at level k (unless the stream starts at plane 0)
+        // planes below s_begin + k*R are not valid at level k (unless the stream starts at plane 0).
+        // Invalid steps still run the same straight-line code (no divergent branches) but read only
+        // slots this step has already waited for, and their results are discarded by the select.
         const bool zv = !(p.dbg & 1) && c >= p.zi0 && c < p.zi1 && (it.s_begin == 0 || c >= it.s_begin + k * R);
-        const double* Ck = sC + (size_t)((iv - (k - 1) * R) % DC) * C::CSLOT;
+        if (k == 1 && !zv) Src = sV + (size_t)(iv % DV) * C::VSLOT;
+        const double* Ck = sC + (size_t)((zv ? iv - (k - 1) * R : iv) % DC) * C::CSLOT;
         double ys[CY + 2 * R];
-        if (zv) {
 #pragma unroll
-          for (int i = 0; i < CY + 2 * R; ++i) {
-            int row = ly0 - R + i;
-            if (k > 1) row = min(max(row, 0), TY - 1);  // level planes have no halo rows
-            ys[i] = Src[row * stride + base];
-          }
+        for (int i = 0; i < CY + 2 * R; ++i) {
+          int row = ly0 - R + i;
+          if (k > 1) row = min(max(row, 0), TY - 1);  // level planes have no halo rows
+          ys[i] = Src[row * stride + base];
         }
 #pragma unroll
         for (int j = 0; j < CY; ++j) {
-          double v = ring[k - 1][j][R];  // ghosts and cells outside the level-k extent keep their input
-          if (zv) {                      // (uniform) -- compute every cell, select: no divergent branches
-            const int ly = ly0 + j;
-            double m[3][R], pl[3][R];
-            const double* row = Src + ly * stride + base;
+          const int ly = ly0 + j;
+          double m[3][R], pl[3][R];
+          const double* row = Src + ly * stride + base;
 #pragma unroll
-            for (int r = 1; r <= R; ++r) {
-              m[0][r - 1] = row[-r];  // stays inside shared memory for edge cells; result discarded
-              pl[0][r - 1] = row[r];
-              m[1][r - 1] = ys[R + j - r];
-              pl[1][r - 1] = ys[R + j + r];
-              m[2][r - 1] = ring[k - 1][j][R - r];
-              pl[2][r - 1] = ring[k - 1][j][R + r];
-            }
-            const int ci = ly * EXB + lx + shc;
-            double W[NC > 0 ? NC : 1];
-            if constexpr (NC > 0) {
-#pragma unroll
-              for (int f = 0; f < NC; ++f) {
-                if (WIN && k > BT - WIN) W[f] = cwin[L > 0 ? (BT - k) * R : 0][j][f];
-                else W[f] = Ck[f * C::CFIELD + ci];
-              }
-            }
-            double u = 0.0;
-            if constexpr (WAVE) u = (k == 1) ? Ck[ci] : ring[k >= 2 ? k - 2 : 0][j][0];
-            const double vc = apply_point<KIND, R>(ring[k - 1][j][R], u, m, pl, W, ps);
-            v = (inter[j] && ((lvl[j] >> k) & 1u)) ? vc : v;
+          for (int r = 1; r <= R; ++r) {
+            m[0][r - 1] = row[-r];  // stays inside shared memory for edge cells; result discarded
+            pl[0][r - 1] = row[r];
+            m[1][r - 1] = ys[R + j - r];
+            pl[1][r - 1] = ys[R + j + r];
+            m[2][r - 1] = ring[k - 1][j][R - r];
+            pl[2][r - 1] = ring[k - 1][j][R + r];
           }
+          const int ci = ly * EXB + lx + shc;
+          double W[NC > 0 ? NC : 1];
+          if constexpr (NC > 0) {
+#pragma unroll
+            for (int f = 0; f < NC; ++f) {
+              if (WIN && k > BT - WIN) W[f] = cwin[L > 0 ? (BT - k) * R : 0][j][f];
+              else W[f] = Ck[f * C::CFIELD + ci];
+            }
+          }
+          double u = 0.0;
+          if constexpr (WAVE) u = (k == 1) ? Ck[ci] : ring[k >= 2 ? k - 2 : 0][j][0];
+          const double vc = apply_point<KIND, R>(ring[k - 1][j][R], u, m, pl, W, ps);
+          // ghosts and cells outside the level-k extent keep their input value
+          const double v = (zv && ((act[j] >> k) & 1u)) ? vc : ring[k - 1][j][R];
           if (k < BT) {
 #pragma unroll
             for (int i = 0; i < RL - 1; ++i) ring[k < BT ? k : 0][j][i] = ring[k < BT ? k : 0][j][i + 1];
@@ -337,7 +336,8 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CY, DV, DC, WIN, MIN
         }
       }
       if constexpr (L > 0) {  // slide the window: drop plane s - BT*R, append plane s - (BT-WIN)*R
-        const double* C1 = sC + (size_t)((iv - CLAG) % DC) * C::CSLOT;
+        // (before the item's first CLAG steps the window entry is never used; read a waited slot)
+        const double* C1 = sC + (size_t)((iv >= iv_b + CLAG ? iv - CLAG : iv) % DC) * C::CSLOT;
 #pragma unroll
         for (int j = 0; j < CY; ++j) {
           const int ci = (ly0 + j) * EXB + lx + shc;
