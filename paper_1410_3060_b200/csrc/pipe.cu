@@ -83,15 +83,18 @@ struct Item {
   int gx0, gy0, zc0, zc1, s_begin, s_end;
 };
 
-// Item origin = the level-1 extent origin: output origin minus R*H (H = BT - 1 halo levels).
+// Item origin = the level-1 extent origin: output origin minus R*H (H = BT - 1 halo levels), shifted
+// left by dx in {0, 1} so that the origin's raw column (gx0 + xoff) is even: then every TMA box puts
+// the tile's cells on 16-byte boundaries of shared memory (OX is even, so all tiles share the shift).
 template <int R, int H, int OX, int OY>
 __device__ __forceinline__ Item decode(int item, int ntx, int nty, const KParams& p) {
   constexpr int BT = H + 1;
+  const int dx = (R - R * H + p.xoff) & 1;
   const int per = ntx * nty;
   const int zc = item / per, t = item - zc * per;
   const int ty = t / ntx, tx = t - ty * ntx;
   Item it;
-  it.gx0 = tx * OX + R - R * H;
+  it.gx0 = tx * OX + R - R * H - dx;
   it.gy0 = ty * OY + R - R * H;
   it.zc0 = p.zo0 + zc * p.zchunk;
   it.zc1 = min(p.zo1, it.zc0 + p.zchunk);
@@ -100,27 +103,60 @@ __device__ __forceinline__ Item decode(int item, int ntx, int nty, const KParams
   return it;
 }
 
+// N consecutive doubles from shared memory: 128-bit loads when VEC (p 16-byte aligned, N even).
+template <int N, bool VEC>
+__device__ __forceinline__ void lds_row(const double* p, double* out) {
+  if constexpr (VEC && N % 2 == 0) {
+#pragma unroll
+    for (int i = 0; i < N / 2; ++i) {
+      const double2 v = reinterpret_cast<const double2*>(p)[i];
+      out[2 * i] = v.x;
+      out[2 * i + 1] = v.y;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < N; ++i) out[i] = p[i];
+  }
+}
+template <int N, bool VEC>
+__device__ __forceinline__ void sts_row(double* p, const double* in) {
+  if constexpr (VEC && N % 2 == 0) {
+#pragma unroll
+    for (int i = 0; i < N / 2; ++i) reinterpret_cast<double2*>(p)[i] = make_double2(in[2 * i], in[2 * i + 1]);
+  } else {
+#pragma unroll
+    for (int i = 0; i < N; ++i) p[i] = in[i];
+  }
+}
+
 }  // namespace
 
-// Consumer threads cover the level-1 extent E1 = TX x TY of a tile (TX threads per row, TY/CY strips
-// of CY cells each): every consumer cell is computed at level 1, and the level-BT output tile is
+// Consumer threads cover the level-1 extent E1 = TX x TY of a tile: each thread owns a block of CX
+// consecutive columns x CY consecutive rows (TX/CX threads per row, TY/CY strips): every consumer
+// cell is computed at level 1, and the level-BT output tile is
 // OX x OY = (TX - 2R(BT-1)) x (TY - 2R(BT-1)).  The Omega^t box (footprint) is E1 grown by R on each
 // side; the coefficient (or wave U) box is E1 itself.  DV / DC = ring depths (planes).
-template <int KIND, int BT, int TX, int TY, int CY, int DV, int DC, int WIN, int MINB>
+template <int KIND, int BT, int TX, int TY, int CX, int CY, int DV, int DC, int WIN, int MINB>
 struct PipeCfg {
   using TR = Traits<KIND>;
   static constexpr int R = TR::R, NC = TR::NCOEF, RL = 2 * R + 1;
   static constexpr bool WAVE = TR::WAVE;
   static constexpr int NS = TY / CY;
-  static constexpr int NCONS = TX * NS;
+  static constexpr int LPR = TX / CX;  // threads per row
+  static constexpr int NCONS = LPR * NS;
+  static constexpr bool VEC = CX >= 2;  // 128-bit shared-memory accesses
+  static constexpr int RP = VEC ? (R + 1) / 2 * 2 : R;  // x-halo columns loaded per side
   static constexpr int THREADS = NCONS + 32;
   static constexpr int FX = TX + 2 * R, FY = TY + 2 * R;         // Omega^t footprint
   static constexpr int OX = TX - 2 * R * (BT - 1), OY = TY - 2 * R * (BT - 1);
   static constexpr int NCF = WAVE ? 1 : NC;  // fields in the C ring (coefficients, or U for the wave)
   static constexpr bool HAS_C = NCF > 0;
-  // TMA boxes start on an even fp64 column (tiled TMA needs 16-byte aligned x coordinates), so the
-  // boxes are 2 columns wider than the data and the data sit at a per-item shift of 0 or 1.
+  // TMA boxes start on an even fp64 column (tiled TMA needs 16-byte aligned x coordinates): the tile
+  // origin's raw column is even (decode), so the coefficient box starts exactly at the level-1 extent
+  // (shift SHC = 0) and the footprint box one column early when R is odd (shift SHV = R & 1); both
+  // boxes are 2 columns wider than the data.
   static constexpr int FXB = FX + 2, EXB = TX + 2;
+  static constexpr int SHV = R & 1, SHC = 0;
   static constexpr int VELEMS = FXB * FY, CFIELD = EXB * TY, CELEMS = CFIELD * NCF;
   static constexpr int VSLOT = (VELEMS + 15) / 16 * 16;  // ring slot strides: TMA destinations
   static constexpr int CSLOT = (CELEMS + 15) / 16 * 16;  // must be 128-byte aligned
@@ -129,7 +165,7 @@ struct PipeCfg {
   static constexpr size_t SMEM = sizeof(double) * ((size_t)DV * VSLOT + (HAS_C ? (size_t)DC * CSLOT : 0) +
                                                    (size_t)NPL * 2 * PELEMS) +
                                  sizeof(uint64_t) * 2 * (DV + DC) + 128;
-  static_assert(TY % CY == 0, "strips");
+  static_assert(TY % CY == 0 && TX % CX == 0 && (CX == 1 || CX % 2 == 0), "cell blocks");
   static_assert(OX > 0 && OY > 0, "tile too small for BT");
   static_assert(NCONS % 32 == 0, "whole consumer warps");
   static_assert(DV >= R + 2, "V ring too shallow");
@@ -145,11 +181,11 @@ struct PipeCfg {
   static_assert(FXB <= 256 && FY <= 256 && EXB <= 256, "TMA box dimension limit");
 };
 
-template <int KIND, int BT, int TX, int TY, int CY, int DV, int DC, int WIN, int MINB>
-__global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CY, DV, DC, WIN, MINB>::THREADS, MINB)
+template <int KIND, int BT, int TX, int TY, int CX, int CY, int DV, int DC, int WIN, int MINB>
+__global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN, MINB>::THREADS, MINB)
     pipe_kernel(const __grid_constant__ CUtensorMap mapV, const __grid_constant__ CUtensorMap mapC,
                 const KParams p, int ntx, int nty, int items) {
-  using C = PipeCfg<KIND, BT, TX, TY, CY, DV, DC, WIN, MINB>;
+  using C = PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN, MINB>;
   constexpr int R = C::R, NC = C::NC, RL = C::RL, NCONS = C::NCONS, FXB = C::FXB, EXB = C::EXB;
   constexpr int L = C::L;
   constexpr bool WAVE = C::WAVE, HAS_C = C::HAS_C;
@@ -205,43 +241,46 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CY, DV, DC, WIN, MIN
   }
 
   // ---------------------------------------------------------------- consumers
+  constexpr int CXN = CX, LPR = C::LPR, RP = C::RP, SHV = C::SHV, SHC = C::SHC;
+  constexpr bool VEC = C::VEC;
   const double ps[6] = {p.s[0], p.s[1], p.s[2], p.s[3], p.s[4], p.s[5]};  // scalars in registers
-  const int lx = tid % TX;           // column in the level-1 extent
-  const int ly0 = (tid / TX) * CY;   // first row of this thread's strip
+  const int x0 = (tid % LPR) * CXN;  // first level-1-extent column of this thread's cell block
+  const int ly0 = (tid / LPR) * CY;  // first row
   const int lane = tid & 31;
   uint32_t iv = 0;
 
   for (int item = blockIdx.x; item < items; item += gridDim.x) {
     const Item it = decode<R, BT - 1, OX, OY>(item, ntx, nty, p);
-    const int gx = it.gx0 + lx;
-    const bool xin = gx >= R && gx < p.nx + R;
-    const int shv = (it.gx0 - R + p.xoff) & 1;  // column shift of the footprint boxes
-    const int shc = (it.gx0 + p.xoff) & 1;      // column shift of the C boxes
-    const int lxv = lx + R + shv;               // this column inside a footprint box row
-    bool outc[CY];
-    unsigned act[CY];  // bit k: cell is interior and inside the level-k extent (computed at level k)
-    long long col[CY];
+    bool outc[CY][CXN];
+    unsigned act[CY][CXN];  // bit k: cell is interior and inside the level-k extent (computed at level k)
+    long long col[CY];      // global offset of the block's first cell in each row
 #pragma unroll
     for (int j = 0; j < CY; ++j) {
       const int ly = ly0 + j, gy = it.gy0 + ly;
-      const bool inter = xin && gy >= R && gy < p.ny + R;
-      act[j] = 0;
+      col[j] = (long long)gy * p.pitch + it.gx0 + x0;
 #pragma unroll
-      for (int k = 1; k <= BT; ++k)
-        if (inter && lx >= (k - 1) * R && lx < TX - (k - 1) * R && ly >= (k - 1) * R && ly < TY - (k - 1) * R)
-          act[j] |= 1u << k;
-      outc[j] = (act[j] >> BT) & 1u;
-      col[j] = (long long)gy * p.pitch + gx;
+      for (int i = 0; i < CXN; ++i) {
+        const int lx = x0 + i, gx = it.gx0 + lx;
+        const bool inter = gx >= R && gx < p.nx + R && gy >= R && gy < p.ny + R;
+        act[j][i] = 0;
+#pragma unroll
+        for (int k = 1; k <= BT; ++k)
+          if (inter && lx >= (k - 1) * R && lx < TX - (k - 1) * R && ly >= (k - 1) * R && ly < TY - (k - 1) * R)
+            act[j][i] |= 1u << k;
+        outc[j][i] = (act[j][i] >> BT) & 1u;
+      }
     }
-    double ring[BT][CY][RL];
+    double ring[BT][CY][CXN][RL];
 #pragma unroll
     for (int k = 0; k < BT; ++k)
 #pragma unroll
       for (int j = 0; j < CY; ++j)
 #pragma unroll
-        for (int i = 0; i < RL; ++i) ring[k][j][i] = 0.0;
-    // register window: at step s, cwin[i] = coefficients of plane s - (BT - WIN) * R - L + i (i < L)
-    double cwin[L > 0 ? L : 1][CY][NC > 0 ? NC : 1];
+        for (int i = 0; i < CXN; ++i)
+#pragma unroll
+          for (int q = 0; q < RL; ++q) ring[k][j][i][q] = 0.0;
+    // register window: at step s, cwin[q] = coefficients of plane s - (BT - WIN) * R - L + q (q < L)
+    double cwin[L > 0 ? L : 1][CY][CXN][NC > 0 ? NC : 1];
 
     const uint32_t iv_b = iv;
     for (int s = it.s_begin; s <= it.s_end; ++s, ++iv) {
@@ -252,82 +291,106 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CY, DV, DC, WIN, MIN
       const double* Vs = sV + (size_t)sv * C::VSLOT;
 #pragma unroll
       for (int j = 0; j < CY; ++j) {
-        const double v = Vs[(ly0 + j + R) * FXB + lxv];
+        double v[CXN];
+        lds_row<CXN, VEC>(Vs + (ly0 + j + R) * FXB + R + SHV + x0, v);
 #pragma unroll
-        for (int i = 0; i < RL - 1; ++i) ring[0][j][i] = ring[0][j][i + 1];
-        ring[0][j][RL - 1] = v;
+        for (int i = 0; i < CXN; ++i) {
+#pragma unroll
+          for (int q = 0; q < RL - 1; ++q) ring[0][j][i][q] = ring[0][j][i][q + 1];
+          ring[0][j][i][RL - 1] = v[i];
+        }
       }
       if constexpr (HAS_C) mbar_wait(&fullC[iv % DC], (iv / DC) & 1);
 
 #pragma unroll
       for (int k = 1; k <= BT; ++k) {
         const int c = s - k * R;
-        // x/y neighbour source: level 1 reads the footprint box of plane s - R (row stride FXB,
-        // cell (lx, ly) at [(ly + R) * FXB + lxv]); level k >= 2 a shared level plane (TX x TY).
-        const double* Src;
-        int stride, base;
-        if (k == 1) {
-          Src = sV + (size_t)((iv - R) % DV) * C::VSLOT;
-          stride = FXB;
-          base = R * FXB + lxv;
-        } else {
-          double* P = sP + (size_t)((k - 2) * 2 + buf) * C::PELEMS;
-#pragma unroll
-          for (int j = 0; j < CY; ++j) P[(ly0 + j) * TX + lx] = ring[k - 1][j][R];
-          if (!(p.dbg & 2)) named_sync(1, NCONS);
-          Src = P;
-          stride = TX;
-          base = lx;
-        }
         // planes below s_begin + k*R are not valid at level k (unless the stream starts at plane 0).
         // Invalid steps still run the same straight-line code (no divergent branches) but read only
         // slots this step has already waited for, and their results are discarded by the select.
         const bool zv = !(p.dbg & 1) && c >= p.zi0 && c < p.zi1 && (it.s_begin == 0 || c >= it.s_begin + k * R);
-        if (k == 1 && !zv) Src = sV + (size_t)(iv % DV) * C::VSLOT;
-        const double* Ck = sC + (size_t)((zv ? iv - (k - 1) * R : iv) % DC) * C::CSLOT;
-        double ys[CY + 2 * R];
+        // x/y neighbour source, addressed as Sb[y * SS + x] in level-1-extent coordinates: level 1
+        // reads the footprint box of plane s - R, level k >= 2 a shared level plane (TX x TY).
+        const double* Sb;
+        int SS;
+        if (k == 1) {
+          Sb = sV + (size_t)((zv ? iv - R : iv) % DV) * C::VSLOT + R * FXB + R + SHV;
+          SS = FXB;
+        } else {
+          double* P = sP + (size_t)((k - 2) * 2 + buf) * C::PELEMS;
 #pragma unroll
-        for (int i = 0; i < CY + 2 * R; ++i) {
-          int row = ly0 - R + i;
+          for (int j = 0; j < CY; ++j) {
+            double v[CXN];
+#pragma unroll
+            for (int i = 0; i < CXN; ++i) v[i] = ring[k - 1][j][i][R];
+            sts_row<CXN, VEC>(P + (ly0 + j) * TX + x0, v);
+          }
+          if (!(p.dbg & 2)) named_sync(1, NCONS);
+          Sb = P;
+          SS = TX;
+        }
+        const double* Ck = sC + (size_t)((zv ? iv - (k - 1) * R : iv) % DC) * C::CSLOT + SHC;
+        // y-strip: rows ly0 - R .. ly0 + CY + R - 1 of this thread's columns
+        double ys[CY + 2 * R][CXN];
+#pragma unroll
+        for (int q = 0; q < CY + 2 * R; ++q) {
+          int row = ly0 - R + q;
           if (k > 1) row = min(max(row, 0), TY - 1);  // level planes have no halo rows
-          ys[i] = Src[row * stride + base];
+          lds_row<CXN, VEC>(Sb + row * SS + x0, ys[q]);
         }
 #pragma unroll
         for (int j = 0; j < CY; ++j) {
           const int ly = ly0 + j;
-          double m[3][R], pl[3][R];
-          const double* row = Src + ly * stride + base;
+          // this row's x-neighbourhood: RP halo columns | the block's CX cells | RP halo columns
+          double xr[RP + CXN + RP];
+          lds_row<RP, VEC>(Sb + ly * SS + x0 - RP, xr);  // in shared memory even at the plane edges
+          lds_row<RP, VEC>(Sb + ly * SS + x0 + CXN, xr + RP + CXN);
 #pragma unroll
-          for (int r = 1; r <= R; ++r) {
-            m[0][r - 1] = row[-r];  // stays inside shared memory for edge cells; result discarded
-            pl[0][r - 1] = row[r];
-            m[1][r - 1] = ys[R + j - r];
-            pl[1][r - 1] = ys[R + j + r];
-            m[2][r - 1] = ring[k - 1][j][R - r];
-            pl[2][r - 1] = ring[k - 1][j][R + r];
-          }
-          const int ci = ly * EXB + lx + shc;
-          double W[NC > 0 ? NC : 1];
+          for (int i = 0; i < CXN; ++i) xr[RP + i] = ys[R + j][i];
+          double Wrow[NC > 0 ? NC : 1][CXN];
           if constexpr (NC > 0) {
+            if (!(WIN && k > BT - WIN)) {
 #pragma unroll
-            for (int f = 0; f < NC; ++f) {
-              if (WIN && k > BT - WIN) W[f] = cwin[L > 0 ? (BT - k) * R : 0][j][f];
-              else W[f] = Ck[f * C::CFIELD + ci];
+              for (int f = 0; f < NC; ++f) lds_row<CXN, VEC>(Ck + f * C::CFIELD + ly * EXB + x0, Wrow[f]);
             }
           }
-          double u = 0.0;
-          if constexpr (WAVE) u = (k == 1) ? Ck[ci] : ring[k >= 2 ? k - 2 : 0][j][0];
-          const double vc = apply_point<KIND, R>(ring[k - 1][j][R], u, m, pl, W, ps);
-          // ghosts and cells outside the level-k extent keep their input value
-          const double v = (zv && ((act[j] >> k) & 1u)) ? vc : ring[k - 1][j][R];
-          if (k < BT) {
+          double urow[CXN];
+          if constexpr (WAVE) {
+            if (k == 1) lds_row<CXN, VEC>(Ck + ly * EXB + x0, urow);
+          }
 #pragma unroll
-            for (int i = 0; i < RL - 1; ++i) ring[k < BT ? k : 0][j][i] = ring[k < BT ? k : 0][j][i + 1];
-            ring[k < BT ? k : 0][j][RL - 1] = v;
-          } else if (outc[j] && c >= it.zc0 && c < it.zc1) {
-            const long long o = (long long)c * p.plane + col[j];
-            __stcs(p.dst + o, v);
-            if constexpr (WAVE && BT >= 2) __stcs(p.dstu + o, ring[BT - 1][j][R]);
+          for (int i = 0; i < CXN; ++i) {
+            double m[3][R], pl[3][R];
+#pragma unroll
+            for (int r = 1; r <= R; ++r) {
+              m[0][r - 1] = xr[RP + i - r];
+              pl[0][r - 1] = xr[RP + i + r];
+              m[1][r - 1] = ys[R + j - r][i];
+              pl[1][r - 1] = ys[R + j + r][i];
+              m[2][r - 1] = ring[k - 1][j][i][R - r];
+              pl[2][r - 1] = ring[k - 1][j][i][R + r];
+            }
+            double W[NC > 0 ? NC : 1];
+            if constexpr (NC > 0) {
+#pragma unroll
+              for (int f = 0; f < NC; ++f)
+                W[f] = (WIN && k > BT - WIN) ? cwin[L > 0 ? (BT - k) * R : 0][j][i][f] : Wrow[f][i];
+            }
+            double u = 0.0;
+            if constexpr (WAVE) u = (k == 1) ? urow[i] : ring[k >= 2 ? k - 2 : 0][j][i][0];
+            const double vc = apply_point<KIND, R>(ring[k - 1][j][i][R], u, m, pl, W, ps);
+            // ghosts and cells outside the level-k extent keep their input value
+            const double v = (zv && ((act[j][i] >> k) & 1u)) ? vc : ring[k - 1][j][i][R];
+            if (k < BT) {
+#pragma unroll
+              for (int q = 0; q < RL - 1; ++q)
+                ring[k < BT ? k : 0][j][i][q] = ring[k < BT ? k : 0][j][i][q + 1];
+              ring[k < BT ? k : 0][j][i][RL - 1] = v;
+            } else if (outc[j][i] && c >= it.zc0 && c < it.zc1) {
+              const long long o = (long long)c * p.plane + col[j] + i;
+              __stcs(p.dst + o, v);
+              if constexpr (WAVE && BT >= 2) __stcs(p.dstu + o, ring[BT - 1][j][i][R]);
+            }
           }
         }
         if (k == 1 && iv >= iv_b + R) {  // footprint plane of step iv - R fully consumed
@@ -337,17 +400,20 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CY, DV, DC, WIN, MIN
       }
       if constexpr (L > 0) {  // slide the window: drop plane s - BT*R, append plane s - (BT-WIN)*R
         // (before the item's first CLAG steps the window entry is never used; read a waited slot)
-        const double* C1 = sC + (size_t)((iv >= iv_b + CLAG ? iv - CLAG : iv) % DC) * C::CSLOT;
+        const double* C1 = sC + (size_t)((iv >= iv_b + CLAG ? iv - CLAG : iv) % DC) * C::CSLOT + SHC;
 #pragma unroll
-        for (int j = 0; j < CY; ++j) {
-          const int ci = (ly0 + j) * EXB + lx + shc;
+        for (int j = 0; j < CY; ++j)
 #pragma unroll
           for (int f = 0; f < NC; ++f) {
+            double w[CXN];
+            lds_row<CXN, VEC>(C1 + f * C::CFIELD + (ly0 + j) * EXB + x0, w);
 #pragma unroll
-            for (int i = 0; i < L - 1; ++i) cwin[i][j][f] = cwin[i + 1][j][f];
-            cwin[L - 1][j][f] = C1[f * C::CFIELD + ci];
+            for (int i = 0; i < CXN; ++i) {
+#pragma unroll
+              for (int q = 0; q < L - 1; ++q) cwin[q][j][i][f] = cwin[q + 1][j][i][f];
+              cwin[L - 1][j][i][f] = w[i];
+            }
           }
-        }
       }
       if (HAS_C && iv >= iv_b + CLAG) {  // C plane of step iv - CLAG fully consumed
         __syncwarp();
@@ -403,10 +469,10 @@ bool make_map(CUtensorMap* m, const double* base, int rank, long long pitch, lon
   return r == CUDA_SUCCESS;
 }
 
-template <int KIND, int BT, int TX, int TY, int CY, int DV, int DC, int WIN = 0, int MINB = 1>
+template <int KIND, int BT, int TX, int TY, int CX, int CY, int DV, int DC, int WIN = 0, int MINB = 1>
 cudaError_t run_pipe(const KParams& p0, int zchunk_req, int num_sms, cudaStream_t stream, LaunchInfo* info) {
-  using C = PipeCfg<KIND, BT, TX, TY, CY, DV, DC, WIN, MINB>;
-  auto kern = pipe_kernel<KIND, BT, TX, TY, CY, DV, DC, WIN, MINB>;
+  using C = PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN, MINB>;
+  auto kern = pipe_kernel<KIND, BT, TX, TY, CX, CY, DV, DC, WIN, MINB>;
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
@@ -416,7 +482,8 @@ cudaError_t run_pipe(const KParams& p0, int zchunk_req, int num_sms, cudaStream_
   KParams p = p0;
   const int planes = p.zo1 - p.zo0;
   if (planes <= 0) return cudaSuccess;
-  const int ntx = (p.nx + C::OX - 1) / C::OX, nty = (p.ny + C::OY - 1) / C::OY;
+  const int dx = (C::R - C::R * (BT - 1) + p.xoff) & 1;  // tile-grid shift of decode()
+  const int ntx = (p.nx + dx + C::OX - 1) / C::OX, nty = (p.ny + C::OY - 1) / C::OY;
   const long long tiles = (long long)ntx * nty;
   int zchunk = zchunk_req;
   if (zchunk <= 0) {
@@ -475,64 +542,56 @@ int max_pipe_bt(int kind) {
 // 128-byte lines (the interior column x = R is 128-byte aligned in the device layout).
 cudaError_t launch_pipe(int kind, int b, const KParams& p, int zchunk_req, int num_sms, int cfg,
                         cudaStream_t stream, LaunchInfo* info) {
-#define PIPE(K, B, TX, TY, CY, DV, DC) return run_pipe<K, B, TX, TY, CY, DV, DC>(p, zchunk_req, num_sms, stream, info)
-#define PIPEW(K, B, TX, TY, CY, DV, DC) return run_pipe<K, B, TX, TY, CY, DV, DC, B - 1>(p, zchunk_req, num_sms, stream, info)
-#define PIPEWN(K, B, TX, TY, CY, DV, DC, W) return run_pipe<K, B, TX, TY, CY, DV, DC, W>(p, zchunk_req, num_sms, stream, info)
-#define PIPE2(K, B, TX, TY, CY, DV, DC, W) return run_pipe<K, B, TX, TY, CY, DV, DC, W, 2>(p, zchunk_req, num_sms, stream, info)
+  // CFG(kind, BT, TX, TY, CX, CY, DV, DC, WIN, MINB)
+#define CFG(K, B, TX, TY, CX, CY, DV, DC, W, M) \
+  return run_pipe<K, B, TX, TY, CX, CY, DV, DC, W, M>(p, zchunk_req, num_sms, stream, info)
+  // Consumer-thread counts are kept at <= 224 (+ 32 producer = 256 threads) where registers matter:
+  // ptxas budgets registers for blocks rounded up to 128 threads (288-thread blocks get 168).
   switch (kind) {
     case K7C:
       switch (b) {
-        case 1: PIPE(K7C, 1, 32, 32, 4, 6, 2);
-        case 2: PIPE(K7C, 2, 32, 32, 4, 6, 2);
-        case 3: PIPE(K7C, 3, 32, 32, 4, 6, 2);
-        case 4: PIPE(K7C, 4, 32, 32, 4, 6, 2);
-        case 5: PIPE(K7C, 5, 32, 32, 4, 6, 2);
-        case 6: PIPE(K7C, 6, 32, 32, 4, 6, 2);
-        case 7: PIPE(K7C, 7, 32, 32, 4, 6, 2);
-        case 8: PIPE(K7C, 8, 32, 32, 4, 6, 2);
+        case 1: CFG(K7C, 1, 32, 28, 1, 4, 6, 2, 0, 1);
+        case 2: CFG(K7C, 2, 32, 28, 1, 4, 6, 2, 0, 1);
+        case 3: CFG(K7C, 3, 32, 28, 1, 4, 6, 2, 0, 1);
+        case 4: CFG(K7C, 4, 32, 28, 1, 4, 6, 2, 0, 1);
+        case 5: CFG(K7C, 5, 32, 28, 1, 4, 6, 2, 0, 1);
+        case 6: CFG(K7C, 6, 32, 28, 1, 4, 6, 2, 0, 1);
+        case 7: CFG(K7C, 7, 32, 28, 1, 4, 6, 2, 0, 1);
+        case 8: CFG(K7C, 8, 32, 28, 1, 4, 6, 2, 0, 1);
       }
       break;
     case K7V:
       switch (b) {
         case 1:
-          if (cfg == 1) PIPE(K7V, 1, 32, 32, 4, 4, 2);
-          if (cfg == 3) PIPE2(K7V, 1, 32, 14, 2, 4, 3, 0);
-          PIPE(K7V, 1, 32, 32, 4, 4, 3);
+          if (cfg == 1) CFG(K7V, 1, 32, 28, 2, 2, 4, 3, 0, 1);
+          CFG(K7V, 1, 32, 32, 1, 4, 4, 3, 0, 1);
         case 2:
-          if (cfg == 1) PIPE(K7V, 2, 32, 28, 4, 4, 3);
-          if (cfg == 2) PIPEW(K7V, 2, 32, 32, 4, 4, 2);
-          if (cfg == 3) PIPE2(K7V, 2, 32, 14, 2, 4, 3, 1);
-          PIPEW(K7V, 2, 32, 28, 4, 4, 3);
+          if (cfg == 1) CFG(K7V, 2, 32, 28, 2, 2, 4, 3, 1, 1);
+          if (cfg == 2) CFG(K7V, 2, 32, 28, 1, 4, 4, 3, 0, 1);
+          CFG(K7V, 2, 32, 28, 1, 4, 4, 3, 1, 1);
         case 3:
-          if (cfg == 1) PIPE(K7V, 3, 32, 20, 4, 4, 4);
-          if (cfg == 2) PIPEWN(K7V, 3, 32, 32, 4, 4, 2, 2);
-          if (cfg == 3) PIPE2(K7V, 3, 32, 14, 2, 4, 2, 2);
-          if (cfg == 4) PIPE2(K7V, 3, 32, 12, 2, 4, 2, 2);
-          if (cfg == 5) PIPE2(K7V, 3, 32, 14, 2, 4, 3, 1);
-          if (cfg == 6) PIPEWN(K7V, 3, 32, 20, 4, 4, 4, 1);
-          if (cfg == 7) PIPEWN(K7V, 3, 32, 24, 4, 5, 3, 1);
-          PIPEWN(K7V, 3, 32, 28, 4, 4, 3, 1);
+          if (cfg == 1) CFG(K7V, 3, 32, 28, 2, 2, 4, 3, 1, 1);
+          if (cfg == 2) CFG(K7V, 3, 32, 20, 1, 4, 4, 4, 0, 1);
+          CFG(K7V, 3, 32, 28, 1, 4, 4, 3, 1, 1);
       }
       break;
     case K25W:
       if (b == 1) {
-        if (cfg == 1) PIPE(K25W, 1, 32, 32, 4, 7, 3);
-        if (cfg == 2) PIPE(K25W, 1, 32, 56, 8, 7, 3);
-        if (cfg == 3) PIPE2(K25W, 1, 32, 14, 2, 7, 3, 0);
-        PIPE(K25W, 1, 64, 16, 4, 7, 3);
+        if (cfg == 1) CFG(K25W, 1, 64, 14, 4, 1, 7, 3, 0, 1);
+        if (cfg == 2) CFG(K25W, 1, 32, 28, 2, 2, 7, 3, 0, 1);
+        if (cfg == 3) CFG(K25W, 1, 64, 14, 2, 2, 7, 3, 0, 1);
+        CFG(K25W, 1, 64, 16, 1, 4, 7, 3, 0, 1);
       }
       break;
     case K25V:
       if (b == 1) {
-        if (cfg == 1) PIPE(K25V, 1, 32, 16, 4, 6, 3);
-        PIPE(K25V, 1, 64, 8, 2, 6, 3);
+        if (cfg == 1) CFG(K25V, 1, 64, 8, 2, 2, 6, 3, 0, 1);
+        if (cfg == 2) CFG(K25V, 1, 64, 8, 4, 1, 6, 3, 0, 1);
+        CFG(K25V, 1, 64, 8, 1, 2, 6, 3, 0, 1);
       }
       break;
   }
-#undef PIPE
-#undef PIPEW
-#undef PIPEWN
-#undef PIPE2
+#undef CFG
   return cudaErrorInvalidValue;
 }
 
