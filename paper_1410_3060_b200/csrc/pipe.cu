@@ -570,24 +570,24 @@ cudaError_t launch_pipe(int kind, int b, const KParams& p, int zchunk_req, int n
           if (cfg == 2) CFG(K7V, 2, 32, 28, 1, 4, 4, 3, 0, 1);
           CFG(K7V, 2, 32, 28, 1, 4, 4, 3, 1, 1);
         case 3:
-          if (cfg == 1) CFG(K7V, 3, 32, 28, 2, 2, 4, 3, 1, 1);
+          if (cfg == 1) CFG(K7V, 3, 32, 28, 1, 4, 4, 3, 1, 1);
           if (cfg == 2) CFG(K7V, 3, 32, 20, 1, 4, 4, 4, 0, 1);
-          CFG(K7V, 3, 32, 28, 1, 4, 4, 3, 1, 1);
+          CFG(K7V, 3, 32, 28, 2, 2, 4, 3, 1, 1);
       }
       break;
     case K25W:
       if (b == 1) {
         if (cfg == 1) CFG(K25W, 1, 64, 14, 4, 1, 7, 3, 0, 1);
         if (cfg == 2) CFG(K25W, 1, 32, 28, 2, 2, 7, 3, 0, 1);
-        if (cfg == 3) CFG(K25W, 1, 64, 14, 2, 2, 7, 3, 0, 1);
-        CFG(K25W, 1, 64, 16, 1, 4, 7, 3, 0, 1);
+        if (cfg == 3) CFG(K25W, 1, 64, 16, 1, 4, 7, 3, 0, 1);
+        CFG(K25W, 1, 64, 14, 2, 2, 7, 3, 0, 1);
       }
       break;
     case K25V:
       if (b == 1) {
-        if (cfg == 1) CFG(K25V, 1, 64, 8, 2, 2, 6, 3, 0, 1);
+        if (cfg == 1) CFG(K25V, 1, 64, 8, 1, 2, 6, 3, 0, 1);
         if (cfg == 2) CFG(K25V, 1, 64, 8, 4, 1, 6, 3, 0, 1);
-        CFG(K25V, 1, 64, 8, 1, 2, 6, 3, 0, 1);
+        CFG(K25V, 1, 64, 8, 2, 2, 6, 3, 0, 1);
       }
       break;
   }

@@ -125,6 +125,18 @@ def test_degenerate_extents(kind):
             assert_parity(kind, g_new, g_old, o_new, o_old, inp.R, 1e-13, inputs=inp)
 
 
+def test_repeatable_bitwise():
+    """Five identical runs of a multi-tile, multi-chunk case give bitwise identical results: a race in
+    the TMA/mbarrier rings or the shared level planes would show up as run-to-run differences
+    (compute-sanitizer is not available on this pool)."""
+    for kind in KINDS:
+        nx, ny, nz = (96, 80, 70) if synth.RADIUS[kind] == 1 else (150, 60, 70)
+        ref = gpu_run(kind, nx, ny, nz, 9, seed=13, zchunk=8)
+        for _ in range(4):
+            got = gpu_run(kind, nx, ny, nz, 9, seed=13, zchunk=8)
+            assert np.array_equal(got[0], ref[0])
+
+
 def test_checkpoint_resume_bitwise():
     """run(T1); read; create from the read state; run(T2) == run(T1 + T2), bitwise (all kinds)."""
     for kind in KINDS:
