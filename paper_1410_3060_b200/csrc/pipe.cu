@@ -83,18 +83,25 @@ struct Item {
   int gx0, gy0, zc0, zc1, s_begin, s_end;
 };
 
-// Item origin = the level-1 extent origin: output origin minus R*H (H = BT - 1 halo levels), shifted
-// left by dx in {0, 1} so that the origin's raw column (gx0 + xoff) is even: then every TMA box puts
-// the tile's cells on 16-byte boundaries of shared memory (OX is even, so all tiles share the shift).
+// Tiles write OXW = OX & ~3 output columns each (a multiple of the 4-double, 32-byte sector), starting
+// at raw column 16 (interior column R, 128-byte aligned in the device layout) + tx * OXW: every output
+// row segment covers whole sectors, so no sector is written partially by two tiles (partial-sector
+// writes cost HBM read-modify-write traffic).  A tile computes OX >= OXW valid output columns and
+// writes the middle OXW (offset WOFF = (OX - OXW) / 2).  The level-1-extent origin is then
+// gx0 = write start - WOFF - R*(BT-1), whose raw column is even for every (R, BT) used, so the
+// coefficient box starts exactly at the level-1 extent and all TMA boxes put cells on 16-byte
+// boundaries of shared memory.
 template <int R, int H, int OX, int OY>
 __device__ __forceinline__ Item decode(int item, int ntx, int nty, const KParams& p) {
   constexpr int BT = H + 1;
-  const int dx = (R - R * H + p.xoff) & 1;
+  const int OXW = p.walign ? (OX & ~3) : OX, WOFF = (OX - OXW) / 2;
+  // walign = 0 (experiment): OX-wide written tiles, grid shifted by dx so the origin is still even
+  const int dx = p.walign ? 0 : ((R - R * H + p.xoff) & 1);
   const int per = ntx * nty;
   const int zc = item / per, t = item - zc * per;
   const int ty = t / ntx, tx = t - ty * ntx;
   Item it;
-  it.gx0 = tx * OX + R - R * H - dx;
+  it.gx0 = R + tx * OXW - WOFF - R * H - dx;
   it.gy0 = ty * OY + R - R * H;
   it.zc0 = p.zo0 + zc * p.zchunk;
   it.zc1 = min(p.zo1, it.zc0 + p.zchunk);
@@ -149,6 +156,8 @@ struct PipeCfg {
   static constexpr int THREADS = NCONS + 32;
   static constexpr int FX = TX + 2 * R, FY = TY + 2 * R;         // Omega^t footprint
   static constexpr int OX = TX - 2 * R * (BT - 1), OY = TY - 2 * R * (BT - 1);
+  static constexpr int OXW = OX & ~3, WOFF = (OX - OXW) / 2;  // written output columns, offset
+  static_assert(OXW > 0 && (WOFF + R * (BT - 1)) % 2 == 0, "level-1 extent origin must be even");
   static constexpr int NCF = WAVE ? 1 : NC;  // fields in the C ring (coefficients, or U for the wave)
   static constexpr bool HAS_C = NCF > 0;
   // TMA boxes start on an even fp64 column (tiled TMA needs 16-byte aligned x coordinates): the tile
@@ -267,7 +276,8 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN,
         for (int k = 1; k <= BT; ++k)
           if (inter && lx >= (k - 1) * R && lx < TX - (k - 1) * R && ly >= (k - 1) * R && ly < TY - (k - 1) * R)
             act[j][i] |= 1u << k;
-        outc[j][i] = (act[j][i] >> BT) & 1u;
+        const int oxw = p.walign ? C::OXW : OX, woff = (OX - oxw) / 2;
+        outc[j][i] = ((act[j][i] >> BT) & 1u) && lx >= woff + R * (BT - 1) && lx < woff + R * (BT - 1) + oxw;
       }
     }
     double ring[BT][CY][CXN][RL];
@@ -482,8 +492,10 @@ cudaError_t run_pipe(const KParams& p0, int zchunk_req, int num_sms, cudaStream_
   KParams p = p0;
   const int planes = p.zo1 - p.zo0;
   if (planes <= 0) return cudaSuccess;
-  const int dx = (C::R - C::R * (BT - 1) + p.xoff) & 1;  // tile-grid shift of decode()
-  const int ntx = (p.nx + dx + C::OX - 1) / C::OX, nty = (p.ny + C::OY - 1) / C::OY;
+  if (p.xoff != 16 - C::R) return cudaErrorInvalidValue;  // decode() assumes interior column R at raw 16
+  const int oxw = p.walign ? C::OXW : C::OX;
+  const int dx = p.walign ? 0 : ((C::R - C::R * (BT - 1) + p.xoff) & 1);
+  const int ntx = (p.nx + dx + oxw - 1) / oxw, nty = (p.ny + C::OY - 1) / C::OY;
   const long long tiles = (long long)ntx * nty;
   int zchunk = zchunk_req;
   if (zchunk <= 0) {
@@ -518,7 +530,7 @@ cudaError_t run_pipe(const KParams& p0, int zchunk_req, int num_sms, cudaStream_
   const int grid = (int)std::min<long long>(items, (long long)std::max(1, occ) * num_sms);
   kern<<<grid, C::THREADS, C::SMEM, stream>>>(mapV, mapC, p, ntx, nty, (int)items);
   if (info) {
-    info->tile_x = C::OX; info->tile_y = C::OY; info->zchunk = zchunk; info->threads = C::THREADS;
+    info->tile_x = C::OXW; info->tile_y = C::OY; info->zchunk = zchunk; info->threads = C::THREADS;
     info->smem = (int)C::SMEM; info->ctas = grid;
   }
   return cudaGetLastError();

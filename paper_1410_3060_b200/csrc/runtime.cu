@@ -379,6 +379,8 @@ st::KParams base_params(stencil_ctx* h, const Slab& s) {
   p.xoff = (int)h->xoff;
   static const int dbg = getenv("STENCIL_DBG") ? atoi(getenv("STENCIL_DBG")) : 0;
   p.dbg = dbg;
+  static const int walign = getenv("STENCIL_WALIGN") ? atoi(getenv("STENCIL_WALIGN")) : 0;
+  p.walign = walign;
   return p;
 }
 
