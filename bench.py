@@ -188,6 +188,9 @@ def main():
     ap.add_argument("--bt", type=int, default=0)
     ap.add_argument("--variant", type=int, default=0)
     ap.add_argument("--zchunk", type=int, default=0)
+    ap.add_argument("--slabs", type=int, default=1,
+                    help="single GPU only: run the z-slab plan with this many slabs on the one device "
+                         "(loopback halo copies; measures the multi-GPU plan's overhead)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -218,8 +221,13 @@ def main():
         if world > 1:
             dist.barrier()
 
-    g = st.Grid(w.kind, w.nx, w.ny, w.nz, seed=synth.DEFAULT_SEED, variant=args.variant, bt=args.bt,
-                zchunk=args.zchunk, rank=rank, nranks=world, nccl_id=nccl_id)
+    slabs = args.slabs if world == 1 else 1
+    if slabs > 1:
+        g = st.Grid(w.kind, w.nx, w.ny, w.nz, seed=synth.DEFAULT_SEED, variant=args.variant, bt=args.bt,
+                    zchunk=args.zchunk, nranks=slabs, local_slabs=slabs)
+    else:
+        g = st.Grid(w.kind, w.nx, w.ny, w.nz, seed=synth.DEFAULT_SEED, variant=args.variant, bt=args.bt,
+                    zchunk=args.zchunk, rank=rank, nranks=world, nccl_id=nccl_id)
     stream = g.stream
     for _ in range(args.warmup):
         g.run(w.T)
@@ -326,7 +334,8 @@ def main():
             "config": {"workload": w.name, "kind": synth.KIND_NAMES[w.kind], "nx": w.nx, "ny": w.ny,
                        "nz": w.nz, "T": w.T, "bt": bt, "variant": info["variant"],
                        "tile": [info["tile_x"], info["tile_y"]], "zchunk": info["zchunk"],
-                       "parallelism": f"z-slab x{world}" if world > 1 else "single GPU",
+                       "parallelism": (f"z-slab x{world} (NCCL)" if world > 1 else
+                                       f"loopback z-slab x{slabs} on 1 GPU" if slabs > 1 else "single GPU"),
                        "l2": "inputs larger than L2 (no flush needed)",
                        "luops_per_step": w.nx * w.ny * w.nz * w.T},
             "roofline": roofline,
