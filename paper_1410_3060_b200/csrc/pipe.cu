@@ -226,6 +226,7 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN,
       if (HAS_C) asm volatile("prefetch.tensormap [%0];" ::"l"(&mapC) : "memory");
       uint32_t iv = 0;
       for (int item = blockIdx.x; item < items; item += gridDim.x) {
+        if ((p.dbg & 8) && item == 0) continue;
         const Item it = decode<R, BT - 1, OX, OY>(item, ntx, nty, p);
         const int xv = (it.gx0 - R + p.xoff) & ~1;  // footprint box
         const int xc = (it.gx0 + p.xoff) & ~1;      // level-1 extent box
@@ -259,6 +260,7 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN,
   uint32_t iv = 0;
 
   for (int item = blockIdx.x; item < items; item += gridDim.x) {
+    if ((p.dbg & 8) && item == 0) continue;
     const Item it = decode<R, BT - 1, OX, OY>(item, ntx, nty, p);
     bool outc[CY][CXN];
     unsigned act[CY][CXN];  // bit k: cell is interior and inside the level-k extent (computed at level k)
@@ -396,7 +398,7 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN,
               for (int q = 0; q < RL - 1; ++q)
                 ring[k < BT ? k : 0][j][i][q] = ring[k < BT ? k : 0][j][i][q + 1];
               ring[k < BT ? k : 0][j][i][RL - 1] = v;
-            } else if (outc[j][i] && c >= it.zc0 && c < it.zc1) {
+            } else if (outc[j][i] && c >= it.zc0 && c < it.zc1 && !((p.dbg & 4) && c == it.zc1 - 1)) {
               const long long o = (long long)c * p.plane + col[j] + i;
               __stcs(p.dst + o, v);
               if constexpr (WAVE && BT >= 2) __stcs(p.dstu + o, ring[BT - 1][j][i][R]);

@@ -193,6 +193,12 @@ void release(stencil_ctx* h) {
   h->ev_edge = h->ev_halo = nullptr;
 }
 
+// Debug / fault-injection knobs, read at every call so tests can toggle them (never set in production).
+int env_int(const char* name) {
+  const char* v = getenv(name);
+  return v ? atoi(v) : 0;
+}
+
 int default_bt(int kind) {
   switch (kind) {
     case ST_7PT_CONST: return 4;  // tools/sweep.py on B200
@@ -377,8 +383,7 @@ st::KParams base_params(stencil_ctx* h, const Slab& s) {
   for (int i = 0; i < 6; ++i) p.s[i] = h->scal[i];
   p.coef_raw = s.coef;
   p.xoff = (int)h->xoff;
-  static const int dbg = getenv("STENCIL_DBG") ? atoi(getenv("STENCIL_DBG")) : 0;
-  p.dbg = dbg;
+  p.dbg = env_int("STENCIL_DBG") | (env_int("STENCIL_FAULT") & 12);
   static const int walign = getenv("STENCIL_WALIGN") ? atoi(getenv("STENCIL_WALIGN")) : 0;
   p.walign = walign;
   return p;
@@ -400,6 +405,7 @@ cudaEvent_t timing_begin(stencil_ctx* h, cudaEvent_t* end) {
 
 // Halo exchange of `depth` planes of buffer b after a block.
 int exchange(stencil_ctx* h, int b, int64_t depth, cudaStream_t cs) {
+  if (env_int("STENCIL_FAULT") & 1) depth -= 1;  // fault injection: halo one plane too shallow
   if (h->nranks == 1 || depth <= 0) return ST_OK;
   const size_t cnt = (size_t)(depth * h->plane);
   if (h->local > 1) {
