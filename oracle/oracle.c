@@ -20,6 +20,8 @@
  *     O^{t+1} = 2*O^t - O^{t-1} + alpha*[w0*O^t + sum_{r=1..4} w_r*((x pair_r)+(y pair_r)+(z pair_r))]
  *     O^{t+1} overwrites the buffer that held O^{t-1} (line 126-128; each point reads its own
  *     O^{t-1} before writing it).
+ *   kind 5, the same wave with the domain-sized alpha_{z,y,x} exactly as Fig. 1e prints it (
+ *     SURVEY.md NEXT-1): alpha is one padded coefficient field, w0..w4 scalars.
  *   kind 4, 25-point variable, axis-symmetric (Fig. 1d):
  *     O' = W0*O + sum_{r=1..4} [ W_{3r-2}*(x pair_r) + W_{3r-1}*(y pair_r) + W_{3r}*(z pair_r) ]
  *
@@ -45,13 +47,13 @@
 static int radius_of(int kind) {
   switch (kind) {
     case 1: case 2: return 1;
-    case 3: case 4: return 4;
+    case 3: case 4: case 5: return 4;
     default: return -1;
   }
 }
 
-static int ncoef_of(int kind) { return kind == 2 ? 7 : kind == 4 ? 13 : 0; }
-static int nscal_of(int kind) { return kind == 1 ? 2 : kind == 3 ? 6 : 0; }
+static int ncoef_of(int kind) { return kind == 2 ? 7 : kind == 4 ? 13 : kind == 5 ? 1 : 0; }
+static int nscal_of(int kind) { return kind == 1 ? 2 : kind == 3 ? 6 : kind == 5 ? 5 : 0; }
 
 /* One sweep of kind 1 (Fig. 1b): dst <- F(src) over the interior. */
 static void sweep_7c(int64_t nx, int64_t ny, int64_t nz, const double *src, double *dst,
@@ -111,6 +113,27 @@ static void sweep_25w(int64_t nx, int64_t ny, int64_t nz, const double *cur, dou
       }
 }
 
+/* One step of kind 5 (Fig. 1e with alpha_{z,y,x}): as kind 3, alpha read from the field A at the point.
+ * s[0] = w0, s[1..4] = w1..w4. */
+static void sweep_25wa(int64_t nx, int64_t ny, int64_t nz, const double *cur, double *prev,
+                       const double *s, const double *A) {
+  const int64_t X = nx + 8, Y = ny + 8;
+  const int64_t sy = X, sz = X * Y;
+  const double w0 = s[0], w1 = s[1], w2 = s[2], w3 = s[3], w4 = s[4];
+#pragma omp parallel for schedule(static)
+  for (int64_t z = 4; z < nz + 4; ++z)
+    for (int64_t y = 4; y < ny + 4; ++y)
+      for (int64_t x = 4; x < nx + 4; ++x) {
+        const int64_t p = z * sz + y * sy + x;
+        const double *c = cur;
+        prev[p] = 2.0 * c[p] - prev[p] + A[p] * (w0 * c[p]
+          + w1 * ((c[p - 1] + c[p + 1]) + (c[p - sy] + c[p + sy]) + (c[p - sz] + c[p + sz]))
+          + w2 * ((c[p - 2] + c[p + 2]) + (c[p - 2 * sy] + c[p + 2 * sy]) + (c[p - 2 * sz] + c[p + 2 * sz]))
+          + w3 * ((c[p - 3] + c[p + 3]) + (c[p - 3 * sy] + c[p + 3 * sy]) + (c[p - 3 * sz] + c[p + 3 * sz]))
+          + w4 * ((c[p - 4] + c[p + 4]) + (c[p - 4 * sy] + c[p + 4 * sy]) + (c[p - 4 * sz] + c[p + 4 * sz])));
+      }
+}
+
 /* One sweep of kind 4 (Fig. 1d).  W[0] centre; W[1+3(r-1)+a] for radius r, axis a = x,y,z. */
 static void sweep_25v(int64_t nx, int64_t ny, int64_t nz, const double *src, double *dst,
                       const double *const *W) {
@@ -141,9 +164,10 @@ static void sweep_25v(int64_t nx, int64_t ny, int64_t nz, const double *src, dou
 /*
  * Advance (V, U) by T time steps.  V, U: padded arrays of (nz+2R)(ny+2R)(nx+2R) doubles.
  *   Jacobi kinds (1, 2, 4): V holds Omega^0; U's interior is scratch (its ghosts must equal V's).
- *   Wave kind (3):          V holds Omega^0, U holds Omega^{-1}.
+ *   Wave kinds (3, 5):      V holds Omega^0, U holds Omega^{-1}.
  * On return V = Omega^T and U = Omega^{T-1}.  coef: ncoef padded fields (kinds 2, 4), else unused.
- * scalars: (w1, w2) for kind 1; (w0, w1, w2, w3, w4, alpha) for kind 3.
+ * scalars: (w1, w2) for kind 1; (w0, w1, w2, w3, w4, alpha) for kind 3; (w0, .., w4) for kind 5,
+ * whose coef[0] is the alpha field.
  * nthreads <= 0: OpenMP default.  Returns 0, -1 (bad argument), -2 (no memory).
  */
 int oracle_run(int kind, int64_t nx, int64_t ny, int64_t nz, double *V, double *U,
@@ -167,6 +191,7 @@ int oracle_run(int kind, int64_t nx, int64_t ny, int64_t nz, double *V, double *
       case 2: sweep_7v(nx, ny, nz, cur, nxt, coef); break;
       case 3: sweep_25w(nx, ny, nz, cur, nxt, scalars); break;
       case 4: sweep_25v(nx, ny, nz, cur, nxt, coef); break;
+      case 5: sweep_25wa(nx, ny, nz, cur, nxt, scalars, coef[0]); break;
     }
     double *tmp = cur; cur = nxt; nxt = tmp;  /* swap: t in {0,1} */
   }

@@ -18,17 +18,22 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "libsynth.so")
 
 # Stencil kinds (SURVEY.md §8(b) numbering; Fig. 1b/1c/1e/1d).
-K7C, K7V, K25W, K25V = 1, 2, 3, 4
-KIND_NAMES = {K7C: "7pt-const", K7V: "7pt-var", K25W: "25pt-wave", K25V: "25pt-var"}
-RADIUS = {K7C: 1, K7V: 1, K25W: 4, K25V: 4}
-N_COEF_FIELDS = {K7C: 0, K7V: 7, K25W: 0, K25V: 13}
-N_SCALARS = {K7C: 2, K7V: 0, K25W: 6, K25V: 0}
-# U[0, c) scale of the coefficient fields (BASELINE.json configs 2, 4, 5).
-COEF_SCALE = {K7V: 1.0 / 7.0, K25V: 1.0 / 25.0}
+K7C, K7V, K25W, K25V, K25WA = 1, 2, 3, 4, 5
+KIND_NAMES = {K7C: "7pt-const", K7V: "7pt-var", K25W: "25pt-wave", K25V: "25pt-var",
+              K25WA: "25pt-wave-alpha-field"}
+RADIUS = {K7C: 1, K7V: 1, K25W: 4, K25V: 4, K25WA: 4}
+N_COEF_FIELDS = {K7C: 0, K7V: 7, K25W: 0, K25V: 13, K25WA: 1}
+N_SCALARS = {K7C: 2, K7V: 0, K25W: 6, K25V: 0, K25WA: 5}
+WAVE_KINDS = (K25W, K25WA)
+# U[0, c) scale of the coefficient fields (BASELINE.json configs 2, 4, 5).  The alpha field of the
+# NEXT-1 wave (Fig. 1e as printed, not a BASELINE.json config) is drawn from U[0, 0.2): the leapfrog
+# update is stable for alpha * max|Laplacian symbol| = alpha * 19.505 < 4, i.e. alpha < 0.205.
+COEF_SCALE = {K7V: 1.0 / 7.0, K25V: 1.0 / 25.0, K25WA: 0.2}
 
 # Scalar weights of the constant kinds (BASELINE.json configs 1 and 3; reading Q3).
 SCALARS_7C = (0.4, 0.1)  # w_c (centre), w_n (each neighbour)
 SCALARS_25W = (3.0 * (-205.0 / 72.0), 8.0 / 5.0, -1.0 / 5.0, 8.0 / 315.0, -1.0 / 560.0, 0.1)  # w0,a1..a4,alpha
+SCALARS_25WA = SCALARS_25W[:5]  # w0, w1..w4 (alpha is a field)
 
 DEFAULT_SEED = 14103060  # reading Q7
 
@@ -138,7 +143,7 @@ def make_inputs(kind: int, nx: int, ny: int, nz: int, seed: int = DEFAULT_SEED, 
         box = tuple((0, d) for d in dims)
     V = fill_box(seed, STREAM_V, dims, box)
     U = V.copy()
-    if kind == K25W:
+    if kind in WAVE_KINDS:
         # interior of the global grid intersected with the box
         lo = [max(b[0], R) for b in box]
         hi = [min(b[1], d - R) for b, d in zip(box, dims)]
@@ -151,5 +156,5 @@ def make_inputs(kind: int, nx: int, ny: int, nz: int, seed: int = DEFAULT_SEED, 
         c = COEF_SCALE[kind]
         coef = [fill_box(seed, stream_w(i), dims, box, scale=c) for i in range(N_COEF_FIELDS[kind])]
     if scalars is None:
-        scalars = {K7C: SCALARS_7C, K25W: SCALARS_25W}.get(kind, ())
+        scalars = {K7C: SCALARS_7C, K25W: SCALARS_25W, K25WA: SCALARS_25WA}.get(kind, ())
     return Inputs(kind, nx, ny, nz, V, U, coef, tuple(scalars))

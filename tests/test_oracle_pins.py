@@ -421,3 +421,67 @@ def test_run_cone_matches_full_run():
         new, old = oracle.run_cone(kind, *n, cells, T, seed=12)
         assert np.array_equal(new, np.array([full_new[c] for c in cells]))
         assert np.array_equal(old, np.array([full_old[c] for c in cells]))
+
+
+# ---------------------------------------------------------------- kind 5: Fig. 1e with alpha_{z,y,x}
+K25WA = synth.K25WA
+
+
+def test_P8_alpha_field_constant_equals_scalar_wave():
+    """A constant alpha field reproduces the scalar-alpha wave bitwise (same expression)."""
+    inp = synth.make_inputs(K25W, 7, 6, 9, seed=3)
+    o3, p3 = oracle.run(inp, 6)
+    A = np.full(inp.V.shape, synth.SCALARS_25W[5])
+    o5, p5 = oracle.run(mk(K25WA, 7, 6, 9, inp.V, inp.U, coef=[A], scalars=synth.SCALARS_25WA), 6)
+    assert np.array_equal(o5, o3) and np.array_equal(p5, p3)
+
+
+def test_P1f_alpha_field_hand_point():
+    """V centre 1, U centre 0.5, V(axis, +-r) = r, alpha(centre) = 0.25 (dyadic), other alpha cells
+    arbitrary: 1.5 + 0.25 * (w0 + 6 * sum_r r w_r), to 2 ulp."""
+    V = star_grid(4, 1.0, lambda a, r: float(r), lambda a, r: float(r))
+    U = V.copy()
+    U[4, 4, 4] = 0.5
+    A = np.full(V.shape, 7.0)
+    A[4, 4, 4] = 0.25
+    new, _ = oracle.run(mk(K25WA, 1, 1, 1, V, U, coef=[A], scalars=synth.SCALARS_25WA), 1)
+    w0, w1, w2, w3, w4 = (Fraction(x) for x in synth.SCALARS_25WA)
+    exact = Fraction(3, 2) + Fraction(1, 4) * (w0 + 6 * (1 * w1 + 2 * w2 + 3 * w3 + 4 * w4))
+    assert ulps(new[4, 4, 4], float(exact)) <= 2
+
+
+def test_P4_alpha_field_exact_rational():
+    inp = synth.make_inputs(K25WA, 5, 4, 3, seed=8)
+    T = 4
+    o_new, o_old = oracle.run(inp, T)
+    F = np.vectorize(Fraction, otypes=[object])
+    cur, prev, A = F(inp.V), F(inp.U), F(inp.coef[0])
+    w = [Fraction(x) for x in inp.scalars]
+    R, sh = 4, inp.V.shape
+    for _ in range(T):
+        nxt = prev.copy()
+        for z, y, x in itertools.product(range(R, sh[0] - R), range(R, sh[1] - R), range(R, sh[2] - R)):
+            L = w[0] * cur[z, y, x]
+            for r in range(1, 5):
+                L += w[r] * (cur[z, y, x - r] + cur[z, y, x + r] + cur[z, y - r, x] + cur[z, y + r, x]
+                             + cur[z - r, y, x] + cur[z + r, y, x])
+            nxt[z, y, x] = 2 * cur[z, y, x] - prev[z, y, x] + A[z, y, x] * L
+        prev, cur = cur, nxt
+    for o, e in ((o_new, cur), (o_old, prev)):
+        ef = e.astype(np.float64)
+        assert np.max(np.abs(o - ef)) / np.max(np.abs(ef)) <= 2 * T * 25 * U_RND * 8
+
+
+def test_P9_alpha_field_locality_and_linearity():
+    n = 17
+    inp = synth.make_inputs(K25WA, n, n, n, seed=2)
+    a, _ = oracle.run(inp, 2)
+    p = (12, 12, 12)
+    V = inp.V.copy(); V[p] += 1.0
+    b, _ = oracle.run(mk(K25WA, n, n, n, V, inp.U, inp.coef, inp.scalars), 2)
+    m = n + 8
+    z, y, x = np.meshgrid(np.arange(m), np.arange(m), np.arange(m), indexing="ij")
+    reach = sum(np.ceil(np.abs(c - pc) / 4) for c, pc in zip((z, y, x), p)) <= 2
+    assert np.array_equal(a != b, reach)
+    c2, _ = oracle.run(mk(K25WA, n, n, n, 2 * inp.V, 2 * inp.U, inp.coef, inp.scalars), 2)
+    assert np.array_equal(c2, 2 * a)
