@@ -35,12 +35,12 @@ METRIC = "GLUP/s"
 # compulsory HBM bytes per lattice cell per fused block of b levels:
 # state read once + written once per block, coefficients read once per block, no write-allocate.
 def block_bytes_per_cell(kind, b):
-    if kind == synth.K25W:
-        return 24 if b == 1 else 32  # b = 1: read V, U, write U in place; b >= 2: both levels in & out
+    if kind in synth.WAVE_KINDS:  # b = 1: read V, U, write U in place; b >= 2: both levels in & out
+        return (24 if b == 1 else 32) + 8 * synth.N_COEF_FIELDS[kind]
     return 16 + 8 * synth.N_COEF_FIELDS[kind]
 
 
-FLOPS_PER_LUP = {synth.K7C: 8, synth.K7V: 13, synth.K25W: 30, synth.K25V: 37}
+FLOPS_PER_LUP = {synth.K7C: 8, synth.K7V: 13, synth.K25W: 30, synth.K25V: 37, synth.K25WA: 30}
 
 
 def load_peaks():
@@ -104,7 +104,8 @@ class ClockSampler:
 
 
 def pick_workload(name, n_gpus):
-    w = workloads.BY_NAME.get(name) or {x.name.split("-")[0]: x for x in workloads.CONFIGS}.get(name)
+    w = workloads.BY_NAME.get(name) or {x.name.split("-")[0]: x
+                                        for x in workloads.CONFIGS + workloads.EXTRA}.get(name)
     if w is None:
         raise SystemExit(f"unknown workload {name}")
     if n_gpus > 1:
@@ -292,11 +293,11 @@ def main():
         inp = synth.make_inputs(w.kind, w.nx, w.ny, w.nz)
         pin = lambda a: torch.from_numpy(a).pin_memory().numpy()  # noqa: E731
         V = pin(inp.V)
-        U = pin(inp.U) if w.kind == synth.K25W else None
-        coeff = [pin(c) for c in inp.coef] if inp.coef else list(inp.scalars)
+        U = pin(inp.U) if w.kind in synth.WAVE_KINDS else None
+        coeff = list(inp.scalars) + [pin(c) for c in inp.coef]
         out = pin(np.empty_like(inp.V))
         del inp
-        h2d = V.nbytes + (U.nbytes if U is not None else 0) + (sum(c.nbytes for c in coeff) if w.kind in (synth.K7V, synth.K25V) else 0)
+        h2d = V.nbytes + (U.nbytes if U is not None else 0) + sum(c.nbytes for c in coeff if hasattr(c, "nbytes"))
         d2h = out.nbytes if world == 1 else out.nbytes // world
 
         def e2e_step():

@@ -14,6 +14,7 @@
  *                 with a scalar alpha (reading Q2)
  *   ST_25PT_VAR   Fig. 1d: O' = W0*O + sum_{r=1..4} sum_{axis} W_{1+3(r-1)+axis}*(pair)
  *                                                                           (13 domain-sized fields)
+ *   ST_25PT_WAVE_A  Fig. 1e with the domain-sized alpha_{z,y,x} as printed: one field
  *
  * Grid and layout: arrays are indexed [z][y][x], x fastest, over the PADDED extent
  * (nz+2R) x (ny+2R) x (nx+2R), R = 1 (7-point) or 4 (25-point).  The outer shell of width R is the
@@ -54,7 +55,9 @@ typedef enum {
   ST_7PT_CONST = 1, /* Fig. 1b */
   ST_7PT_VAR = 2,   /* Fig. 1c */
   ST_25PT_WAVE = 3, /* Fig. 1e, scalar alpha */
-  ST_25PT_VAR = 4   /* Fig. 1d */
+  ST_25PT_VAR = 4,  /* Fig. 1d */
+  ST_25PT_WAVE_A = 5 /* Fig. 1e exactly as printed: alpha_{z,y,x} a domain-sized field (SURVEY
+                        NEXT-1); w0..w4 scalars */
 } st_kind;
 
 enum {
@@ -123,12 +126,13 @@ void stencil_opts_default(st_opts *o);
  * (nz+2R)*(ny+2R)*(nx+2R) doubles in the GLOBAL layout (every rank passes the global arrays and
  * copies its slab; the library copies everything before returning; the caller keeps ownership).
  *   v0      : Omega^0, ghosts included (fixed boundary values).
- *   u0      : ST_25PT_WAVE only: Omega^{-1}; only its interior is used (ghosts come from v0).
+ *   u0      : wave kinds (3, 5) only: Omega^{-1}; only its interior is used (ghosts come from v0).
  *             Other kinds: must be NULL.
  *   coeff   : n_coeff pointers.  ST_7PT_CONST: 2 pointers to one double each (w1 centre, w2
  *             neighbour).  ST_25PT_WAVE: 6 pointers to one double each (w0, w1, w2, w3, w4, alpha).
  *             ST_7PT_VAR: 7 padded fields W0..W6.  ST_25PT_VAR: 13 padded fields W0..W12 in
- *             Fig. 1c / 1d numbering.  Only the interior cells of a field are read.
+ *             Fig. 1c / 1d numbering.  ST_25PT_WAVE_A: 6 pointers, w0..w4 (one double each) then
+ *             the padded alpha field.  Only the interior cells of a field are read.
  *   opts    : NULL = defaults.
  * Errors: ST_E_INVAL (kind, extent < 1, n_coeff, NULL, nz < nranks, rank out of range),
  *         ST_E_NOMEM, ST_E_CUDA, ST_E_NCCL.
@@ -142,9 +146,10 @@ int stencil_create(stencil_ctx **out, int kind, int64_t nx, int64_t ny, int64_t 
  * (reading Q6): V^0 and ghosts ~ U[-1,1) (stream 0); wave
  * Omega^{-1} interior ~ U[-1,1) (stream 1); W_i ~ U[0,1/7) or U[0,1/25) (stream 2+i).  The draw is
  * a function of the global padded index, so every rank fills its own slab without communication.
- *   scalars : constant kinds: 2 (7-point) or 6 (wave) doubles in the order of stencil_create's coeff;
- *             NULL = the BASELINE.json values (0.4, 0.1) / (3*(-205/72), 8/5, -1/5, 8/315, -1/560,
- *             0.1).  Variable kinds: must be NULL.
+ * ST_25PT_WAVE_A's alpha field ~ U[0, 0.2) (stream 2; the leapfrog is stable for alpha < 0.205).
+ *   scalars : constant kinds: 2 (7-point) or 6 (wave) doubles in the order of stencil_create's coeff,
+ *             ST_25PT_WAVE_A: 5 (w0..w4); NULL = the BASELINE.json values (0.4, 0.1) /
+ *             (3*(-205/72), 8/5, -1/5, 8/315, -1/560, 0.1).  Variable kinds 2, 4: must be NULL.
  */
 int stencil_create_seeded(stencil_ctx **out, int kind, int64_t nx, int64_t ny, int64_t nz,
                           uint64_t seed, const double *scalars, const st_opts *opts);
@@ -157,7 +162,7 @@ int stencil_run(stencil_ctx *h, int64_t T);
 int stencil_sync(stencil_ctx *h);
 
 /*
- * Copy a time level to the host.  level 0 = Omega^t (newest), level 1 = Omega^{t-1} (ST_25PT_WAVE
+ * Copy a time level to the host.  level 0 = Omega^t (newest), level 1 = Omega^{t-1} (wave kinds
  * only; ST_E_INVAL for the Jacobi kinds, whose level 1 is scratch).  out: HOST pointer to a dense
  * padded GLOBAL array of out_elems >= (nz+2R)(ny+2R)(nx+2R) doubles; this rank writes the padded
  * planes it owns ([own_z0, own_z1) of st_info; rank 0 owns the bottom R ghost planes, the last

@@ -9,7 +9,7 @@ There is no CPU fallback: importing works without a GPU (so the host-side plan a
 can be tested), but creating a grid without a CUDA device raises StencilError.
 """
 from ._binding import (  # noqa: F401
-    ST_7PT_CONST, ST_7PT_VAR, ST_25PT_WAVE, ST_25PT_VAR,
+    ST_7PT_CONST, ST_7PT_VAR, ST_25PT_WAVE, ST_25PT_VAR, ST_25PT_WAVE_A, WAVE_KINDS,
     ST_VARIANT_AUTO, ST_VARIANT_NAIVE, ST_VARIANT_STREAM, ST_VARIANT_PIPE,
     ST_OK, ST_E_INVAL, ST_E_NOMEM, ST_E_CUDA, ST_E_NCCL, ST_E_STATE,
     EXPORTED_SYMBOLS, LIB_PATH, StencilError, StOpts, StInfo,

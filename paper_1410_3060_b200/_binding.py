@@ -14,11 +14,13 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libstencil.so")
 
-ST_7PT_CONST, ST_7PT_VAR, ST_25PT_WAVE, ST_25PT_VAR = 1, 2, 3, 4
+ST_7PT_CONST, ST_7PT_VAR, ST_25PT_WAVE, ST_25PT_VAR, ST_25PT_WAVE_A = 1, 2, 3, 4, 5
 ST_VARIANT_AUTO, ST_VARIANT_NAIVE, ST_VARIANT_STREAM, ST_VARIANT_PIPE = 0, 1, 2, 3
 ST_OK, ST_E_INVAL, ST_E_NOMEM, ST_E_CUDA, ST_E_NCCL, ST_E_STATE = 0, -1, -2, -3, -4, -5
-RADIUS = {1: 1, 2: 1, 3: 4, 4: 4}
-N_COEFF = {1: 2, 2: 7, 3: 6, 4: 13}
+RADIUS = {1: 1, 2: 1, 3: 4, 4: 4, 5: 4}
+N_COEFF = {1: 2, 2: 7, 3: 6, 4: 13, 5: 6}
+N_SCALARS = {1: 2, 2: 0, 3: 6, 4: 0, 5: 5}  # leading scalar entries of coeff; the rest are fields
+WAVE_KINDS = (3, 5)
 
 EXPORTED_SYMBOLS = [
     "stencil_opts_default", "stencil_create", "stencil_create_seeded", "stencil_run", "stencil_sync",
@@ -130,15 +132,14 @@ def _f64(a, n=None, name="array"):
 
 
 def stencil_create(kind, nx, ny, nz, coeff, v0, u0=None, opts: StOpts | None = None):
-    """coeff: list of scalars (constant kinds) or padded fields (variable kinds); host numpy arrays."""
+    """coeff: the kind's scalar weights first (N_SCALARS[kind] numbers), then its padded coefficient
+    fields (host numpy arrays), in include/stencil.h's order."""
     R = RADIUS.get(kind, 0)
     n = (nx + 2 * R) * (ny + 2 * R) * (nz + 2 * R)
-    keep = []
-    if kind in (ST_7PT_CONST, ST_25PT_WAVE):
-        arrs = [np.array([float(c)], dtype=np.float64) for c in coeff]
-    else:
-        arrs = [_f64(c, n, "coefficient field") for c in coeff]
-    keep += arrs
+    ns = N_SCALARS.get(kind, 0)
+    coeff = list(coeff)
+    arrs = [np.array([float(c)], dtype=np.float64) for c in coeff[:ns]]
+    arrs += [_f64(c, n, "coefficient field") for c in coeff[ns:]]
     ptrs = (ctypes.c_void_p * max(1, len(arrs)))(*[a.ctypes.data for a in arrs])
     v0 = _f64(v0, n, "v0")
     u0 = None if u0 is None else _f64(u0, n, "u0")

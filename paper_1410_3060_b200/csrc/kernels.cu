@@ -228,6 +228,7 @@ cudaError_t launch_naive(int kind, const KParams& p, cudaStream_t stream, Launch
     case K7C: naive_kernel<K7C><<<grid, block, 0, stream>>>(p); break;
     case K7V: naive_kernel<K7V><<<grid, block, 0, stream>>>(p); break;
     case K25W: naive_kernel<K25W><<<grid, block, 0, stream>>>(p); break;
+    case K25WA: naive_kernel<K25WA><<<grid, block, 0, stream>>>(p); break;
     case K25V: naive_kernel<K25V><<<grid, block, 0, stream>>>(p); break;
     default: return cudaErrorInvalidValue;
   }
@@ -284,6 +285,7 @@ int max_stream_bt(int kind) {
     case K7C: return 6;
     case K7V: return 4;
     case K25W: return 1;
+    case K25WA: return 1;
     case K25V: return 1;
     default: return 0;
   }
@@ -301,6 +303,9 @@ cudaError_t launch_stream(int kind, int b, const KParams& p, int zchunk_req, int
       break;
     case K25W:
       if (b == 1) return run_stream<K25W, 1, 64, 8, 2>(p, zchunk_req, num_sms, stream, info);
+      break;
+    case K25WA:
+      if (b == 1) return run_stream<K25WA, 1, 64, 8, 2>(p, zchunk_req, num_sms, stream, info);
       break;
     case K25V:
       if (b == 1) return run_stream<K25V, 1, 64, 8, 2>(p, zchunk_req, num_sms, stream, info);

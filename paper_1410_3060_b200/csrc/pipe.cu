@@ -158,7 +158,9 @@ struct PipeCfg {
   static constexpr int OX = TX - 2 * R * (BT - 1), OY = TY - 2 * R * (BT - 1);
   static constexpr int OXW = OX & ~3, WOFF = (OX - OXW) / 2;  // written output columns, offset
   static_assert(OXW > 0 && (WOFF + R * (BT - 1)) % 2 == 0, "level-1 extent origin must be even");
-  static constexpr int NCF = WAVE ? 1 : NC;  // fields in the C ring (coefficients, or U for the wave)
+  // fields of the C ring: the wave's Omega^{t-1} (field 0), then the NC coefficient fields
+  static constexpr int FOFF = WAVE ? 1 : 0;
+  static constexpr int NCF = FOFF + NC;
   static constexpr bool HAS_C = NCF > 0;
   // TMA boxes start on an even fp64 column (tiled TMA needs 16-byte aligned x coordinates): the tile
   // origin's raw column is even (decode), so the coefficient box starts exactly at the level-1 extent
@@ -166,7 +168,11 @@ struct PipeCfg {
   // boxes are 2 columns wider than the data.
   static constexpr int FXB = FX + 2, EXB = TX + 2;
   static constexpr int SHV = R & 1, SHC = 0;
-  static constexpr int VELEMS = FXB * FY, CFIELD = EXB * TY, CELEMS = CFIELD * NCF;
+  static constexpr int VELEMS = FXB * FY, CFIELD = EXB * TY;
+  // coefficient field f sits at CF0 + f * CFIELD; the wave's Omega^{t-1} (a separate TMA load) at 0,
+  // padded so the coefficient box that follows it starts on a 128-byte boundary
+  static constexpr int CF0 = FOFF ? (CFIELD + 15) / 16 * 16 : 0;
+  static constexpr int CELEMS = CF0 + CFIELD * NC;
   static constexpr int VSLOT = (VELEMS + 15) / 16 * 16;  // ring slot strides: TMA destinations
   static constexpr int CSLOT = (CELEMS + 15) / 16 * 16;  // must be 128-byte aligned
   static constexpr int PELEMS = TX * TY;                  // one level plane (levels 1..BT-1)
@@ -193,7 +199,7 @@ struct PipeCfg {
 template <int KIND, int BT, int TX, int TY, int CX, int CY, int DV, int DC, int WIN, int MINB>
 __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN, MINB>::THREADS, MINB)
     pipe_kernel(const __grid_constant__ CUtensorMap mapV, const __grid_constant__ CUtensorMap mapC,
-                const KParams p, int ntx, int nty, int items) {
+                const __grid_constant__ CUtensorMap mapA, const KParams p, int ntx, int nty, int items) {
   using C = PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN, MINB>;
   constexpr int R = C::R, NC = C::NC, RL = C::RL, NCONS = C::NCONS, FXB = C::FXB, EXB = C::EXB;
   constexpr int L = C::L;
@@ -238,11 +244,14 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN,
           if constexpr (HAS_C) {
             const uint32_t sc = iv % DC, nc = iv / DC;
             mbar_wait(&emptyC[sc], (nc & 1) ^ 1);
-            mbar_expect_tx(&fullC[sc], C::CELEMS * sizeof(double));
-            if constexpr (WAVE)
+            mbar_expect_tx(&fullC[sc], (C::CFIELD * C::NCF) * sizeof(double));  // bytes the TMA boxes move
+            if constexpr (WAVE) {
               tma_load_3d(sC + (size_t)sc * C::CSLOT, &mapC, &fullC[sc], xc, it.gy0, s - R);
-            else
+              if constexpr (NC > 0)  // the wave's alpha field behind Omega^{t-1} in the same slot
+                tma_load_4d(sC + (size_t)sc * C::CSLOT + C::CF0, &mapA, &fullC[sc], xc, it.gy0, s - R, 0);
+            } else {
               tma_load_4d(sC + (size_t)sc * C::CSLOT, &mapC, &fullC[sc], xc, it.gy0, s - R, 0);
+            }
           }
         }
       }
@@ -363,7 +372,8 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN,
           if constexpr (NC > 0) {
             if (!(WIN && k > BT - WIN)) {
 #pragma unroll
-              for (int f = 0; f < NC; ++f) lds_row<CXN, VEC>(Ck + f * C::CFIELD + ly * EXB + x0, Wrow[f]);
+              for (int f = 0; f < NC; ++f)
+                lds_row<CXN, VEC>(Ck + C::CF0 + f * C::CFIELD + ly * EXB + x0, Wrow[f]);
             }
           }
           double urow[CXN];
@@ -418,7 +428,7 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN,
 #pragma unroll
           for (int f = 0; f < NC; ++f) {
             double w[CXN];
-            lds_row<CXN, VEC>(C1 + f * C::CFIELD + (ly0 + j) * EXB + x0, w);
+            lds_row<CXN, VEC>(C1 + C::CF0 + f * C::CFIELD + (ly0 + j) * EXB + x0, w);
 #pragma unroll
             for (int i = 0; i < CXN; ++i) {
 #pragma unroll
@@ -517,20 +527,23 @@ cudaError_t run_pipe(const KParams& p0, int zchunk_req, int num_sms, cudaStream_
   p.zchunk = zchunk;
   const int nzc = (planes + zchunk - 1) / zchunk;
   const long long items = tiles * nzc;
-  CUtensorMap mapV, mapC;
+  CUtensorMap mapV, mapC, mapA;
   memset(&mapC, 0, sizeof mapC);
+  memset(&mapA, 0, sizeof mapA);
   if (!make_map(&mapV, p.src_raw, 3, p.pitch, p.ny + 2 * C::R, p.zl, 1, p.plane, 0, C::FXB, C::FY, 1))
     return cudaErrorInvalidValue;
   if (C::HAS_C) {
     bool ok = C::WAVE ? make_map(&mapC, p.srcu_raw, 3, p.pitch, p.ny + 2 * C::R, p.zl, 1, p.plane, 0, C::EXB, TY, 1)
                       : make_map(&mapC, p.coef_raw, 4, p.pitch, p.ny + 2 * C::R, p.zl, C::NC, p.plane, p.cstride,
                                  C::EXB, TY, C::NC);
+    if (ok && C::WAVE && C::NC > 0)
+      ok = make_map(&mapA, p.coef_raw, 4, p.pitch, p.ny + 2 * C::R, p.zl, C::NC, p.plane, p.cstride, C::EXB, TY, C::NC);
     if (!ok) return cudaErrorInvalidValue;
   }
   int occ = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, C::THREADS, C::SMEM);
   const int grid = (int)std::min<long long>(items, (long long)std::max(1, occ) * num_sms);
-  kern<<<grid, C::THREADS, C::SMEM, stream>>>(mapV, mapC, p, ntx, nty, (int)items);
+  kern<<<grid, C::THREADS, C::SMEM, stream>>>(mapV, mapC, mapA, p, ntx, nty, (int)items);
   if (info) {
     info->tile_x = C::OXW; info->tile_y = C::OY; info->zchunk = zchunk; info->threads = C::THREADS;
     info->smem = (int)C::SMEM; info->ctas = grid;
@@ -545,6 +558,7 @@ int max_pipe_bt(int kind) {
     case K7C: return 8;
     case K7V: return 3;
     case K25W: return 1;
+    case K25WA: return 1;
     case K25V: return 1;
     default: return 0;
   }
@@ -595,6 +609,12 @@ cudaError_t launch_pipe(int kind, int b, const KParams& p, int zchunk_req, int n
         if (cfg == 2) CFG(K25W, 1, 32, 28, 2, 2, 7, 3, 0, 1);
         if (cfg == 3) CFG(K25W, 1, 64, 16, 1, 4, 7, 3, 0, 1);
         CFG(K25W, 1, 64, 14, 2, 2, 7, 3, 0, 1);
+      }
+      break;
+    case K25WA:
+      if (b == 1) {
+        if (cfg == 1) CFG(K25WA, 1, 64, 16, 1, 4, 7, 3, 0, 1);
+        CFG(K25WA, 1, 64, 14, 2, 2, 7, 3, 0, 1);
       }
       break;
     case K25V:

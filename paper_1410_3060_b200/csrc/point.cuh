@@ -10,13 +10,15 @@
 
 namespace st {
 
-enum Kind { K7C = 1, K7V = 2, K25W = 3, K25V = 4 };
+enum Kind { K7C = 1, K7V = 2, K25W = 3, K25V = 4, K25WA = 5 };
 
 template <int KIND> struct Traits;
 template <> struct Traits<K7C>  { static constexpr int R = 1, NCOEF = 0, NSCAL = 2; static constexpr bool WAVE = false; };
 template <> struct Traits<K7V>  { static constexpr int R = 1, NCOEF = 7, NSCAL = 0; static constexpr bool WAVE = false; };
 template <> struct Traits<K25W> { static constexpr int R = 4, NCOEF = 0, NSCAL = 6; static constexpr bool WAVE = true; };
 template <> struct Traits<K25V> { static constexpr int R = 4, NCOEF = 13, NSCAL = 0; static constexpr bool WAVE = false; };
+// Fig. 1e with the domain-sized alpha_{z,y,x} as printed: one coefficient field.
+template <> struct Traits<K25WA> { static constexpr int R = 4, NCOEF = 1, NSCAL = 5; static constexpr bool WAVE = true; };
 
 // Neighbour access convention for all functions below: m[a][r-1] / p[a][r-1] are the values at
 // distance r in the minus / plus direction of axis a (a = 0 x, 1 y, 2 z); c is the centre.
@@ -60,10 +62,11 @@ __device__ __forceinline__ double point_25v(double c, const double (&m)[3][4], c
   return __dadd_rn(__dadd_rn(acc[0], acc[1]), acc[2]);
 }
 
-// Fig. 1e, scalar alpha: 2*O^t - O^{t-1} + alpha*[w0*O^t + sum_r w_r*(x+y+z pairs_r)].
-// s = {w0, w1, w2, w3, w4, alpha}; u = O^{t-1} at the point.
+// Fig. 1e: 2*O^t - O^{t-1} + alpha*[w0*O^t + sum_r w_r*(x+y+z pairs_r)].
+// s = {w0, w1, w2, w3, w4, *}; alpha = the scalar s[5] (kind 3) or the field value at the point
+// (kind 5); u = O^{t-1} at the point.
 __device__ __forceinline__ double point_25w(double c, double u, const double (&m)[3][4],
-                                            const double (&p)[3][4], const double (&s)[6]) {
+                                            const double (&p)[3][4], const double (&s)[6], double alpha) {
   double L = __dmul_rn(s[0], c);
 #pragma unroll
   for (int r = 0; r < 4; ++r) {
@@ -71,7 +74,7 @@ __device__ __forceinline__ double point_25w(double c, double u, const double (&m
                          __dadd_rn(m[2][r], p[2][r]));
     L = __fma_rn(s[1 + r], S, L);
   }
-  return __fma_rn(s[5], L, __dsub_rn(__dmul_rn(2.0, c), u));
+  return __fma_rn(alpha, L, __dsub_rn(__dmul_rn(2.0, c), u));
 }
 
 // Dispatch on the kind; W = the coefficient values at the point (variable kinds), u = O^{t-1} (wave),
@@ -92,9 +95,12 @@ __device__ __forceinline__ double apply_point(double c, double u, const double (
 #pragma unroll
     for (int i = 0; i < 13; ++i) w[i] = W[i];
     return point_25v(c, m, pl, w);
+  } else if constexpr (KIND == K25WA) {
+    const double s[6] = {ps[0], ps[1], ps[2], ps[3], ps[4], 0.0};
+    return point_25w(c, u, m, pl, s, W[0]);
   } else {
     const double s[6] = {ps[0], ps[1], ps[2], ps[3], ps[4], ps[5]};
-    return point_25w(c, u, m, pl, s);
+    return point_25w(c, u, m, pl, s, s[5]);
   }
 }
 

@@ -42,9 +42,10 @@ void set_err(const char* fmt, ...) {
   g_err = buf;
 }
 
-int radius_of(int kind) { return (kind == 1 || kind == 2) ? 1 : (kind == 3 || kind == 4) ? 4 : -1; }
-int ncoef_of(int kind) { return kind == 2 ? 7 : kind == 4 ? 13 : 0; }
-int nscal_of(int kind) { return kind == 1 ? 2 : kind == 3 ? 6 : 0; }
+int radius_of(int kind) { return (kind == 1 || kind == 2) ? 1 : (kind >= 3 && kind <= 5) ? 4 : -1; }
+int ncoef_of(int kind) { return kind == 2 ? 7 : kind == 4 ? 13 : kind == 5 ? 1 : 0; }  // domain-sized fields
+int nscal_of(int kind) { return kind == 1 ? 2 : kind == 3 ? 6 : kind == 5 ? 5 : 0; }    // scalar weights
+bool is_wave(int kind) { return kind == ST_25PT_WAVE || kind == ST_25PT_WAVE_A; }
 
 // ---------------------------------------------------------------- NCCL, loaded at run time
 // The Python binding imports torch first, so libnccl.so.2 (torch's) is normally already loaded;
@@ -307,7 +308,7 @@ int create_common(stencil_ctx** out, int kind, int64_t nx, int64_t ny, int64_t n
   h->xoff = 16 - R;
   h->pitch = ((h->xoff + h->X) + 15) / 16 * 16;
   h->plane = h->pitch * h->Y;
-  h->nbuf = (kind == ST_25PT_WAVE && h->bt >= 2) ? 4 : 2;
+  h->nbuf = (is_wave(kind) && h->bt >= 2) ? 4 : 2;
   for (auto& s : h->slabs) {
     const size_t bytes = (size_t)h->plane * (size_t)s.zl * sizeof(double);
     for (int b = 0; b < h->nbuf; ++b) {
@@ -488,7 +489,7 @@ int launch_range(stencil_ctx* h, Slab& s, int b, int d0, int d1, int64_t z0, int
 // neither the planes being sent nor the halo planes being received.  The next block waits for the
 // exchange (ev_halo).
 int run_block(stencil_ctx* h, int b) {
-  const bool wave = h->kind == ST_25PT_WAVE;
+  const bool wave = is_wave(h->kind);
   int new0, new1, d0, d1 = -1;
   if (!wave) {
     d0 = h->lv1;
@@ -597,13 +598,13 @@ int stencil_create(stencil_ctx** out, int kind, int64_t nx, int64_t ny, int64_t 
                    const st_opts* opts) {
   const int R = radius_of(kind);
   if (R < 0) { set_err("bad kind %d", kind); return ST_E_INVAL; }
-  const int want = kind == 1 ? 2 : kind == 2 ? 7 : kind == 3 ? 6 : 13;
+  const int want = kind == 1 ? 2 : kind == 2 ? 7 : kind == 3 ? 6 : kind == 4 ? 13 : 6;
   if (n_coeff != want) { set_err("kind %d needs n_coeff=%d (got %d)", kind, want, n_coeff); return ST_E_INVAL; }
   if (!coeff || !v0) { set_err("NULL coeff or v0"); return ST_E_INVAL; }
   for (int i = 0; i < n_coeff; ++i)
     if (!coeff[i]) { set_err("coeff[%d] is NULL", i); return ST_E_INVAL; }
-  if (kind == ST_25PT_WAVE && !u0) { set_err("ST_25PT_WAVE needs u0"); return ST_E_INVAL; }
-  if (kind != ST_25PT_WAVE && u0) { set_err("u0 must be NULL for kind %d", kind); return ST_E_INVAL; }
+  if (is_wave(kind) && !u0) { set_err("wave kinds need u0"); return ST_E_INVAL; }
+  if (!is_wave(kind) && u0) { set_err("u0 must be NULL for kind %d", kind); return ST_E_INVAL; }
   stencil_ctx* h = nullptr;
   int rc = create_common(out, kind, nx, ny, nz, opts, &h);
   if (rc) { fail_create(h); return rc; }
@@ -611,7 +612,7 @@ int stencil_create(stencil_ctx** out, int kind, int64_t nx, int64_t ny, int64_t 
   cudaError_t e = cudaSuccess;
   for (auto& s : h->slabs) {
     for (int b = 0; b < h->nbuf && e == cudaSuccess; ++b) e = upload_planes(h, s, s.buf[b], v0);
-    if (e == cudaSuccess && kind == ST_25PT_WAVE) {
+    if (e == cudaSuccess && is_wave(kind)) {
       // level 1 = Omega^{-1}: interior from u0, ghosts from v0 (reading Q9).  Upload u0's
       // planes, then restore ghosts from v0: ghost planes wholesale, ghost rows/columns by 2-D copies.
       double* d = s.buf[h->lv1] + h->xoff;
@@ -636,11 +637,12 @@ int stencil_create(stencil_ctx** out, int kind, int64_t nx, int64_t ny, int64_t 
         }
       }
     }
+    // coefficient fields follow the scalars in coeff[] (kind 5: w0..w4, then the alpha field)
     for (int i = 0; i < h->ncoef && e == cudaSuccess; ++i)
-      e = upload_planes(h, s, s.coef + (size_t)i * h->plane * s.zl, coeff[i]);
+      e = upload_planes(h, s, s.coef + (size_t)i * h->plane * s.zl, coeff[h->nscal + i]);
   }
   if (e != cudaSuccess) rc = cuda_fail(h, e, "upload");
-  if (rc == ST_OK && !h->ncoef)
+  if (rc == ST_OK)
     for (int i = 0; i < h->nscal; ++i) h->scal[i] = *coeff[i];
   if (rc == ST_OK) {
     e = cudaStreamSynchronize(h->stream);  // host arrays may be freed by the caller after return
@@ -663,12 +665,14 @@ int stencil_create_seeded(stencil_ctx** out, int kind, int64_t nx, int64_t ny, i
   const double d25w[6] = {3.0 * (-205.0 / 72.0), 8.0 / 5.0, -1.0 / 5.0, 8.0 / 315.0, -1.0 / 560.0, 0.1};
   if (kind == ST_7PT_CONST) for (int i = 0; i < 2; ++i) h->scal[i] = scalars ? scalars[i] : d7c[i];
   if (kind == ST_25PT_WAVE) for (int i = 0; i < 6; ++i) h->scal[i] = scalars ? scalars[i] : d25w[i];
+  if (kind == ST_25PT_WAVE_A) for (int i = 0; i < 5; ++i) h->scal[i] = scalars ? scalars[i] : d25w[i];
   const long long GZ = nz + 2 * R;
-  const double c = kind == ST_7PT_VAR ? 1.0 / 7.0 : 1.0 / 25.0;
+  // U[0, c): 1/7 (7v), 1/25 (25v), 0.2 for the wave's alpha field (stable below 0.205, synth/__init__.py)
+  const double c = kind == ST_7PT_VAR ? 1.0 / 7.0 : kind == ST_25PT_VAR ? 1.0 / 25.0 : 0.2;
   cudaError_t e = cudaSuccess;
   for (auto& s : h->slabs) {
     for (int b = 0; b < h->nbuf && e == cudaSuccess; ++b) {
-      const int mode = (kind == ST_25PT_WAVE && b == h->lv1) ? 1 : 0;
+      const int mode = (is_wave(kind) && b == h->lv1) ? 1 : 0;
       e = st::launch_fill(s.buf[b] + h->xoff, h->pitch, h->plane, (int)s.zl, s.store_z0, h->X, h->Y, GZ, R,
                           seed, 0, mode, 0.0, h->stream);
     }
@@ -720,7 +724,7 @@ int stencil_sync(stencil_ctx* h) {
 int stencil_read_planes(stencil_ctx* h, int level, int64_t z0, int64_t z1, double* out, int64_t out_elems) {
   int rc = check_handle(h);
   if (rc) return rc;
-  if (level < 0 || level > 1 || (level == 1 && h->kind != ST_25PT_WAVE)) {
+  if (level < 0 || level > 1 || (level == 1 && !is_wave(h->kind))) {
     set_err("level %d not readable for kind %d", level, h->kind);
     return ST_E_INVAL;
   }
@@ -763,7 +767,7 @@ int stencil_read(stencil_ctx* h, int level, double* out, int64_t out_elems) {
 int stencil_write(stencil_ctx* h, int level, const double* in, int64_t in_elems) {
   int rc = check_handle(h);
   if (rc) return rc;
-  if (level < 0 || level > 1 || (level == 1 && h->kind != ST_25PT_WAVE)) {
+  if (level < 0 || level > 1 || (level == 1 && !is_wave(h->kind))) {
     set_err("level %d not writable for kind %d", level, h->kind);
     return ST_E_INVAL;
   }
@@ -774,9 +778,9 @@ int stencil_write(stencil_ctx* h, int level, const double* in, int64_t in_elems)
   cudaError_t e = cudaSuccess;
   for (auto& s : h->slabs) {
     if (e == cudaSuccess) e = upload_planes(h, s, s.buf[level == 0 ? h->lv0 : h->lv1], in);
-    if (e == cudaSuccess && level == 0 && h->kind != ST_25PT_WAVE)
+    if (e == cudaSuccess && level == 0 && !is_wave(h->kind))
       e = upload_planes(h, s, s.buf[h->lv1], in);  // keep level 1's ghosts equal to the new ghosts
-    if (e == cudaSuccess && h->kind == ST_25PT_WAVE && h->nbuf == 4 && level == 0)
+    if (e == cudaSuccess && is_wave(h->kind) && h->nbuf == 4 && level == 0)
       for (int b = 0; b < 4 && e == cudaSuccess; ++b)
         if (b != h->lv0 && b != h->lv1) e = upload_planes(h, s, s.buf[b], in);  // spare buffers' ghosts
   }

@@ -4,7 +4,7 @@ Configuration data only (kind, extents, T); the values are drawn by synth.make_i
 """
 from dataclasses import dataclass
 
-from . import K7C, K7V, K25W, K25V
+from . import K7C, K7V, K25W, K25V, K25WA
 
 
 @dataclass(frozen=True)
@@ -29,7 +29,10 @@ C4 = Workload("C4-25pt-var-512", K25V, 512, 512, 512, 100)
 C5 = Workload("C5-25pt-var-1024", K25V, 1024, 1024, 1024, 200)
 
 CONFIGS = [C1, C2, C3, C4, C5]
-BY_NAME = {w.name: w for w in CONFIGS}
+# SURVEY.md NEXT-1 (not a BASELINE.json config): C3's wave with the domain-sized alpha field of Fig. 1e.
+C3A = Workload("C3A-25pt-wave-alpha-512", K25WA, 512, 512, 512, 100)
+EXTRA = [C3A]
+BY_NAME = {w.name: w for w in CONFIGS + EXTRA}
 
 
 def weak_c5(n_gpus: int) -> Workload:

@@ -6,6 +6,7 @@ import paper_1410_3060_b200 as st
 import synth
 
 WAVE = synth.K25W
+WAVES = synth.WAVE_KINDS
 
 
 def interior(R):
@@ -19,15 +20,15 @@ def gpu_run(kind, nx, ny, nz, T, seed=synth.DEFAULT_SEED, variant=0, bt=0, zchun
         g = st.Grid(kind, nx, ny, nz, seed=seed, scalars=scalars, variant=variant, bt=bt, zchunk=zchunk,
                     tile_cfg=tile_cfg)
     else:
-        coeff = inputs.coef if inputs.coef else list(inputs.scalars)
-        u0 = inputs.U if kind == WAVE else None
+        coeff = list(inputs.scalars) + list(inputs.coef)
+        u0 = inputs.U if kind in WAVES else None
         g = st.Grid(kind, nx, ny, nz, v0=inputs.V, u0=u0, coeff=coeff, variant=variant, bt=bt,
                     zchunk=zchunk, tile_cfg=tile_cfg)
     with g:
         if T > 0:
             g.run(T)
         new = g.read(0)
-        old = g.read(1) if kind == WAVE else None
+        old = g.read(1) if kind in WAVES else None
         info = g.info()
     return new, old, info
 
@@ -41,12 +42,12 @@ def rel_err(g, o, R):
 def assert_parity(kind, g_new, g_old, o_new, o_old, R, tol, inputs=None):
     e = rel_err(g_new, o_new, R)
     assert e <= tol, f"normwise relative error {e:.3e} > {tol:.1e}"
-    if kind == WAVE:
+    if kind in WAVES:
         e1 = rel_err(g_old, o_old, R)
         assert e1 <= tol, f"level-1 normwise relative error {e1:.3e} > {tol:.1e}"
     if inputs is not None:  # G5: ghosts bitwise untouched
         m = np.ones(g_new.shape, bool)
         m[interior(R)] = False
         assert np.array_equal(g_new[m], inputs.V[m])
-        if kind == WAVE:
+        if kind in WAVES:
             assert np.array_equal(g_old[m], inputs.V[m])

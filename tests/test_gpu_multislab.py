@@ -7,7 +7,7 @@ import pytest
 import oracle
 import paper_1410_3060_b200 as st
 import synth
-from gpu_common import WAVE, assert_parity
+from gpu_common import WAVES, assert_parity
 
 pytestmark = pytest.mark.gpu
 
@@ -16,7 +16,7 @@ def run(kind, n, T, **kw):
     with st.Grid(kind, *n, seed=31, **kw) as g:
         g.run(T)
         new = g.read(0)
-        old = g.read(1) if kind == WAVE else None
+        old = g.read(1) if kind in WAVES else None
         info = g.info()
     return new, old, info
 
@@ -26,6 +26,7 @@ CASES = [
     (synth.K7V, (40, 33, 37), 9),
     (synth.K25W, (70, 20, 41), 6),
     (synth.K25V, (70, 20, 41), 6),
+    (synth.K25WA, (70, 20, 41), 6),
 ]
 
 
@@ -38,7 +39,7 @@ def test_loopback_slabs_bitwise_equal_single(kind, n, T, P):
         got = run(kind, n, T, nranks=P, local_slabs=P, variant=variant, bt=bt)
         assert got[2]["nranks"] == P and got[2]["local_slabs"] == P
         assert np.array_equal(got[0], ref[0]), (variant, bt)
-        if kind == WAVE:
+        if kind in WAVES:
             assert np.array_equal(got[1], ref[1]), (variant, bt)
 
 

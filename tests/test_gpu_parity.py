@@ -7,24 +7,24 @@ import pytest
 import oracle
 import paper_1410_3060_b200 as st
 import synth
-from gpu_common import WAVE, assert_parity, gpu_run, interior, rel_err
+from gpu_common import WAVES, assert_parity, gpu_run, interior, rel_err
 
 pytestmark = pytest.mark.gpu
 
-KINDS = [synth.K7C, synth.K7V, synth.K25W, synth.K25V]
+KINDS = [synth.K7C, synth.K7V, synth.K25W, synth.K25V, synth.K25WA]
 # several tiles in x and y with ragged tails, several z-chunks (7-point output tiles 32x32 .. 16x16,
 # 25-point output tiles 64 x 8 / 32 x 16 / 64 x 16; streaming variant 30 x 30 .. 22 x 22, 56 x 8)
 SHAPES = {synth.K7C: (61, 70, 45), synth.K7V: (61, 70, 45), synth.K25W: (130, 37, 41),
-          synth.K25V: (130, 37, 41)}
+          synth.K25V: (130, 37, 41), synth.K25WA: (130, 37, 41)}
 
 
 def max_bt(kind, variant=st.ST_VARIANT_PIPE):
     if variant == st.ST_VARIANT_STREAM:
-        return {synth.K7C: 6, synth.K7V: 4, synth.K25W: 1, synth.K25V: 1}[kind]
-    return {synth.K7C: 8, synth.K7V: 3, synth.K25W: 1, synth.K25V: 1}[kind]
+        return {synth.K7C: 6, synth.K7V: 4, synth.K25W: 1, synth.K25V: 1, synth.K25WA: 1}[kind]
+    return {synth.K7C: 8, synth.K7V: 3, synth.K25W: 1, synth.K25V: 1, synth.K25WA: 1}[kind]
 
 
-N_CFG = {synth.K7C: 1, synth.K7V: 3, synth.K25W: 4, synth.K25V: 3}  # pipe tile configurations
+N_CFG = {synth.K7C: 1, synth.K7V: 3, synth.K25W: 4, synth.K25V: 3, synth.K25WA: 2}  # pipe tile configurations
 
 
 @pytest.mark.parametrize("kind", KINDS)
@@ -33,7 +33,7 @@ def test_seeded_fill_matches_host_generator(kind):
     new, old, _ = gpu_run(kind, nx, ny, nz, 0, seed=77)
     inp = synth.make_inputs(kind, nx, ny, nz, seed=77)
     assert np.array_equal(new, inp.V)
-    if kind == WAVE:
+    if kind in WAVES:
         assert np.array_equal(old, inp.U)
 
 
@@ -44,7 +44,7 @@ def test_create_from_host_equals_seeded(kind):
     a = gpu_run(kind, nx, ny, nz, 7, seed=5)
     b = gpu_run(kind, nx, ny, nz, 7, inputs=inp)
     assert np.array_equal(a[0], b[0])
-    if kind == WAVE:
+    if kind in WAVES:
         assert np.array_equal(a[1], b[1])
 
 
@@ -78,7 +78,7 @@ def test_parity_T20_default_plan(kind):
 
 
 @pytest.mark.parametrize("kind", [synth.K7C, synth.K7V, synth.K25V])
-def test_shadow_scaled_per_cell(kind):
+def test_shadow_scaled_per_cell(kind):  # needs non-negative weights: not the waves
     """G2: |g - o| <= 1e-11 * S(p), S = oracle on |inputs| (non-negative coefficients), T = 60."""
     n = (70, 66, 64) if synth.RADIUS[kind] == 1 else (72, 40, 48)
     inp = synth.make_inputs(kind, *n, seed=2)
@@ -105,7 +105,7 @@ def test_variants_bitwise_identical(kind):
         got = gpu_run(kind, nx, ny, nz, T, seed=9, variant=variant, bt=bt, zchunk=zchunk, tile_cfg=cfg)
         assert got[2]["bt"] == bt
         assert np.array_equal(got[0], ref[0]), (variant, bt, zchunk, cfg)
-        if kind == WAVE:
+        if kind in WAVES:
             assert np.array_equal(got[1], ref[1]), (variant, bt, zchunk, cfg)
 
 
@@ -144,11 +144,11 @@ def test_checkpoint_resume_bitwise():
         inp = synth.make_inputs(kind, nx, ny, nz, seed=6)
         full = gpu_run(kind, nx, ny, nz, 9, seed=6)
         a_new, a_old, _ = gpu_run(kind, nx, ny, nz, 4, seed=6)
-        res = synth.Inputs(kind, nx, ny, nz, a_new, a_old if kind == WAVE else a_new.copy(), inp.coef,
+        res = synth.Inputs(kind, nx, ny, nz, a_new, a_old if kind in WAVES else a_new.copy(), inp.coef,
                            inp.scalars)
         b = gpu_run(kind, nx, ny, nz, 5, inputs=res)
         assert np.array_equal(b[0], full[0])
-        if kind == WAVE:
+        if kind in WAVES:
             assert np.array_equal(b[1], full[1])
 
 

@@ -22,7 +22,7 @@ ap.add_argument("--variant", type=int, default=0)
 ap.add_argument("--zchunk", type=int, default=0)
 a = ap.parse_args()
 torch.cuda.set_device(0)
-w = {x.name.split("-")[0]: x for x in workloads.CONFIGS}[a.workload]
+w = {x.name.split("-")[0]: x for x in workloads.CONFIGS + workloads.EXTRA}[a.workload]
 g = st.Grid(w.kind, w.nx, w.ny, w.nz, seed=synth.DEFAULT_SEED, variant=a.variant, bt=a.bt, zchunk=a.zchunk)
 bt = g.info()["bt"]
 g.run(a.T or 2 * bt)

@@ -31,7 +31,7 @@ def main():
     torch.cuda.set_device(0)
     s = torch.cuda.current_stream()
     for name in a.workloads.split(","):
-        w = {x.name.split("-")[0]: x for x in workloads.CONFIGS}[name]
+        w = {x.name.split("-")[0]: x for x in workloads.CONFIGS + workloads.EXTRA}[name]
         T = a.T or w.T
         for variant in [int(v) for v in a.variants.split(",")]:
             for bt, zc, cfg in [(int(b), int(z), int(c)) for b in a.bts.split(",")
