@@ -12,7 +12,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libstencil.so")
+# STENCIL_LIB overrides the library path (A/B comparisons of two builds in one process tree)
+LIB_PATH = os.environ.get("STENCIL_LIB") or os.path.join(_HERE, "libstencil.so")
 
 ST_7PT_CONST, ST_7PT_VAR, ST_25PT_WAVE, ST_25PT_VAR, ST_25PT_WAVE_A = 1, 2, 3, 4, 5
 ST_VARIANT_AUTO, ST_VARIANT_NAIVE, ST_VARIANT_STREAM, ST_VARIANT_PIPE = 0, 1, 2, 3
