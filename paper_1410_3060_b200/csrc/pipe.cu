@@ -163,11 +163,12 @@ struct PipeCfg {
   static constexpr int NCF = FOFF + NC;
   static constexpr bool HAS_C = NCF > 0;
   // TMA boxes start on an even fp64 column (tiled TMA needs 16-byte aligned x coordinates): the tile
-  // origin's raw column is even (decode), so the coefficient box starts exactly at the level-1 extent
-  // (shift SHC = 0) and the footprint box one column early when R is odd (shift SHV = R & 1); both
-  // boxes are 2 columns wider than the data.
-  static constexpr int FXB = FX + 2, EXB = TX + 2;
+  // origin's raw column is even (decode), so the coefficient box is exactly the level-1 extent
+  // (shift SHC = 0) and the footprint box starts one column early when R is odd (shift SHV = R & 1).
   static constexpr int SHV = R & 1, SHC = 0;
+  // box widths (even: 16-byte rows).  The coefficient box keeps 2 spare columns for R = 1 (measured:
+  // a 32-double row stride loses 5 % on the 7-point kernels, profiles/r01_summary.md).
+  static constexpr int FXB = (FX + SHV + 1) / 2 * 2, EXB = TX + (R == 1 ? 2 : 0);
   static constexpr int VELEMS = FXB * FY, CFIELD = EXB * TY;
   // coefficient field f sits at CF0 + f * CFIELD; the wave's Omega^{t-1} (a separate TMA load) at 0,
   // padded so the coefficient box that follows it starts on a 128-byte boundary
