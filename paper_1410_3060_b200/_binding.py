@@ -220,6 +220,16 @@ def stencil_plan_slab(nz, R, nranks, rank, bt):
             "bt": e.value}
 
 
+def tuned_plan(kind, nx, ny, nz):
+    """(bt, tile_cfg, zchunk) that tools/tune.py measured fastest for this kind and shape, or None."""
+    import json
+    path = os.path.join(_HERE, "tuned.json")
+    try:
+        return json.load(open(path)).get(f"{kind}:{nx}x{ny}x{nz}")
+    except (OSError, ValueError):
+        return None
+
+
 # ------------------------------------------------------------------ torch-backed device memory
 _torch_alloc_cb = None
 _torch_free_cb = None
@@ -258,8 +268,12 @@ class Grid:
     def __init__(self, kind, nx, ny, nz, *, seed=None, scalars=None, v0=None, u0=None, coeff=None,
                  variant=ST_VARIANT_AUTO, bt=0, zchunk=0, tile_cfg=0, rank=0, nranks=1, nccl_id=None,
                  local_slabs=1,
-                 device=None, stream=None, torch_memory=True):
+                 device=None, stream=None, torch_memory=True, tuned=False):
         import torch
+        if tuned and bt == 0:  # plan measured by tools/tune.py for this kind and shape, if any
+            plan = tuned_plan(kind, nx, ny, nz)
+            if plan:
+                bt, tile_cfg, zchunk = plan["bt"], plan["tile_cfg"], plan["zchunk"]
         self.kind, self.nx, self.ny, self.nz = kind, nx, ny, nz
         self.R = RADIUS[kind]
         o = stencil_opts_default()

@@ -1,0 +1,79 @@
+"""Auto-tuner for the pipe kernel's plan (the paper's D_w / N_F search, P:808-822,
+brute force after model pruning): for a workload, enumerate (bt, tile_cfg, zchunk) candidates that the
+shared-memory/register footprint admits (the library rejects the rest), time short runs, and write the
+best plan per workload to paper_1410_3060_b200/tuned.json, which `Grid(..., tuned=True)` applies.
+
+python tools/tune.py --workloads C2,C3,C4 [--T 20]
+"""
+import argparse
+import json
+import os
+import statistics
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import paper_1410_3060_b200 as st  # noqa: E402
+import synth  # noqa: E402
+from synth import workloads  # noqa: E402
+
+TUNED = os.path.join(ROOT, "paper_1410_3060_b200", "tuned.json")
+MAX_BT = {1: 8, 2: 3, 3: 1, 4: 1, 5: 1}
+N_CFG = {1: 1, 2: 3, 3: 4, 4: 3, 5: 2}
+
+
+def time_plan(w, T, bt, cfg, zchunk, reps=3):
+    s = torch.cuda.current_stream()
+    g = st.Grid(w.kind, w.nx, w.ny, w.nz, seed=synth.DEFAULT_SEED, bt=bt, tile_cfg=cfg, zchunk=zchunk)
+    try:
+        g.run(T)
+        g.sync()
+        ts = []
+        for _ in range(reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            g.run(T)
+            e1.record(s)
+            e1.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        return w.nx * w.ny * w.nz * T / statistics.median(ts) / 1e6
+    finally:
+        g.close()
+        torch.cuda.empty_cache()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--workloads", default="C1,C2,C3,C4")
+    ap.add_argument("--T", type=int, default=0, help="steps per timed run (0: min(workload T, 24))")
+    a = ap.parse_args()
+    torch.cuda.set_device(0)
+    table = json.load(open(TUNED)) if os.path.exists(TUNED) else {}
+    names = {x.name.split("-")[0]: x for x in workloads.CONFIGS + workloads.EXTRA}
+    for name in a.workloads.split(","):
+        w = names[name]
+        T = a.T or min(w.T, 24)
+        best = None
+        for bt in range(1, MAX_BT[w.kind] + 1):
+            for cfg in range(N_CFG[w.kind]):
+                for zc in (0, 64, 256):
+                    try:
+                        g = time_plan(w, T, bt, cfg, zc)
+                    except st.StencilError as e:
+                        print(json.dumps({"workload": name, "bt": bt, "cfg": cfg, "error": str(e)[:80]}))
+                        continue
+                    print(json.dumps({"workload": name, "bt": bt, "cfg": cfg, "zchunk": zc, "glups": round(g, 2)}),
+                          flush=True)
+                    if best is None or g > best["glups"]:
+                        best = {"bt": bt, "tile_cfg": cfg, "zchunk": zc, "glups": round(g, 2), "T": T}
+        best["workload"] = w.name
+        table[f"{w.kind}:{w.nx}x{w.ny}x{w.nz}"] = best
+        print(json.dumps({"workload": name, "best": best}), flush=True)
+    json.dump(table, open(TUNED, "w"), indent=1)
+
+
+if __name__ == "__main__":
+    main()
