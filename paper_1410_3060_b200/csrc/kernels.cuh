@@ -31,6 +31,7 @@ struct KParams {
   int dbg;     // experiment knob (STENCIL_DBG): bit 0 = skip all compute in the pipe kernel, bit 1 =
                // skip level barriers; fault injection for the mutation tests (STENCIL_FAULT):
                // bit 2 = never write the last plane of a z-chunk, bit 3 = skip work item 0
+  unsigned int* sched;  // pipe kernel: 2 zeroed device counters (next work item, CTAs done)
   int walign;  // pipe kernel: tiles write sector-aligned output segments (STENCIL_WALIGN=1; default 0:
                // measured slower under the power cap for OX % 4 != 0, profiles/r01_summary.md)
 };

@@ -180,7 +180,7 @@ struct PipeCfg {
   static constexpr int NPL = BT - 1;                      // shared level planes (double-buffered)
   static constexpr size_t SMEM = sizeof(double) * ((size_t)DV * VSLOT + (HAS_C ? (size_t)DC * CSLOT : 0) +
                                                    (size_t)NPL * 2 * PELEMS) +
-                                 sizeof(uint64_t) * 2 * (DV + DC) + 128;
+                                 sizeof(uint64_t) * (2 * (DV + DC) + 8) + 4 * sizeof(int) + 128;
   static_assert(TY % CY == 0 && TX % CX == 0 && (CX == 1 || CX % 2 == 0), "cell blocks");
   static_assert(OX > 0 && OY > 0, "tile too small for BT");
   static_assert(NCONS % 32 == 0, "whole consumer warps");
@@ -217,11 +217,17 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN,
   uint64_t* emptyV = bars + DV;
   uint64_t* fullC = bars + 2 * DV;
   uint64_t* emptyC = bars + 2 * DV + DC;
+  // dynamic work distribution: the producer takes item ids from a global counter (p.sched[0]) and
+  // hands them to the consumers through a 4-entry queue; id -1 ends the CTA
+  uint64_t* itemFull = bars + 2 * (DV + DC);
+  uint64_t* itemEmpty = itemFull + 4;
+  volatile int* itemq = reinterpret_cast<volatile int*>(itemEmpty + 4);
 
   const int tid = threadIdx.x;
   if (tid == 0) {
     for (int i = 0; i < DV; ++i) { mbar_init(&fullV[i], 1); mbar_init(&emptyV[i], NCONS / 32); }
     for (int i = 0; i < DC; ++i) { mbar_init(&fullC[i], 1); mbar_init(&emptyC[i], NCONS / 32); }
+    for (int i = 0; i < 4; ++i) { mbar_init(&itemFull[i], 1); mbar_init(&itemEmpty[i], NCONS / 32); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -232,7 +238,14 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN,
       asm volatile("prefetch.tensormap [%0];" ::"l"(&mapV) : "memory");
       if (HAS_C) asm volatile("prefetch.tensormap [%0];" ::"l"(&mapC) : "memory");
       uint32_t iv = 0;
-      for (int item = blockIdx.x; item < items; item += gridDim.x) {
+      for (uint32_t n = 0;; ++n) {
+        const uint32_t qs = n & 3;
+        mbar_wait(&itemEmpty[qs], ((n >> 2) & 1) ^ 1);
+        int item = (int)atomicAdd(p.sched, 1u);
+        if (item >= items) item = -1;
+        itemq[qs] = item;
+        mbar_arrive(&itemFull[qs]);  // release: the id is visible to the consumers' acquire
+        if (item < 0) break;
         if ((p.dbg & 8) && item == 0) continue;
         const Item it = decode<R, BT - 1, OX, OY>(item, ntx, nty, p);
         const int xv = (it.gx0 - R + p.xoff) & ~1;  // footprint box
@@ -256,6 +269,13 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN,
           }
         }
       }
+      // every CTA has drawn its terminating id before the last one gets here: reset for the next launch
+      __threadfence();
+      if (atomicAdd(p.sched + 1, 1u) == gridDim.x - 1) {
+        p.sched[0] = 0;
+        p.sched[1] = 0;
+        __threadfence();
+      }
     }
     return;
   }
@@ -269,7 +289,13 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN,
   const int lane = tid & 31;
   uint32_t iv = 0;
 
-  for (int item = blockIdx.x; item < items; item += gridDim.x) {
+  for (uint32_t n = 0;; ++n) {
+    const uint32_t qs = n & 3;
+    mbar_wait(&itemFull[qs], (n >> 2) & 1);
+    const int item = itemq[qs];
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&itemEmpty[qs]);
+    if (item < 0) break;
     if ((p.dbg & 8) && item == 0) continue;
     const Item it = decode<R, BT - 1, OX, OY>(item, ntx, nty, p);
     bool outc[CY][CXN];

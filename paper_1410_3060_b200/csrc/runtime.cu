@@ -111,6 +111,7 @@ struct stencil_ctx {
   int nbuf = 2;
   int lv0 = 0, lv1 = 1;  // buffer index of Omega^t and Omega^{t-1} (same in every slab)
   double scal[6] = {0, 0, 0, 0, 0, 0};
+  unsigned int* sched = nullptr;  // pipe kernel work counters (zero between launches)
 
   std::vector<std::pair<void*, size_t>> allocs;
   int64_t steps = 0;
@@ -331,6 +332,9 @@ int create_common(stencil_ctx** out, int kind, int64_t nx, int64_t ny, int64_t n
   }
   h->lv0 = 0;
   h->lv1 = 1;
+  h->sched = (unsigned int*)dev_alloc(h, 256);
+  if (!h->sched) { set_err("device allocation of 256 bytes failed"); return ST_E_NOMEM; }
+  CK(cudaMemsetAsync(h->sched, 0, 256, h->stream), "zero work counters");
 
   if (o.nranks > 1) {
     CK(cudaStreamCreateWithFlags(&h->comm_stream, cudaStreamNonBlocking), "comm stream");
@@ -383,6 +387,7 @@ st::KParams base_params(stencil_ctx* h, const Slab& s) {
   p.zo1 = (int)(s.hi - s.store_z0);
   for (int i = 0; i < 6; ++i) p.s[i] = h->scal[i];
   p.coef_raw = s.coef;
+  p.sched = h->sched;
   p.xoff = (int)h->xoff;
   p.dbg = env_int("STENCIL_DBG") | (env_int("STENCIL_FAULT") & 12);
   static const int walign = getenv("STENCIL_WALIGN") ? atoi(getenv("STENCIL_WALIGN")) : 0;
