@@ -136,6 +136,27 @@ __device__ __forceinline__ void sts_row(double* p, const double* in) {
   }
 }
 
+// Streaming (evict-first) global stores of the cells i < N with m[i] set; 128-bit stores for pairs when
+// VEC (p is 16-byte aligned: the cell block's first column has an even raw index, see decode()).
+template <int N, bool VEC>
+__device__ __forceinline__ void stg_row(double* p, const double* v, const bool* m) {
+  if constexpr (VEC && N % 2 == 0) {
+#pragma unroll
+    for (int i = 0; i < N; i += 2) {
+      if (m[i] && m[i + 1]) {
+        __stcs(reinterpret_cast<double2*>(p + i), make_double2(v[i], v[i + 1]));
+      } else {
+        if (m[i]) __stcs(p + i, v[i]);
+        if (m[i + 1]) __stcs(p + i + 1, v[i + 1]);
+      }
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+      if (m[i]) __stcs(p + i, v[i]);
+  }
+}
+
 }  // namespace
 
 // Consumer threads cover the level-1 extent E1 = TX x TY of a tile: each thread owns a block of CX
@@ -143,7 +164,7 @@ __device__ __forceinline__ void sts_row(double* p, const double* in) {
 // cell is computed at level 1, and the level-BT output tile is
 // OX x OY = (TX - 2R(BT-1)) x (TY - 2R(BT-1)).  The Omega^t box (footprint) is E1 grown by R on each
 // side; the coefficient (or wave U) box is E1 itself.  DV / DC = ring depths (planes).
-template <int KIND, int BT, int TX, int TY, int CX, int CY, int DV, int DC, int WIN, int MINB>
+template <int KIND, int BT, int TX, int TY, int CX, int CY, int DV, int DC, int WIN, int MINB, bool UNR>
 struct PipeCfg {
   using TR = Traits<KIND>;
   static constexpr int R = TR::R, NC = TR::NCOEF, RL = 2 * R + 1;
@@ -197,11 +218,11 @@ struct PipeCfg {
   static_assert(FXB <= 256 && FY <= 256 && EXB <= 256, "TMA box dimension limit");
 };
 
-template <int KIND, int BT, int TX, int TY, int CX, int CY, int DV, int DC, int WIN, int MINB>
-__global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN, MINB>::THREADS, MINB)
+template <int KIND, int BT, int TX, int TY, int CX, int CY, int DV, int DC, int WIN, int MINB, bool UNR>
+__global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN, MINB, UNR>::THREADS, MINB)
     pipe_kernel(const __grid_constant__ CUtensorMap mapV, const __grid_constant__ CUtensorMap mapC,
                 const __grid_constant__ CUtensorMap mapA, const KParams p, int ntx, int nty, int items) {
-  using C = PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN, MINB>;
+  using C = PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN, MINB, UNR>;
   constexpr int R = C::R, NC = C::NC, RL = C::RL, NCONS = C::NCONS, FXB = C::FXB, EXB = C::EXB;
   constexpr int L = C::L;
   constexpr bool WAVE = C::WAVE, HAS_C = C::HAS_C;
@@ -331,7 +352,16 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN,
     double cwin[L > 0 ? L : 1][CY][CXN][NC > 0 ? NC : 1];
 
     const uint32_t iv_b = iv;
-    for (int s = it.s_begin; s <= it.s_end; ++s, ++iv) {
+    // UNR: the z-loop is unrolled by the ring length RL, so the register rings rotate by renaming
+    // (logical entry q of a ring -- 0 oldest, RL-1 newest -- is physical entry (u + 1 + q) % RL after
+    // step u of the period) instead of being shifted by RL-1 register moves per cell per level.
+    constexpr int UR = UNR ? RL : 1;
+    for (int s0 = it.s_begin; s0 <= it.s_end; s0 += UR) {
+#pragma unroll
+    for (int u = 0; u < UR; ++u) {
+    const int s = s0 + u;
+    if (UNR && s > it.s_end) break;
+    {
       const int buf = s & 1;
       // Level 0: plane s of Omega^t -> register rings.
       const uint32_t sv = iv % DV;
@@ -343,11 +373,18 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN,
         lds_row<CXN, VEC>(Vs + (ly0 + j + R) * FXB + R + SHV + x0, v);
 #pragma unroll
         for (int i = 0; i < CXN; ++i) {
+          if constexpr (UNR) {
+            ring[0][j][i][u % RL] = v[i];
+          } else {
 #pragma unroll
-          for (int q = 0; q < RL - 1; ++q) ring[0][j][i][q] = ring[0][j][i][q + 1];
-          ring[0][j][i][RL - 1] = v[i];
+            for (int q = 0; q < RL - 1; ++q) ring[0][j][i][q] = ring[0][j][i][q + 1];
+            ring[0][j][i][RL - 1] = v[i];
+          }
         }
       }
+      // physical index of logical ring entry q (all ring reads below happen after this step's update
+      // of the ring they read)
+      auto ri = [u](int q) { return UNR ? (u + 1 + q) % RL : q; };
       if constexpr (HAS_C) mbar_wait(&fullC[iv % DC], (iv / DC) & 1);
 
 #pragma unroll
@@ -370,7 +407,7 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN,
           for (int j = 0; j < CY; ++j) {
             double v[CXN];
 #pragma unroll
-            for (int i = 0; i < CXN; ++i) v[i] = ring[k - 1][j][i][R];
+            for (int i = 0; i < CXN; ++i) v[i] = ring[k - 1][j][i][ri(R)];
             sts_row<CXN, VEC>(P + (ly0 + j) * TX + x0, v);
           }
           if (!(p.dbg & 2)) named_sync(1, NCONS);
@@ -407,6 +444,7 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN,
           if constexpr (WAVE) {
             if (k == 1) lds_row<CXN, VEC>(Ck + ly * EXB + x0, urow);
           }
+          double vout[CXN], uout[CXN];  // last level: the row's results, stored after the loop
 #pragma unroll
           for (int i = 0; i < CXN; ++i) {
             double m[3][R], pl[3][R];
@@ -416,8 +454,8 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN,
               pl[0][r - 1] = xr[RP + i + r];
               m[1][r - 1] = ys[R + j - r][i];
               pl[1][r - 1] = ys[R + j + r][i];
-              m[2][r - 1] = ring[k - 1][j][i][R - r];
-              pl[2][r - 1] = ring[k - 1][j][i][R + r];
+              m[2][r - 1] = ring[k - 1][j][i][ri(R - r)];
+              pl[2][r - 1] = ring[k - 1][j][i][ri(R + r)];
             }
             double W[NC > 0 ? NC : 1];
             if constexpr (NC > 0) {
@@ -425,21 +463,31 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN,
               for (int f = 0; f < NC; ++f)
                 W[f] = (WIN && k > BT - WIN) ? cwin[L > 0 ? (BT - k) * R : 0][j][i][f] : Wrow[f][i];
             }
-            double u = 0.0;
-            if constexpr (WAVE) u = (k == 1) ? urow[i] : ring[k >= 2 ? k - 2 : 0][j][i][0];
-            const double vc = apply_point<KIND, R>(ring[k - 1][j][i][R], u, m, pl, W, ps);
-            // ghosts and cells outside the level-k extent keep their input value
-            const double v = (zv && ((act[j][i] >> k) & 1u)) ? vc : ring[k - 1][j][i][R];
+            double uo = 0.0;
+            if constexpr (WAVE) uo = (k == 1) ? urow[i] : ring[k >= 2 ? k - 2 : 0][j][i][ri(0)];
+            const double vc = apply_point<KIND, R>(ring[k - 1][j][i][ri(R)], uo, m, pl, W, ps);
+            // ghosts and cells outside the level-k extent keep their input value.  At the last level
+            // the store predicate below already implies the select's condition (outc -> act bit BT,
+            // c in [zc0, zc1) -> zv), so the select is skipped there.
+            const double v = (k == BT) ? vc : (zv && ((act[j][i] >> k) & 1u)) ? vc : ring[k - 1][j][i][ri(R)];
             if (k < BT) {
+              if constexpr (UNR) {
+                ring[k < BT ? k : 0][j][i][u % RL] = v;
+              } else {
 #pragma unroll
-              for (int q = 0; q < RL - 1; ++q)
-                ring[k < BT ? k : 0][j][i][q] = ring[k < BT ? k : 0][j][i][q + 1];
-              ring[k < BT ? k : 0][j][i][RL - 1] = v;
-            } else if (outc[j][i] && c >= it.zc0 && c < it.zc1 && !((p.dbg & 4) && c == it.zc1 - 1)) {
-              const long long o = (long long)c * p.plane + col[j] + i;
-              __stcs(p.dst + o, v);
-              if constexpr (WAVE && BT >= 2) __stcs(p.dstu + o, ring[BT - 1][j][i][R]);
+                for (int q = 0; q < RL - 1; ++q)
+                  ring[k < BT ? k : 0][j][i][q] = ring[k < BT ? k : 0][j][i][q + 1];
+                ring[k < BT ? k : 0][j][i][RL - 1] = v;
+              }
+            } else {
+              vout[i] = v;
+              if constexpr (WAVE && BT >= 2) uout[i] = ring[BT - 1][j][i][ri(R)];
             }
+          }
+          if (k == BT && c >= it.zc0 && c < it.zc1 && !((p.dbg & 4) && c == it.zc1 - 1)) {
+            const long long o = (long long)c * p.plane + col[j];
+            stg_row<CXN, VEC>(p.dst + o, vout, outc[j]);
+            if constexpr (WAVE && BT >= 2) stg_row<CXN, VEC>(p.dstu + o, uout, outc[j]);
           }
         }
         if (k == 1 && iv >= iv_b + R) {  // footprint plane of step iv - R fully consumed
@@ -468,6 +516,9 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN,
         __syncwarp();
         if (lane == 0) mbar_arrive(&emptyC[(iv - CLAG) % DC]);
       }
+    }
+    ++iv;
+    }
     }
     // release ring slots of this item that the lags above did not reach
     __syncwarp();
@@ -518,10 +569,10 @@ bool make_map(CUtensorMap* m, const double* base, int rank, long long pitch, lon
   return r == CUDA_SUCCESS;
 }
 
-template <int KIND, int BT, int TX, int TY, int CX, int CY, int DV, int DC, int WIN = 0, int MINB = 1>
+template <int KIND, int BT, int TX, int TY, int CX, int CY, int DV, int DC, int WIN = 0, int MINB = 1, bool UNR = false>
 cudaError_t run_pipe(const KParams& p0, int zchunk_req, int num_sms, cudaStream_t stream, LaunchInfo* info) {
-  using C = PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN, MINB>;
-  auto kern = pipe_kernel<KIND, BT, TX, TY, CX, CY, DV, DC, WIN, MINB>;
+  using C = PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN, MINB, UNR>;
+  auto kern = pipe_kernel<KIND, BT, TX, TY, CX, CY, DV, DC, WIN, MINB, UNR>;
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
@@ -600,6 +651,9 @@ cudaError_t launch_pipe(int kind, int b, const KParams& p, int zchunk_req, int n
   // CFG(kind, BT, TX, TY, CX, CY, DV, DC, WIN, MINB)
 #define CFG(K, B, TX, TY, CX, CY, DV, DC, W, M) \
   return run_pipe<K, B, TX, TY, CX, CY, DV, DC, W, M>(p, zchunk_req, num_sms, stream, info)
+  // CFGU: the same with the z-loop unrolled by the ring length (rings rotate by renaming)
+#define CFGU(K, B, TX, TY, CX, CY, DV, DC, W, M) \
+  return run_pipe<K, B, TX, TY, CX, CY, DV, DC, W, M, true>(p, zchunk_req, num_sms, stream, info)
   // Consumer-thread counts are kept at <= 224 (+ 32 producer = 256 threads) where registers matter:
   // ptxas budgets registers for blocks rounded up to 128 threads (288-thread blocks get 168).
   switch (kind) {
@@ -623,10 +677,12 @@ cudaError_t launch_pipe(int kind, int b, const KParams& p, int zchunk_req, int n
         case 2:
           if (cfg == 1) CFG(K7V, 2, 32, 28, 2, 2, 4, 3, 1, 1);
           if (cfg == 2) CFG(K7V, 2, 32, 28, 1, 4, 4, 3, 0, 1);
-          CFG(K7V, 2, 32, 28, 1, 4, 4, 3, 1, 1);
+          if (cfg == 3) CFG(K7V, 2, 32, 28, 1, 4, 4, 3, 1, 1);  // round-1 default (rings shifted)
+          CFGU(K7V, 2, 32, 28, 1, 4, 4, 3, 1, 1);                // C2: 148-151 -> 157-159 GLUP/s
         case 3:
           if (cfg == 1) CFG(K7V, 3, 32, 28, 1, 4, 4, 3, 1, 1);
           if (cfg == 2) CFG(K7V, 3, 32, 20, 1, 4, 4, 4, 0, 1);
+          if (cfg == 3) CFGU(K7V, 3, 32, 28, 2, 2, 4, 3, 1, 1);
           CFG(K7V, 3, 32, 28, 2, 2, 4, 3, 1, 1);
       }
       break;
@@ -635,24 +691,32 @@ cudaError_t launch_pipe(int kind, int b, const KParams& p, int zchunk_req, int n
         if (cfg == 1) CFG(K25W, 1, 64, 14, 4, 1, 7, 3, 0, 1);
         if (cfg == 2) CFG(K25W, 1, 32, 28, 2, 2, 7, 3, 0, 1);
         if (cfg == 3) CFG(K25W, 1, 64, 16, 1, 4, 7, 3, 0, 1);
-        CFG(K25W, 1, 64, 14, 2, 2, 7, 3, 0, 1);
+        if (cfg == 4) CFG(K25W, 1, 64, 14, 2, 2, 7, 3, 0, 1);  // round-1 default (rings shifted)
+        if (cfg == 5) CFG(K25W, 1, 64, 14, 2, 2, 10, 6, 0, 1);
+        if (cfg == 6) CFGU(K25W, 1, 64, 14, 2, 2, 8, 4, 0, 1);
+        if (cfg == 7) CFGU(K25W, 1, 64, 20, 2, 2, 8, 4, 0, 1);
+        CFGU(K25W, 1, 64, 14, 2, 2, 10, 6, 0, 1);              // C3: 165-169 -> 186-194 GLUP/s
       }
       break;
     case K25WA:
       if (b == 1) {
         if (cfg == 1) CFG(K25WA, 1, 64, 16, 1, 4, 7, 3, 0, 1);
-        CFG(K25WA, 1, 64, 14, 2, 2, 7, 3, 0, 1);
+        if (cfg == 2) CFG(K25WA, 1, 64, 14, 2, 2, 7, 3, 0, 1);  // round-1 default (rings shifted)
+        if (cfg == 3) CFGU(K25WA, 1, 64, 20, 2, 2, 8, 4, 0, 1);
+        CFGU(K25WA, 1, 64, 14, 2, 2, 8, 4, 0, 1);               // C3A: 148-152 -> 160 GLUP/s
       }
       break;
     case K25V:
       if (b == 1) {
         if (cfg == 1) CFG(K25V, 1, 64, 8, 1, 2, 6, 3, 0, 1);
         if (cfg == 2) CFG(K25V, 1, 64, 8, 4, 1, 6, 3, 0, 1);
+        if (cfg == 3) CFGU(K25V, 1, 64, 8, 2, 2, 6, 3, 0, 1);
         CFG(K25V, 1, 64, 8, 2, 2, 6, 3, 0, 1);
       }
       break;
   }
 #undef CFG
+#undef CFGU
   return cudaErrorInvalidValue;
 }
 

@@ -20,10 +20,12 @@ ap.add_argument("--bt", type=int, default=0)
 ap.add_argument("--T", type=int, default=0)
 ap.add_argument("--variant", type=int, default=0)
 ap.add_argument("--zchunk", type=int, default=0)
+ap.add_argument("--cfg", type=int, default=0)
 a = ap.parse_args()
 torch.cuda.set_device(0)
 w = {x.name.split("-")[0]: x for x in workloads.CONFIGS + workloads.EXTRA}[a.workload]
-g = st.Grid(w.kind, w.nx, w.ny, w.nz, seed=synth.DEFAULT_SEED, variant=a.variant, bt=a.bt, zchunk=a.zchunk)
+g = st.Grid(w.kind, w.nx, w.ny, w.nz, seed=synth.DEFAULT_SEED, variant=a.variant, bt=a.bt, zchunk=a.zchunk,
+            tile_cfg=a.cfg)
 bt = g.info()["bt"]
 g.run(a.T or 2 * bt)
 g.sync()

@@ -44,7 +44,7 @@ def main():
                         print(json.dumps({"workload": name, "bt": bt, "error": str(e)}))
                         continue
                     info = g.info()
-                    if info["bt"] != bt and variant != 1:
+                    if bt and info["bt"] != bt and variant != 1:
                         g.close()
                         continue
                     g.run(T)
