@@ -192,6 +192,11 @@ def main():
     ap.add_argument("--slabs", type=int, default=1,
                     help="single GPU only: run the z-slab plan with this many slabs on the one device "
                          "(loopback halo copies; measures the multi-GPU plan's overhead)")
+    ap.add_argument("--halo", default="copy", choices=["copy", "peer"],
+                    help="z-slab halo exchange: copy = edge kernels + NCCL send/recv (device copies in "
+                         "loopback) overlapped with the interior kernel; peer = fused into the kernel, "
+                         "which stores the neighbours' halo planes straight into their memory (CUDA IPC "
+                         "over NVLink across processes)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -223,12 +228,13 @@ def main():
             dist.barrier()
 
     slabs = args.slabs if world == 1 else 1
+    halo = st.ST_HALO_PEER if args.halo == "peer" else st.ST_HALO_COPY
     if slabs > 1:
         g = st.Grid(w.kind, w.nx, w.ny, w.nz, seed=synth.DEFAULT_SEED, variant=args.variant, bt=args.bt,
-                    zchunk=args.zchunk, nranks=slabs, local_slabs=slabs)
+                    zchunk=args.zchunk, nranks=slabs, local_slabs=slabs, halo=halo)
     else:
         g = st.Grid(w.kind, w.nx, w.ny, w.nz, seed=synth.DEFAULT_SEED, variant=args.variant, bt=args.bt,
-                    zchunk=args.zchunk, rank=rank, nranks=world, nccl_id=nccl_id)
+                    zchunk=args.zchunk, rank=rank, nranks=world, nccl_id=nccl_id, halo=halo)
     stream = g.stream
     for _ in range(args.warmup):
         g.run(w.T)
@@ -302,7 +308,8 @@ def main():
 
         def e2e_step():
             with st.Grid(w.kind, w.nx, w.ny, w.nz, v0=V, u0=U, coeff=coeff, variant=args.variant,
-                         bt=args.bt, zchunk=args.zchunk, rank=rank, nranks=world, nccl_id=nccl_id) as ge:
+                         bt=args.bt, zchunk=args.zchunk, rank=rank, nranks=world, nccl_id=nccl_id,
+                         halo=halo) as ge:
                 ge.run(w.T)
                 ge.read(0, out=out)
         e2e_step()
@@ -335,8 +342,10 @@ def main():
             "config": {"workload": w.name, "kind": synth.KIND_NAMES[w.kind], "nx": w.nx, "ny": w.ny,
                        "nz": w.nz, "T": w.T, "bt": bt, "variant": info["variant"],
                        "tile": [info["tile_x"], info["tile_y"]], "zchunk": info["zchunk"],
-                       "parallelism": (f"z-slab x{world} (NCCL)" if world > 1 else
-                                       f"loopback z-slab x{slabs} on 1 GPU" if slabs > 1 else "single GPU"),
+                       "parallelism": (f"z-slab x{world} ({'fused peer-store halos' if args.halo == 'peer' else 'NCCL halos'})"
+                                       if world > 1 else
+                                       f"loopback z-slab x{slabs} on 1 GPU ({args.halo} halos)" if slabs > 1
+                                       else "single GPU"),
                        "l2": "inputs larger than L2 (no flush needed)",
                        "luops_per_step": w.nx * w.ny * w.nz * w.T},
             "roofline": roofline,

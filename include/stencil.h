@@ -82,6 +82,22 @@ enum {
                             mbarriers; persistent CTAs.  The default. */
 };
 
+/* Halo exchange between z-slabs. */
+enum {
+  ST_HALO_COPY = 0, /* after every fused block: edge kernels, then the R*bt boundary planes are copied
+                       (device copies between the slabs of one handle; NCCL send/recv between
+                       processes on a comm stream) while the interior kernel runs ("halo-first",
+                       P:833-836).  The default. */
+  ST_HALO_PEER = 1  /* fused: one kernel per slab and block; the kernel stores the planes that are a
+                       z-neighbour's halo straight into the neighbour's buffer as it produces them
+                       (another slab of this handle, or the neighbour process's GPU memory mapped over
+                       NVLink with CUDA IPC), then a stream-ordered flag write in the neighbour's
+                       memory tells it the block's halos have landed (cuStreamWriteValue64 /
+                       cuStreamWaitValue64).  No edge/interior split, no copy, no NCCL on the data
+                       path.  Pipe variant only.  Across processes every rank must call
+                       stencil_peer_export / stencil_peer_import after creating and before running. */
+};
+
 /* Device allocator: return a device pointer to >= bytes (256-byte aligned) or NULL. */
 typedef void *(*st_alloc_fn)(size_t bytes, void *stream, void *user);
 typedef void (*st_free_fn)(void *ptr, size_t bytes, void *stream, void *user);
@@ -103,6 +119,9 @@ typedef struct {
   st_alloc_fn alloc;   /* NULL = cudaMalloc */
   st_free_fn free;     /* NULL = cudaFree */
   void *alloc_user;
+  int halo;            /* ST_HALO_COPY (0) or ST_HALO_PEER; used when nranks > 1.  ST_HALO_PEER across
+                          processes allocates the state buffers with cudaMalloc (CUDA IPC needs whole
+                          allocations), ignoring alloc/free for them */
 } st_opts;
 
 typedef struct {
@@ -115,6 +134,7 @@ typedef struct {
   int64_t device_bytes;           /* device memory held by the handle */
   int64_t steps_done;             /* time steps applied since creation (Omega^steps_done is level 0) */
   int64_t launches;               /* kernel launches enqueued since creation / last stats reset */
+  int halo;                       /* ST_HALO_* in effect */
 } st_info;
 
 /* Fill *o with defaults: device -1, auto variant/bt/tiles, single rank (local_slabs 1), NULL stream,
@@ -211,6 +231,20 @@ int stencil_nccl_unique_id(void *out, size_t out_bytes);
  */
 int stencil_plan_slab(int64_t nz, int R, int nranks, int rank, int bt, int64_t *own_z0,
                       int64_t *own_z1, int64_t *store_z0, int64_t *store_z1, int *bt_eff);
+
+/*
+ * ST_HALO_PEER across processes (one slab per process): wire the z-neighbours' memory.
+ * stencil_peer_export writes this rank's descriptor (CUDA IPC handles of its state buffers and of
+ * its halo-arrival flags, plus its slab geometry) into desc[0 .. ST_PEER_DESC_BYTES).  The caller
+ * moves the descriptors between processes (the Python binding all-gathers them with
+ * torch.distributed) and every rank calls stencil_peer_import with the descriptors of rank-1
+ * ("below", NULL on rank 0) and rank+1 ("above", NULL on the last rank).  Collective: all ranks must
+ * import before any rank runs.  Errors: ST_E_INVAL (wrong mode, short buffer, descriptor of the
+ * wrong rank / geometry, missing neighbour), ST_E_CUDA (IPC mapping failed, e.g. no peer access).
+ */
+#define ST_PEER_DESC_BYTES 512
+int stencil_peer_export(stencil_ctx *h, void *desc, size_t desc_bytes);
+int stencil_peer_import(stencil_ctx *h, const void *below, const void *above);
 
 /* Library version string. */
 const char *stencil_version(void);

@@ -12,11 +12,13 @@ from ._binding import (  # noqa: F401
     ST_7PT_CONST, ST_7PT_VAR, ST_25PT_WAVE, ST_25PT_VAR, ST_25PT_WAVE_A, WAVE_KINDS,
     ST_VARIANT_AUTO, ST_VARIANT_NAIVE, ST_VARIANT_STREAM, ST_VARIANT_PIPE,
     ST_OK, ST_E_INVAL, ST_E_NOMEM, ST_E_CUDA, ST_E_NCCL, ST_E_STATE,
+    ST_HALO_COPY, ST_HALO_PEER, ST_PEER_DESC_BYTES,
     EXPORTED_SYMBOLS, LIB_PATH, StencilError, StOpts, StInfo,
     lib, stencil_opts_default, stencil_create, stencil_create_seeded, stencil_run, stencil_sync,
     stencil_read, stencil_read_planes, stencil_write, stencil_info, stencil_set_timing,
     stencil_kernel_time, stencil_destroy, stencil_last_error, stencil_nccl_unique_id,
-    stencil_plan_slab, stencil_version,
+    stencil_plan_slab, stencil_version, stencil_peer_export, stencil_peer_import, peer_neighbours,
+    exchange_peer_descriptors,
     Grid, RADIUS,
 )
 

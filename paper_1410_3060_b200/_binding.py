@@ -18,6 +18,8 @@ LIB_PATH = os.environ.get("STENCIL_LIB") or os.path.join(_HERE, "libstencil.so")
 ST_7PT_CONST, ST_7PT_VAR, ST_25PT_WAVE, ST_25PT_VAR, ST_25PT_WAVE_A = 1, 2, 3, 4, 5
 ST_VARIANT_AUTO, ST_VARIANT_NAIVE, ST_VARIANT_STREAM, ST_VARIANT_PIPE = 0, 1, 2, 3
 ST_OK, ST_E_INVAL, ST_E_NOMEM, ST_E_CUDA, ST_E_NCCL, ST_E_STATE = 0, -1, -2, -3, -4, -5
+ST_HALO_COPY, ST_HALO_PEER = 0, 1
+ST_PEER_DESC_BYTES = 512
 RADIUS = {1: 1, 2: 1, 3: 4, 4: 4, 5: 4}
 N_COEFF = {1: 2, 2: 7, 3: 6, 4: 13, 5: 6}
 N_SCALARS = {1: 2, 2: 0, 3: 6, 4: 0, 5: 5}  # leading scalar entries of coeff; the rest are fields
@@ -27,7 +29,7 @@ EXPORTED_SYMBOLS = [
     "stencil_opts_default", "stencil_create", "stencil_create_seeded", "stencil_run", "stencil_sync",
     "stencil_read", "stencil_read_planes", "stencil_write", "stencil_info", "stencil_set_timing",
     "stencil_kernel_time", "stencil_destroy", "stencil_last_error", "stencil_nccl_unique_id",
-    "stencil_plan_slab", "stencil_version",
+    "stencil_plan_slab", "stencil_version", "stencil_peer_export", "stencil_peer_import",
 ]
 
 ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p)
@@ -39,14 +41,15 @@ class StOpts(ctypes.Structure):
                 ("tile_cfg", ctypes.c_int), ("local_slabs", ctypes.c_int), ("zchunk", ctypes.c_int),
                 ("rank", ctypes.c_int), ("nranks", ctypes.c_int), ("nccl_id", ctypes.c_void_p),
                 ("stream", ctypes.c_void_p), ("alloc", ALLOC_FN), ("free", FREE_FN),
-                ("alloc_user", ctypes.c_void_p)]
+                ("alloc_user", ctypes.c_void_p), ("halo", ctypes.c_int)]
 
 
 class StInfo(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int) for n in ("kind", "R", "bt", "variant", "rank", "nranks", "local_slabs",
                                              "tile_x", "tile_y", "zchunk")] + \
                [(n, ctypes.c_int64) for n in ("nx", "ny", "nz", "own_z0", "own_z1", "pitch", "plane",
-                                               "local_planes", "device_bytes", "steps_done", "launches")]
+                                               "local_planes", "device_bytes", "steps_done", "launches")] + \
+               [("halo", ctypes.c_int)]
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}
@@ -96,6 +99,8 @@ def lib():
         "stencil_plan_slab": (I, [I64, I, I, I, I, ctypes.POINTER(I64), ctypes.POINTER(I64),
                                   ctypes.POINTER(I64), ctypes.POINTER(I64), ctypes.POINTER(I)]),
         "stencil_version": (ctypes.c_char_p, []),
+        "stencil_peer_export": (I, [P, P, ctypes.c_size_t]),
+        "stencil_peer_import": (I, [P, P, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -211,6 +216,34 @@ def stencil_nccl_unique_id() -> bytes:
     return buf.raw
 
 
+def stencil_peer_export(h) -> bytes:
+    buf = ctypes.create_string_buffer(ST_PEER_DESC_BYTES)
+    _check(lib().stencil_peer_export(h, buf, ST_PEER_DESC_BYTES))
+    return buf.raw
+
+
+def stencil_peer_import(h, below: bytes | None, above: bytes | None):
+    b = None if below is None else ctypes.create_string_buffer(bytes(below), ST_PEER_DESC_BYTES)
+    a = None if above is None else ctypes.create_string_buffer(bytes(above), ST_PEER_DESC_BYTES)
+    _check(lib().stencil_peer_import(h, b, a))
+
+
+def peer_neighbours(descs, rank):
+    """(below, above) descriptors of rank's z-neighbours from the all-gathered list (None at the ends)."""
+    n = len(descs)
+    if not 0 <= rank < n:
+        raise ValueError(f"rank {rank} outside 0..{n - 1}")
+    return (descs[rank - 1] if rank > 0 else None), (descs[rank + 1] if rank < n - 1 else None)
+
+
+def exchange_peer_descriptors(desc: bytes, group=None):
+    """All-gather every rank's ST_HALO_PEER descriptor over torch.distributed (host plumbing only)."""
+    import torch.distributed as dist
+    out = [None] * dist.get_world_size(group)
+    dist.all_gather_object(out, desc, group=group)
+    return out
+
+
 def stencil_plan_slab(nz, R, nranks, rank, bt):
     a, b, c, d = (ctypes.c_int64() for _ in range(4))
     e = ctypes.c_int()
@@ -267,7 +300,7 @@ class Grid:
 
     def __init__(self, kind, nx, ny, nz, *, seed=None, scalars=None, v0=None, u0=None, coeff=None,
                  variant=ST_VARIANT_AUTO, bt=0, zchunk=0, tile_cfg=0, rank=0, nranks=1, nccl_id=None,
-                 local_slabs=1,
+                 local_slabs=1, halo=ST_HALO_COPY,
                  device=None, stream=None, torch_memory=True, tuned=False):
         import torch
         if tuned and bt == 0:  # plan measured by tools/tune.py for this kind and shape, if any
@@ -280,6 +313,7 @@ class Grid:
         o.device = torch.cuda.current_device() if device is None else device
         o.variant, o.bt, o.zchunk, o.tile_cfg = variant, bt, zchunk, tile_cfg
         o.rank, o.nranks, o.local_slabs = rank, nranks, local_slabs
+        o.halo = halo
         self._id = None
         if nranks > 1 and local_slabs == 1:
             self._id = ctypes.create_string_buffer(bytes(nccl_id), 128)
@@ -298,6 +332,11 @@ class Grid:
             if coeff is None:
                 coeff = scalars
             self.h = stencil_create(kind, nx, ny, nz, coeff, v0, u0, o)
+        self.rank, self.nranks, self.halo = rank, nranks, halo
+        self._ipc = halo == ST_HALO_PEER and nranks > 1 and local_slabs == 1
+        if self._ipc:  # fused halo exchange across processes: wire the neighbours' memory (collective)
+            descs = exchange_peer_descriptors(stencil_peer_export(self.h))
+            stencil_peer_import(self.h, *peer_neighbours(descs, rank))
 
     @property
     def padded_shape(self):
@@ -320,7 +359,14 @@ class Grid:
         return stencil_read_planes(self.h, level, z0, z1, out)
 
     def write(self, level, arr):
-        stencil_write(self.h, level, arr)
+        if self._ipc:  # neighbours store into this rank's halos: write between two barriers
+            import torch.distributed as dist
+            self.sync()
+            dist.barrier()
+            stencil_write(self.h, level, arr)
+            dist.barrier()
+        else:
+            stencil_write(self.h, level, arr)
 
     def info(self):
         return stencil_info(self.h)
@@ -333,7 +379,7 @@ class Grid:
 
     def close(self):
         if getattr(self, "h", None):
-            stencil_destroy(self.h)
+            stencil_destroy(self.h)  # ST_HALO_PEER: waits until the neighbours' last stores landed
             self.h = None
 
     def __enter__(self):

@@ -32,6 +32,14 @@ struct KParams {
                // skip level barriers; fault injection for the mutation tests (STENCIL_FAULT):
                // bit 2 = never write the last plane of a z-chunk, bit 3 = skip work item 0
   unsigned int* sched;  // pipe kernel: 2 zeroed device counters (next work item, CTAs done)
+  // Fused halo exchange (pipe kernel only): last-level output planes in local range
+  // [rz0[q], rz1[q]) are also stored through rdst[q] (and rdstu[q], wave second level), a pointer into
+  // a z-neighbour's buffer pre-offset so that the same element offset addresses the same global cell.
+  // NULL = no remote target.  rfence: end with a system-scope fence (peer memory of another process).
+  double* rdst[2];
+  double* rdstu[2];
+  int rz0[2], rz1[2];
+  int rfence;
   int walign;  // pipe kernel: tiles write sector-aligned output segments (STENCIL_WALIGN=1; default 0:
                // measured slower under the power cap for OX % 4 != 0, profiles/r01_summary.md)
 };

@@ -488,6 +488,15 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN,
             const long long o = (long long)c * p.plane + col[j];
             stg_row<CXN, VEC>(p.dst + o, vout, outc[j]);
             if constexpr (WAVE && BT >= 2) stg_row<CXN, VEC>(p.dstu + o, uout, outc[j]);
+            // fused halo exchange: planes that are a z-neighbour's halo planes are
+            // also stored straight into the neighbour's buffer (peer memory over NVLink, or another
+            // slab on this device), tile by tile as they are produced
+#pragma unroll
+            for (int q = 0; q < 2; ++q)
+              if (p.rdst[q] && c >= p.rz0[q] && c < p.rz1[q]) {
+                stg_row<CXN, VEC>(p.rdst[q] + o, vout, outc[j]);
+                if constexpr (WAVE && BT >= 2) stg_row<CXN, VEC>(p.rdstu[q] + o, uout, outc[j]);
+              }
           }
         }
         if (k == 1 && iv >= iv_b + R) {  // footprint plane of step iv - R fully consumed
@@ -528,6 +537,8 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN,
         for (uint32_t i = (iv >= iv_b + CLAG ? iv - CLAG : iv_b); i < iv; ++i) mbar_arrive(&emptyC[i % DC]);
     }
   }
+  // peer stores of another process's memory are ordered before the stream's completion signal
+  if (p.rfence) __threadfence_system();
 }
 
 // ------------------------------------------------------------------------------------------------ host

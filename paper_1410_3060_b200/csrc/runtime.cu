@@ -9,15 +9,21 @@
 //   * slabs of the same handle (opts.local_slabs = nranks, one process, one GPU): device-to-device
 //     copies on the handle's stream ("loopback"; the same plan as multi-GPU, testable on one GPU);
 //   * slabs of different processes (one slab per process and GPU): NCCL send/recv in one group.
+// With opts.halo = ST_HALO_PEER the exchange is fused into the kernel instead: one launch per slab
+// and block stores the neighbours' halo planes straight into their buffers (pipe kernel, KParams
+// rdst), and across processes a stream-ordered flag write into the neighbour's memory (CUDA IPC)
+// announces the block; the neighbour's stream waits on that flag before its next block.
 #include "../../include/stencil.h"
 #include "kernels.cuh"
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
 
 #include <algorithm>
 #include <atomic>
+#include <mutex>
 #include <cstdlib>
 #include <cstdarg>
 #include <cstdio>
@@ -82,6 +88,42 @@ Nccl* nccl() {
   return &n;
 }
 
+// ---------------------------------------------------------------- stream memory operations
+// (driver API, resolved through the runtime so the library does not link libcuda directly)
+using WaitValue64Fn = CUresult (*)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+using WriteValue64Fn = CUresult (*)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+struct MemOps {
+  WaitValue64Fn wait = nullptr;
+  WriteValue64Fn write = nullptr;
+};
+const MemOps& memops() {
+  static MemOps m;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue64", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      m.wait = reinterpret_cast<WaitValue64Fn>(f);
+    f = nullptr;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue64", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      m.write = reinterpret_cast<WriteValue64Fn>(f);
+  });
+  return m;
+}
+
+// Descriptor of one rank's memory for ST_HALO_PEER (stencil_peer_export / import).
+struct PeerDesc {
+  uint64_t magic;
+  int32_t rank, nranks, kind, nbuf, bt, pad;
+  int64_t nx, ny, nz, pitch, plane, store_z0, zl;
+  cudaIpcMemHandle_t buf[4];
+  cudaIpcMemHandle_t flags;
+};
+constexpr uint64_t kPeerMagic = 0x3330363031343153ull;  // "S1410603"
+static_assert(sizeof(PeerDesc) <= ST_PEER_DESC_BYTES, "peer descriptor too large");
+
 // One z-slab: global padded planes [store_z0, store_z1) stored, [own_z0, own_z1) owned,
 // interior planes [lo, hi) computed.
 struct Slab {
@@ -133,6 +175,19 @@ struct stencil_ctx {
   bool halo_pending = false;
   bool overlap = true;  // STENCIL_NO_OVERLAP=1: bulk-synchronous schedule (one launch, then exchange)
 
+  // ST_HALO_PEER (fused halo exchange)
+  int halo = ST_HALO_COPY;
+  int64_t blocks = 0;            // fused blocks run since creation (the flag protocol's counter)
+  bool peer_ready = false;       // neighbours wired (loopback: at create; processes: after import)
+  bool ipc = false;              // peers are other processes (CUDA IPC)
+  uint64_t* flags = nullptr;     // this rank's halo-arrival counters: [0] from below, [1] from above
+  struct Peer {
+    bool on = false;
+    double* buf[4] = {nullptr, nullptr, nullptr, nullptr};  // raw state buffers (IPC-mapped)
+    uint64_t* flags = nullptr;                              // the neighbour's counters
+    int64_t store_z0 = 0;
+  } peer[2];                     // [0] below (rank - 1), [1] above (rank + 1)
+
   double* at(const Slab& s, int b) const { return s.buf[b] + xoff; }
   int64_t own_z0() const { return slabs.front().own_z0; }
   int64_t own_z1() const { return slabs.back().own_z1; }
@@ -179,6 +234,13 @@ void* dev_alloc(stencil_ctx* h, size_t bytes) {
 
 void release(stencil_ctx* h) {
   cudaStreamSynchronize(h->stream);
+  for (auto& pr : h->peer) {
+    if (!h->ipc || !pr.on) continue;
+    for (auto* b : pr.buf)
+      if (b) cudaIpcCloseMemHandle(b);
+    if (pr.flags) cudaIpcCloseMemHandle(pr.flags);
+    pr = stencil_ctx::Peer{};
+  }
   for (auto& a : h->allocs) {
     if (h->free_fn) h->free_fn(a.first, a.second, (void*)h->stream, h->alloc_user);
     else cudaFree(a.first);
@@ -262,6 +324,11 @@ int create_common(stencil_ctx** out, int kind, int64_t nx, int64_t ny, int64_t n
     return ST_E_INVAL;
   }
   if (nz < o.nranks) { set_err("nz=%lld < nranks=%d", (long long)nz, o.nranks); return ST_E_INVAL; }
+  if (o.halo != ST_HALO_COPY && o.halo != ST_HALO_PEER) { set_err("bad halo mode %d", o.halo); return ST_E_INVAL; }
+  if (o.halo == ST_HALO_PEER && o.variant != ST_VARIANT_AUTO && o.variant != ST_VARIANT_PIPE) {
+    set_err("halo mode ST_HALO_PEER needs the pipe variant (got variant %d)", o.variant);
+    return ST_E_INVAL;
+  }
   const bool use_nccl = o.nranks > 1 && local == 1;
   if (use_nccl && !o.nccl_id) { set_err("nranks > 1 with one slab per process needs nccl_id"); return ST_E_INVAL; }
 
@@ -287,6 +354,12 @@ int create_common(stencil_ctx** out, int kind, int64_t nx, int64_t ny, int64_t n
   h->alloc = o.alloc; h->free_fn = o.free; h->alloc_user = o.alloc_user;
   h->zchunk_req = o.zchunk;
   h->tile_cfg = o.tile_cfg;
+  h->halo = o.nranks > 1 ? o.halo : ST_HALO_COPY;
+  h->ipc = h->halo == ST_HALO_PEER && use_nccl;
+  if (h->ipc) {  // IPC maps whole allocations: state buffers and flags come straight from cudaMalloc
+    h->alloc = nullptr;
+    h->free_fn = nullptr;
+  }
   CK(cudaSetDevice(dev), "cudaSetDevice");
   CK(cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, dev), "device attribute");
 
@@ -332,6 +405,15 @@ int create_common(stencil_ctx** out, int kind, int64_t nx, int64_t ny, int64_t n
   }
   h->lv0 = 0;
   h->lv1 = 1;
+  if (h->halo == ST_HALO_PEER) {
+    if (h->ipc) {
+      h->flags = (uint64_t*)dev_alloc(h, 256);
+      if (!h->flags) { set_err("device allocation of 256 bytes failed (halo flags)"); return ST_E_NOMEM; }
+      CK(cudaMemsetAsync(h->flags, 0, 256, h->stream), "zero halo flags");
+    } else {  // loopback: the neighbours are the handle's own slabs, stream-ordered
+      h->peer_ready = true;
+    }
+  }
   h->sched = (unsigned int*)dev_alloc(h, 256);
   if (!h->sched) { set_err("device allocation of 256 bytes failed"); return ST_E_NOMEM; }
   CK(cudaMemsetAsync(h->sched, 0, 256, h->stream), "zero work counters");
@@ -458,11 +540,42 @@ int exchange(stencil_ctx* h, int b, int64_t depth, cudaStream_t cs) {
   return ST_OK;
 }
 
+// ST_HALO_PEER: the remote targets of slab s's output planes.  Side q = 0 (below) receives planes
+// [lo, lo + H) of the new level(s), side 1 (above) planes [hi - H, hi): exactly the halo planes the
+// neighbour stores (its store range reaches H = R*bt planes past its owned planes).
+void peer_targets(stencil_ctx* h, const Slab& s, int d0, int d1, st::KParams& p) {
+  const int64_t H = (int64_t)h->R * h->bt - ((env_int("STENCIL_FAULT") & 1) ? 1 : 0);  // fault: too shallow
+  for (int q = 0; q < 2; ++q) {
+    const Slab* n = nullptr;
+    double* const* nbuf = nullptr;
+    int64_t nz0 = 0;
+    if (!h->ipc) {
+      const int idx = (int)(&s - h->slabs.data()) + (q == 0 ? -1 : 1);
+      if (idx < 0 || idx >= (int)h->slabs.size()) continue;
+      n = &h->slabs[idx];
+      nbuf = n->buf;
+      nz0 = n->store_z0;
+    } else {
+      if (!h->peer[q].on) continue;
+      nbuf = h->peer[q].buf;
+      nz0 = h->peer[q].store_z0;
+    }
+    const int64_t shift = (s.store_z0 - nz0) * h->plane + h->xoff;  // same global cell, other slab
+    p.rdst[q] = nbuf[d0] + shift;
+    p.rdstu[q] = d1 >= 0 ? nbuf[d1] + shift : nullptr;
+    const int64_t g0 = q == 0 ? s.lo : s.hi - H, g1 = q == 0 ? s.lo + H : s.hi;
+    p.rz0[q] = (int)(g0 - s.store_z0);
+    p.rz1[q] = (int)(g1 - s.store_z0);
+  }
+  p.rfence = h->ipc ? 1 : 0;
+}
+
 // Launch the kernel of the handle's variant for b levels over output planes [z0, z1) (global padded
-// indices) of slab s.
-int launch_range(stencil_ctx* h, Slab& s, int b, int d0, int d1, int64_t z0, int64_t z1) {
+// indices) of slab s; peer = also store the neighbours' halo planes into their buffers.
+int launch_range(stencil_ctx* h, Slab& s, int b, int d0, int d1, int64_t z0, int64_t z1, bool peer = false) {
   if (z1 <= z0) return ST_OK;
   st::KParams p = base_params(h, s);
+  if (peer) peer_targets(h, s, d0, d1, p);
   p.zo0 = (int)(z0 - s.store_z0);
   p.zo1 = (int)(z1 - s.store_z0);
   p.src = h->at(s, h->lv0);
@@ -514,8 +627,39 @@ int run_block(stencil_ctx* h, int b) {
     new1 = spare[1];
   }
   int rc = ST_OK;
-  const int64_t depth = (int64_t)h->R * b;
-  if (h->nranks == 1) {
+  // The halo exchanged after every block is the full stored depth H = R*bt, also after a shorter
+  // remainder block (b = T mod bt): the next run's first block needs H planes of the new level.
+  const int64_t depth = (int64_t)h->R * h->bt;
+  if (h->nranks > 1 && h->halo == ST_HALO_PEER) {
+    // Fused exchange: one launch per slab, the kernel stores the neighbours' halo planes itself.
+    if (!h->peer_ready) {
+      set_err("ST_HALO_PEER across processes: call stencil_peer_import on every rank before running");
+      return ST_E_STATE;
+    }
+    const MemOps& m = memops();
+    if (h->ipc) {
+      // wait until both neighbours have stored block blocks-1's halos into this rank's buffers (and
+      // thereby finished reading the buffers this block's remote stores overwrite)
+      if (!m.wait || !m.write) { set_err("stream memory operations unavailable"); h->poisoned = true; return ST_E_CUDA; }
+      for (int q = 0; q < 2; ++q)
+        if (h->peer[q].on) {
+          CUresult r = m.wait((CUstream)h->stream, (CUdeviceptr)(h->flags + q), (cuuint64_t)h->blocks,
+                              CU_STREAM_WAIT_VALUE_GEQ);
+          if (r != CUDA_SUCCESS) { set_err("cuStreamWaitValue64 failed (%d)", (int)r); h->poisoned = true; return ST_E_CUDA; }
+        }
+    }
+    for (auto& s : h->slabs)
+      if ((rc = launch_range(h, s, b, d0, d1, s.lo, s.hi, true))) return rc;
+    if (h->ipc) {
+      // announce: neighbour below counts arrivals from above in its flags[1], neighbour above in [0]
+      for (int q = 0; q < 2; ++q)
+        if (h->peer[q].on) {
+          CUresult r = m.write((CUstream)h->stream, (CUdeviceptr)(h->peer[q].flags + (1 - q)),
+                               (cuuint64_t)(h->blocks + 1), CU_STREAM_WRITE_VALUE_DEFAULT);
+          if (r != CUDA_SUCCESS) { set_err("cuStreamWriteValue64 failed (%d)", (int)r); h->poisoned = true; return ST_E_CUDA; }
+        }
+    }
+  } else if (h->nranks == 1) {
     for (auto& s : h->slabs)
       if ((rc = launch_range(h, s, b, d0, d1, s.lo, s.hi))) return rc;
   } else {
@@ -558,7 +702,23 @@ int run_block(stencil_ctx* h, int b) {
   h->lv0 = new0;
   h->lv1 = new1;
   h->steps += b;
+  h->blocks++;
   return rc;
+}
+
+// ST_HALO_PEER across processes: enqueue a wait until both neighbours have delivered every block run
+// so far (no remote store into this rank's memory is still in flight afterwards).
+int wait_peers(stencil_ctx* h) {
+  if (!h->ipc || !h->peer_ready) return ST_OK;
+  const MemOps& m = memops();
+  if (!m.wait) { set_err("stream memory operations unavailable"); h->poisoned = true; return ST_E_CUDA; }
+  for (int q = 0; q < 2; ++q)
+    if (h->peer[q].on) {
+      CUresult r = m.wait((CUstream)h->stream, (CUdeviceptr)(h->flags + q), (cuuint64_t)h->blocks,
+                          CU_STREAM_WAIT_VALUE_GEQ);
+      if (r != CUDA_SUCCESS) { set_err("cuStreamWaitValue64 failed (%d)", (int)r); h->poisoned = true; return ST_E_CUDA; }
+    }
+  return ST_OK;
 }
 
 int check_handle(stencil_ctx* h) {
@@ -721,6 +881,7 @@ int stencil_run(stencil_ctx* h, int64_t T) {
 int stencil_sync(stencil_ctx* h) {
   int rc = check_handle(h);
   if (rc) return rc;
+  if ((rc = wait_peers(h))) return rc;
   cudaError_t e = cudaStreamSynchronize(h->stream);
   if (e != cudaSuccess) return cuda_fail(h, e, "stream synchronize");
   return ST_OK;
@@ -780,6 +941,7 @@ int stencil_write(stencil_ctx* h, int level, const double* in, int64_t in_elems)
   if (!in || in_elems < total) { set_err("in must hold %lld doubles", (long long)total); return ST_E_INVAL; }
   Guard g(h);
   if (!g.ok) { set_err("handle used concurrently"); return ST_E_STATE; }
+  if ((rc = wait_peers(h))) return rc;
   cudaError_t e = cudaSuccess;
   for (auto& s : h->slabs) {
     if (e == cudaSuccess) e = upload_planes(h, s, s.buf[level == 0 ? h->lv0 : h->lv1], in);
@@ -807,6 +969,66 @@ int stencil_info(const stencil_ctx* h, st_info* o) {
   for (auto& s : h->slabs) zl += s.zl;
   o->local_planes = zl;
   o->device_bytes = h->device_bytes; o->steps_done = h->steps; o->launches = h->launches;
+  o->halo = h->halo;
+  return ST_OK;
+}
+
+int stencil_peer_export(stencil_ctx* h, void* desc, size_t desc_bytes) {
+  int rc = check_handle(h);
+  if (rc) return rc;
+  if (!desc || desc_bytes < ST_PEER_DESC_BYTES) { set_err("desc must hold %d bytes", ST_PEER_DESC_BYTES); return ST_E_INVAL; }
+  if (!h->ipc) { set_err("stencil_peer_export: handle is not in ST_HALO_PEER mode across processes"); return ST_E_INVAL; }
+  CK(cudaSetDevice(h->device), "cudaSetDevice");
+  const Slab& s = h->slabs.front();
+  PeerDesc d;
+  memset(&d, 0, sizeof d);
+  d.magic = kPeerMagic;
+  d.rank = h->rank; d.nranks = h->nranks; d.kind = h->kind; d.nbuf = h->nbuf; d.bt = h->bt;
+  d.nx = h->nx; d.ny = h->ny; d.nz = h->nz; d.pitch = h->pitch; d.plane = h->plane;
+  d.store_z0 = s.store_z0; d.zl = s.zl;
+  for (int b = 0; b < h->nbuf; ++b) CK(cudaIpcGetMemHandle(&d.buf[b], s.buf[b]), "cudaIpcGetMemHandle");
+  CK(cudaIpcGetMemHandle(&d.flags, h->flags), "cudaIpcGetMemHandle");
+  memset(desc, 0, ST_PEER_DESC_BYTES);
+  memcpy(desc, &d, sizeof d);
+  return ST_OK;
+}
+
+int stencil_peer_import(stencil_ctx* h, const void* below, const void* above) {
+  int rc = check_handle(h);
+  if (rc) return rc;
+  if (!h->ipc) { set_err("stencil_peer_import: handle is not in ST_HALO_PEER mode across processes"); return ST_E_INVAL; }
+  if (h->peer_ready) { set_err("stencil_peer_import: already imported"); return ST_E_STATE; }
+  if ((h->rank > 0) != (below != nullptr) || (h->rank < h->nranks - 1) != (above != nullptr)) {
+    set_err("stencil_peer_import: rank %d of %d needs %s below and %s above", h->rank, h->nranks,
+            h->rank > 0 ? "a descriptor" : "NULL", h->rank < h->nranks - 1 ? "a descriptor" : "NULL");
+    return ST_E_INVAL;
+  }
+  CK(cudaSetDevice(h->device), "cudaSetDevice");
+  const void* src[2] = {below, above};
+  for (int q = 0; q < 2; ++q) {
+    if (!src[q]) continue;
+    PeerDesc d;
+    memcpy(&d, src[q], sizeof d);
+    const int want = h->rank + (q == 0 ? -1 : 1);
+    if (d.magic != kPeerMagic || d.rank != want || d.nranks != h->nranks || d.kind != h->kind ||
+        d.nbuf != h->nbuf || d.bt != h->bt || d.nx != h->nx || d.ny != h->ny || d.nz != h->nz ||
+        d.pitch != h->pitch || d.plane != h->plane) {
+      set_err("stencil_peer_import: descriptor %s does not describe rank %d of this grid", q ? "above" : "below", want);
+      return ST_E_INVAL;
+    }
+    auto& pr = h->peer[q];
+    for (int b = 0; b < h->nbuf; ++b) {
+      void* ptr = nullptr;
+      CK(cudaIpcOpenMemHandle(&ptr, d.buf[b], cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+      pr.buf[b] = (double*)ptr;
+    }
+    void* fp = nullptr;
+    CK(cudaIpcOpenMemHandle(&fp, d.flags, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+    pr.flags = (uint64_t*)fp;
+    pr.store_z0 = d.store_z0;
+    pr.on = true;
+  }
+  h->peer_ready = true;
   return ST_OK;
 }
 
@@ -838,6 +1060,7 @@ int stencil_kernel_time(stencil_ctx* h, double* ms, int64_t* launches, int reset
 int stencil_destroy(stencil_ctx* h) {
   if (!h) return ST_OK;
   cudaSetDevice(h->device);
+  if (!h->poisoned) wait_peers(h);  // no neighbour may still be storing into this rank's buffers
   release(h);
   delete h;
   return ST_OK;

@@ -1,6 +1,8 @@
 """The multi-GPU z-slab plan on one GPU: a handle holding all P slabs
 ("loopback": halos exchanged by device copies after every fused block, the same plan and kernels as the
-NCCL path) must reproduce the single-slab run bitwise (G4 across slab counts) and match the oracle."""
+NCCL path; or, with ST_HALO_PEER, stored by the kernel straight into the neighbour slab -- the fused
+exchange of SURVEY NEXT-2) must reproduce the single-slab run bitwise (G4 across slab counts) and match
+the oracle."""
 import numpy as np
 import pytest
 
@@ -14,7 +16,8 @@ pytestmark = pytest.mark.gpu
 
 def run(kind, n, T, **kw):
     with st.Grid(kind, *n, seed=31, **kw) as g:
-        g.run(T)
+        for t in (T if isinstance(T, tuple) else (T,)):  # a tuple = consecutive stencil_run calls
+            g.run(t)
         new = g.read(0)
         old = g.read(1) if kind in WAVES else None
         info = g.info()
@@ -84,3 +87,40 @@ def test_invalid_slab_options():
         st.Grid(synth.K7V, 8, 8, 8, seed=1, nranks=2, local_slabs=3)
     with pytest.raises(st.StencilError):
         st.Grid(synth.K25V, 8, 8, 12, seed=1, nranks=4, local_slabs=4)  # 3-plane slabs < R = 4
+
+
+@pytest.mark.parametrize("kind,n,T", CASES)
+@pytest.mark.parametrize("P", [2, 3, 5])
+def test_peer_halo_bitwise_equal_single(kind, n, T, P):
+    """Fused halo exchange (ST_HALO_PEER): one launch per slab and block, the kernel stores the
+    neighbours' halo planes itself; bitwise equal to one slab for every bt the slabs allow."""
+    ref = run(kind, n, T)
+    R = synth.RADIUS[kind]
+    for bt in sorted({0, 1, 2 if R == 1 else 1, 3 if R == 1 else 1}):
+        got = run(kind, n, T, nranks=P, local_slabs=P, halo=st.ST_HALO_PEER, bt=bt)
+        info = got[2]
+        assert info["halo"] == st.ST_HALO_PEER
+        b = info["bt"]
+        assert info["launches"] == P * -(-T // b)  # no edge/interior split, no copies
+        assert np.array_equal(got[0], ref[0]), bt
+        if kind in WAVES:
+            assert np.array_equal(got[1], ref[1]), bt
+
+
+@pytest.mark.parametrize("kind,bt", [(synth.K7C, 4), (synth.K7V, 2), (synth.K7V, 3)])
+@pytest.mark.parametrize("halo", [0, 1])
+def test_remainder_block_then_next_run(kind, bt, halo):
+    """run(T1) ending in a short block (T1 mod bt != 0) followed by run(T2): the halos after the short
+    block must still cover the full R*bt depth the next run's first block reads."""
+    n = (40, 33, 37)
+    T = (bt + 1, 2 * bt, bt - 1 if bt > 1 else 1)
+    ref = run(kind, n, T)
+    got = run(kind, n, T, nranks=3, local_slabs=3, bt=bt, halo=halo)
+    assert got[2]["bt"] == bt
+    assert np.array_equal(got[0], ref[0])
+
+
+def test_peer_halo_needs_pipe_variant():
+    with pytest.raises(st.StencilError):
+        st.Grid(synth.K7V, 16, 16, 16, seed=1, nranks=2, local_slabs=2, halo=st.ST_HALO_PEER,
+                variant=st.ST_VARIANT_STREAM)

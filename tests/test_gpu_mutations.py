@@ -1,6 +1,6 @@
 """Mutation tests: inject a fault into the CUDA path and check that the parity
 and invariance checks used elsewhere in the suite catch it.  Faults (STENCIL_FAULT bits, test-only):
-1 = multi-slab halo exchanged one plane too shallow, 4 = the last plane of every z-chunk never written
+1 = multi-slab halo exchanged (or, fused, stored into the neighbour) one plane too shallow, 4 = the last plane of every z-chunk never written
 (stale plane), 8 = work item 0 skipped (stale tile)."""
 import numpy as np
 import pytest
@@ -20,7 +20,8 @@ def _parity_err(kind, n, T, **kw):
 
 
 @pytest.mark.parametrize("kind", [synth.K7V, synth.K25V])
-@pytest.mark.parametrize("fault,extra", [(4, {}), (8, {}), (1, {"nranks": 3, "local_slabs": 3})])
+@pytest.mark.parametrize("fault,extra", [(4, {}), (8, {}), (1, {"nranks": 3, "local_slabs": 3}),
+                                         (1, {"nranks": 3, "local_slabs": 3, "halo": 1})])
 def test_injected_fault_is_detected(monkeypatch, kind, fault, extra):
     n = (40, 33, 37) if synth.RADIUS[kind] == 1 else (70, 20, 41)
     T = 5

@@ -1,5 +1,5 @@
-"""The N > 1 path's host logic on CPU: z-slab plan (stencil_plan_slab) + per-block halo exchange of depth
-R*b, run with world_size 2 (and 3) over torch.distributed `gloo` processes.  Each rank advances its slab
+"""The N > 1 path's host logic on CPU: z-slab plan (stencil_plan_slab) + per-block halo exchange of the
+full stored depth R*bt (also after a short remainder block), run with world_size 2 (and 3) over torch.distributed `gloo` processes.  Each rank advances its slab
 with the oracle on its stored planes (halo planes act as fixed ghosts during a block, exact for the
 owned planes by the R-per-step cone argument) and exchanges the R*b boundary planes of the new levels
 after every block -- the schedule runtime.cu runs with NCCL.  The concatenated owned planes must equal
@@ -63,14 +63,15 @@ def _worker(rank, world, port, kind, n, T, bt, out_dir):
         inp = synth.make_inputs(kind, nx, ny, nz, seed=21, box=box)
         V, U = inp.V, inp.U
         nz_box = V.shape[0] - 2 * R
-        left = T
-        while left > 0:
-            b = min(b_eff, left)
-            oracle.run_arrays(kind, nx, ny, nz_box, V, U, inp.coef, inp.scalars, b, 1)
-            _exchange(V, plan, rank, world, R * b, R)
-            if kind == synth.K25W:
-                _exchange(U, plan, rank, world, R * b, R)
-            left -= b
+        for Tr in (T if isinstance(T, tuple) else (T,)):  # consecutive stencil_run calls
+            left = Tr
+            while left > 0:
+                b = min(b_eff, left)
+                oracle.run_arrays(kind, nx, ny, nz_box, V, U, inp.coef, inp.scalars, b, 1)
+                _exchange(V, plan, rank, world, R * b_eff, R)
+                if kind == synth.K25W:
+                    _exchange(U, plan, rank, world, R * b_eff, R)
+                left -= b
         z0 = plan["store_z0"]
         own = V[plan["own_z0"] - z0: plan["own_z1"] - z0]
         own_u = U[plan["own_z0"] - z0: plan["own_z1"] - z0]
@@ -85,15 +86,44 @@ def _worker(rank, world, port, kind, n, T, bt, out_dir):
     (synth.K7C, (7, 6, 13), 9, 4, 3),
     (synth.K25V, (9, 10, 26), 5, 2, 2),
     (synth.K25W, (9, 8, 27), 5, 3, 3),
+    (synth.K7V, (9, 8, 21), (3, 4, 2), 2, 3),   # remainder block, then more runs
+    (synth.K7C, (7, 6, 25), (5, 7), 4, 2),
 ])
 def test_slab_schedule_gloo_equals_global(tmp_path, kind, n, T, bt, world):
     port = _free_port()
     mp.spawn(_worker, args=(world, port, kind, n, T, bt, str(tmp_path)), nprocs=world, join=True)
     inp = synth.make_inputs(kind, *n, seed=21)
-    ref_v, ref_u = oracle.run(inp, T, nthreads=1)
+    ref_v, ref_u = oracle.run(inp, sum(T) if isinstance(T, tuple) else T, nthreads=1)
     got_v = np.concatenate([np.load(tmp_path / f"r{r}_v.npy") for r in range(world)])
     assert got_v.shape == ref_v.shape
     assert np.array_equal(got_v, ref_v)
     if kind == synth.K25W:
         got_u = np.concatenate([np.load(tmp_path / f"r{r}_u.npy") for r in range(world)])
         assert np.array_equal(got_u, ref_u)
+
+
+def _desc_worker(rank, world, port, out_dir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        desc = bytes([rank]) * st.ST_PEER_DESC_BYTES  # stands in for stencil_peer_export's bytes
+        descs = st.exchange_peer_descriptors(desc)
+        below, above = st.peer_neighbours(descs, rank)
+        np.save(os.path.join(out_dir, f"d{rank}.npy"),
+                np.array([-1 if below is None else below[0], -1 if above is None else above[0],
+                          len(descs), min(len(d) for d in descs)]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_peer_descriptor_exchange_gloo(tmp_path, world):
+    """ST_HALO_PEER's host plumbing: every rank all-gathers the descriptors and imports rank-1's as
+    `below` and rank+1's as `above` (None at the ends)."""
+    port = _free_port()
+    mp.spawn(_desc_worker, args=(world, port, str(tmp_path)), nprocs=world, join=True)
+    for r in range(world):
+        below, above, n, size = np.load(tmp_path / f"d{r}.npy")
+        assert below == (r - 1 if r > 0 else -1) and above == (r + 1 if r < world - 1 else -1)
+        assert n == world and size == st.ST_PEER_DESC_BYTES
