@@ -7,8 +7,10 @@ workload (T time steps, i.e. ceil(T/bt) fused-level kernel launches), inputs res
   N = 1   : configs[1] = C2, 7-point variable coefficients, 512^3 interior, T = 100 (--workload picks
             another BASELINE.json config: C1..C5).
   N > 1   : launched by torchrun, one rank per GPU.  Weak scaling of the same workload: the global
-            grid is nx x ny x (nz * N), split into N z-slabs with R*bt-deep halos exchanged by NCCL
-            send/recv after every fused block.  value = all ranks' LUPs / max-over-
+            grid is nx x ny x (nz * N), split into N z-slabs with R*bt-deep halos.  --halo peer (default):
+            the kernel stores the neighbours' halo planes straight into their GPU memory (CUDA IPC over
+            NVLink) and a stream-ordered flag announces each block; --halo copy: edge
+            kernels + NCCL send/recv overlapped with the interior kernel.  value = all ranks' LUPs / max-over-
             ranks device time.
   --impl reference : the CPU oracle (oracle/, test infrastructure) timed on this host's cores on a
             bounded sample of the same workload (this tier's reference arm; rank 0 only).
@@ -192,7 +194,7 @@ def main():
     ap.add_argument("--slabs", type=int, default=1,
                     help="single GPU only: run the z-slab plan with this many slabs on the one device "
                          "(loopback halo copies; measures the multi-GPU plan's overhead)")
-    ap.add_argument("--halo", default="copy", choices=["copy", "peer"],
+    ap.add_argument("--halo", default="peer", choices=["copy", "peer"],
                     help="z-slab halo exchange: copy = edge kernels + NCCL send/recv (device copies in "
                          "loopback) overlapped with the interior kernel; peer = fused into the kernel, "
                          "which stores the neighbours' halo planes straight into their memory (CUDA IPC "
@@ -229,12 +231,31 @@ def main():
 
     slabs = args.slabs if world == 1 else 1
     halo = st.ST_HALO_PEER if args.halo == "peer" else st.ST_HALO_COPY
+    halo_note = None
     if slabs > 1:
         g = st.Grid(w.kind, w.nx, w.ny, w.nz, seed=synth.DEFAULT_SEED, variant=args.variant, bt=args.bt,
                     zchunk=args.zchunk, nranks=slabs, local_slabs=slabs, halo=halo)
     else:
         g = st.Grid(w.kind, w.nx, w.ny, w.nz, seed=synth.DEFAULT_SEED, variant=args.variant, bt=args.bt,
-                    zchunk=args.zchunk, rank=rank, nranks=world, nccl_id=nccl_id, halo=halo)
+                    zchunk=args.zchunk, rank=rank, nranks=world, nccl_id=nccl_id, halo=halo,
+                    wire_peers=False)
+        if world > 1 and halo == st.ST_HALO_PEER:
+            # wire the neighbours' memory (CUDA IPC); if any rank cannot, every rank falls back to the
+            # NCCL halo exchange together (a half-wired job would wait forever on a flag)
+            ok = 1
+            try:
+                descs = st.exchange_peer_descriptors(g.peer_export())
+                g.peer_import(*st.peer_neighbours(descs, rank))
+            except st.StencilError as e:
+                ok, halo_note = 0, f"peer wiring failed on rank {rank}: {e}"
+            flag = torch.tensor([ok], dtype=torch.int32, device=dev)
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+            if not int(flag.item()):
+                g.close()
+                halo, args.halo = st.ST_HALO_COPY, "copy"
+                halo_note = halo_note or "peer wiring failed on another rank"
+                g = st.Grid(w.kind, w.nx, w.ny, w.nz, seed=synth.DEFAULT_SEED, variant=args.variant,
+                            bt=args.bt, zchunk=args.zchunk, rank=rank, nranks=world, nccl_id=nccl_id)
     stream = g.stream
     for _ in range(args.warmup):
         g.run(w.T)
@@ -346,6 +367,8 @@ def main():
                                        if world > 1 else
                                        f"loopback z-slab x{slabs} on 1 GPU ({args.halo} halos)" if slabs > 1
                                        else "single GPU"),
+                       "halo": args.halo if (world > 1 or slabs > 1) else None,
+                       "halo_note": halo_note,
                        "l2": "inputs larger than L2 (no flush needed)",
                        "luops_per_step": w.nx * w.ny * w.nz * w.T},
             "roofline": roofline,

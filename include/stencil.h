@@ -93,9 +93,11 @@ enum {
                        (another slab of this handle, or the neighbour process's GPU memory mapped over
                        NVLink with CUDA IPC), then a stream-ordered flag write in the neighbour's
                        memory tells it the block's halos have landed (cuStreamWriteValue64 /
-                       cuStreamWaitValue64).  No edge/interior split, no copy, no NCCL on the data
-                       path.  Pipe variant only.  Across processes every rank must call
-                       stencil_peer_export / stencil_peer_import after creating and before running. */
+                       cuStreamWaitValue64).  No edge/interior split, no copy, no NCCL at all (no
+                       nccl_id needed).  Pipe variant only.  With one slab per handle every rank must
+                       call stencil_peer_export / stencil_peer_import after creating and before
+                       running (ranks may also be several handles of one process: their descriptors
+                       are then used without IPC). */
 };
 
 /* Device allocator: return a device pointer to >= bytes (256-byte aligned) or NULL. */

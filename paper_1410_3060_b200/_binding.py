@@ -300,7 +300,7 @@ class Grid:
 
     def __init__(self, kind, nx, ny, nz, *, seed=None, scalars=None, v0=None, u0=None, coeff=None,
                  variant=ST_VARIANT_AUTO, bt=0, zchunk=0, tile_cfg=0, rank=0, nranks=1, nccl_id=None,
-                 local_slabs=1, halo=ST_HALO_COPY,
+                 local_slabs=1, halo=ST_HALO_COPY, wire_peers=True,
                  device=None, stream=None, torch_memory=True, tuned=False):
         import torch
         if tuned and bt == 0:  # plan measured by tools/tune.py for this kind and shape, if any
@@ -315,7 +315,7 @@ class Grid:
         o.rank, o.nranks, o.local_slabs = rank, nranks, local_slabs
         o.halo = halo
         self._id = None
-        if nranks > 1 and local_slabs == 1:
+        if nranks > 1 and local_slabs == 1 and halo == ST_HALO_COPY:
             self._id = ctypes.create_string_buffer(bytes(nccl_id), 128)
             o.nccl_id = ctypes.cast(self._id, ctypes.c_void_p)
         if stream is None:
@@ -334,7 +334,8 @@ class Grid:
             self.h = stencil_create(kind, nx, ny, nz, coeff, v0, u0, o)
         self.rank, self.nranks, self.halo = rank, nranks, halo
         self._ipc = halo == ST_HALO_PEER and nranks > 1 and local_slabs == 1
-        if self._ipc:  # fused halo exchange across processes: wire the neighbours' memory (collective)
+        self._wired = wire_peers
+        if self._ipc and wire_peers:  # fused halo exchange across processes: wire the neighbours' memory
             descs = exchange_peer_descriptors(stencil_peer_export(self.h))
             stencil_peer_import(self.h, *peer_neighbours(descs, rank))
 
@@ -358,8 +359,14 @@ class Grid:
         out = np.empty((z1 - z0,) + self.padded_shape[1:], dtype=np.float64)
         return stencil_read_planes(self.h, level, z0, z1, out)
 
+    def peer_export(self) -> bytes:
+        return stencil_peer_export(self.h)
+
+    def peer_import(self, below, above):
+        stencil_peer_import(self.h, below, above)
+
     def write(self, level, arr):
-        if self._ipc:  # neighbours store into this rank's halos: write between two barriers
+        if self._ipc and self._wired:  # neighbours store into this rank's halos: write between two barriers
             import torch.distributed as dist
             self.sync()
             dist.barrier()

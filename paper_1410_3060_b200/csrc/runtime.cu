@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <atomic>
@@ -118,6 +119,9 @@ struct PeerDesc {
   uint64_t magic;
   int32_t rank, nranks, kind, nbuf, bt, pad;
   int64_t nx, ny, nz, pitch, plane, store_z0, zl;
+  int64_t pid;                  // exporting process: a descriptor from this process is used directly
+  uint64_t raw_buf[4], raw_flags;  // (the neighbour is another handle here, e.g. two ranks emulated
+  int32_t device, pad2;            //  on one GPU in one process; CUDA IPC cannot open own handles)
   cudaIpcMemHandle_t buf[4];
   cudaIpcMemHandle_t flags;
 };
@@ -183,6 +187,7 @@ struct stencil_ctx {
   uint64_t* flags = nullptr;     // this rank's halo-arrival counters: [0] from below, [1] from above
   struct Peer {
     bool on = false;
+    bool opened = false;  // pointers come from cudaIpcOpenMemHandle (closed at release)
     double* buf[4] = {nullptr, nullptr, nullptr, nullptr};  // raw state buffers (IPC-mapped)
     uint64_t* flags = nullptr;                              // the neighbour's counters
     int64_t store_z0 = 0;
@@ -235,7 +240,7 @@ void* dev_alloc(stencil_ctx* h, size_t bytes) {
 void release(stencil_ctx* h) {
   cudaStreamSynchronize(h->stream);
   for (auto& pr : h->peer) {
-    if (!h->ipc || !pr.on) continue;
+    if (!h->ipc || !pr.on || !pr.opened) continue;
     for (auto* b : pr.buf)
       if (b) cudaIpcCloseMemHandle(b);
     if (pr.flags) cudaIpcCloseMemHandle(pr.flags);
@@ -329,7 +334,8 @@ int create_common(stencil_ctx** out, int kind, int64_t nx, int64_t ny, int64_t n
     set_err("halo mode ST_HALO_PEER needs the pipe variant (got variant %d)", o.variant);
     return ST_E_INVAL;
   }
-  const bool use_nccl = o.nranks > 1 && local == 1;
+  const bool one_slab = o.nranks > 1 && local == 1;           // one slab per process
+  const bool use_nccl = one_slab && o.halo == ST_HALO_COPY;   // ST_HALO_PEER needs no communicator
   if (use_nccl && !o.nccl_id) { set_err("nranks > 1 with one slab per process needs nccl_id"); return ST_E_INVAL; }
 
   int ndev = 0;
@@ -355,7 +361,7 @@ int create_common(stencil_ctx** out, int kind, int64_t nx, int64_t ny, int64_t n
   h->zchunk_req = o.zchunk;
   h->tile_cfg = o.tile_cfg;
   h->halo = o.nranks > 1 ? o.halo : ST_HALO_COPY;
-  h->ipc = h->halo == ST_HALO_PEER && use_nccl;
+  h->ipc = h->halo == ST_HALO_PEER && one_slab;
   if (h->ipc) {  // IPC maps whole allocations: state buffers and flags come straight from cudaMalloc
     h->alloc = nullptr;
     h->free_fn = nullptr;
@@ -986,8 +992,14 @@ int stencil_peer_export(stencil_ctx* h, void* desc, size_t desc_bytes) {
   d.rank = h->rank; d.nranks = h->nranks; d.kind = h->kind; d.nbuf = h->nbuf; d.bt = h->bt;
   d.nx = h->nx; d.ny = h->ny; d.nz = h->nz; d.pitch = h->pitch; d.plane = h->plane;
   d.store_z0 = s.store_z0; d.zl = s.zl;
-  for (int b = 0; b < h->nbuf; ++b) CK(cudaIpcGetMemHandle(&d.buf[b], s.buf[b]), "cudaIpcGetMemHandle");
+  d.pid = (int64_t)getpid();
+  d.device = h->device;
+  for (int b = 0; b < h->nbuf; ++b) {
+    CK(cudaIpcGetMemHandle(&d.buf[b], s.buf[b]), "cudaIpcGetMemHandle");
+    d.raw_buf[b] = (uint64_t)(uintptr_t)s.buf[b];
+  }
   CK(cudaIpcGetMemHandle(&d.flags, h->flags), "cudaIpcGetMemHandle");
+  d.raw_flags = (uint64_t)(uintptr_t)h->flags;
   memset(desc, 0, ST_PEER_DESC_BYTES);
   memcpy(desc, &d, sizeof d);
   return ST_OK;
@@ -1017,14 +1029,26 @@ int stencil_peer_import(stencil_ctx* h, const void* below, const void* above) {
       return ST_E_INVAL;
     }
     auto& pr = h->peer[q];
-    for (int b = 0; b < h->nbuf; ++b) {
-      void* ptr = nullptr;
-      CK(cudaIpcOpenMemHandle(&ptr, d.buf[b], cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
-      pr.buf[b] = (double*)ptr;
+    if (d.pid == (int64_t)getpid()) {  // a handle of this process: its pointers are valid here
+      if (d.device != h->device) {
+        cudaError_t pe = cudaDeviceEnablePeerAccess(d.device, 0);
+        if (pe != cudaSuccess && pe != cudaErrorPeerAccessAlreadyEnabled) return cuda_fail(h, pe, "peer access");
+        cudaGetLastError();
+      }
+      for (int b = 0; b < h->nbuf; ++b) pr.buf[b] = (double*)(uintptr_t)d.raw_buf[b];
+      pr.flags = (uint64_t*)(uintptr_t)d.raw_flags;
+      pr.opened = false;
+    } else {
+      for (int b = 0; b < h->nbuf; ++b) {
+        void* ptr = nullptr;
+        CK(cudaIpcOpenMemHandle(&ptr, d.buf[b], cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+        pr.buf[b] = (double*)ptr;
+      }
+      void* fp = nullptr;
+      CK(cudaIpcOpenMemHandle(&fp, d.flags, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+      pr.flags = (uint64_t*)fp;
+      pr.opened = true;
     }
-    void* fp = nullptr;
-    CK(cudaIpcOpenMemHandle(&fp, d.flags, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
-    pr.flags = (uint64_t*)fp;
     pr.store_z0 = d.store_z0;
     pr.on = true;
   }

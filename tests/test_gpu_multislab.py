@@ -124,3 +124,60 @@ def test_peer_halo_needs_pipe_variant():
     with pytest.raises(st.StencilError):
         st.Grid(synth.K7V, 16, 16, 16, seed=1, nranks=2, local_slabs=2, halo=st.ST_HALO_PEER,
                 variant=st.ST_VARIANT_STREAM)
+
+
+@pytest.mark.parametrize("kind,n,T", [CASES[1], CASES[3], (synth.K7V, (40, 33, 37), (5, 4)),
+                                      (synth.K25W, (70, 20, 41), (3, 2))])
+@pytest.mark.parametrize("P", [2, 3])
+def test_peer_ranks_as_handles_in_one_process(kind, n, T, P):
+    """The one-slab-per-rank ST_HALO_PEER protocol (descriptor export/import, remote stores into the
+    neighbour's buffers, stream-ordered flag write / wait per block) with P ranks emulated as P handles
+    of this process on their own streams (descriptors from the same process are used without IPC).
+    The streams only wait on flags with cuStreamWaitValue64 -- no kernel spins -- and every rank's work
+    is enqueued before any stream can block.  Owned planes of all ranks == one slab, bitwise."""
+    import torch
+    ref = run(kind, n, T)
+    streams = [torch.cuda.Stream() for _ in range(P)]
+    gs = [st.Grid(kind, *n, seed=31, rank=r, nranks=P, halo=st.ST_HALO_PEER, wire_peers=False,
+                  stream=streams[r]) for r in range(P)]
+    try:
+        descs = [g.peer_export() for g in gs]
+        assert all(len(d) == st.ST_PEER_DESC_BYTES for d in descs)
+        for r, g in enumerate(gs):
+            g.peer_import(*st.peer_neighbours(descs, r))
+        for t in (T if isinstance(T, tuple) else (T,)):
+            for g in gs:
+                g.run(t)
+        new = np.zeros(gs[0].padded_shape)
+        old = np.zeros(gs[0].padded_shape)
+        for g in gs:
+            g.read(0, out=new)
+            if kind in WAVES:
+                g.read(1, out=old)
+        assert np.array_equal(new, ref[0])
+        if kind in WAVES:
+            assert np.array_equal(old, ref[1])
+        assert gs[0].info()["halo"] == st.ST_HALO_PEER
+    finally:
+        for g in gs:
+            g.close()
+
+
+def test_peer_import_validates():
+    a = st.Grid(synth.K7V, 16, 16, 16, seed=1, rank=0, nranks=2, halo=st.ST_HALO_PEER, wire_peers=False)
+    b = st.Grid(synth.K7V, 16, 16, 16, seed=1, rank=1, nranks=2, halo=st.ST_HALO_PEER, wire_peers=False)
+    try:
+        da, db = a.peer_export(), b.peer_export()
+        with pytest.raises(st.StencilError):
+            a.peer_import(None, None)       # rank 0 of 2 needs an `above`
+        with pytest.raises(st.StencilError):
+            a.peer_import(None, da)         # its own descriptor is not rank 1's
+        with pytest.raises(st.StencilError):
+            a.run(1)                        # not wired yet
+        a.peer_import(None, db)
+        b.peer_import(da, None)
+        with pytest.raises(st.StencilError):
+            b.peer_import(da, None)         # twice
+    finally:
+        a.close()
+        b.close()
