@@ -488,15 +488,6 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN,
             const long long o = (long long)c * p.plane + col[j];
             stg_row<CXN, VEC>(p.dst + o, vout, outc[j]);
             if constexpr (WAVE && BT >= 2) stg_row<CXN, VEC>(p.dstu + o, uout, outc[j]);
-            // fused halo exchange: planes that are a z-neighbour's halo planes are
-            // also stored straight into the neighbour's buffer (peer memory over NVLink, or another
-            // slab on this device), tile by tile as they are produced
-#pragma unroll
-            for (int q = 0; q < 2; ++q)
-              if (p.rdst[q] && c >= p.rz0[q] && c < p.rz1[q]) {
-                stg_row<CXN, VEC>(p.rdst[q] + o, vout, outc[j]);
-                if constexpr (WAVE && BT >= 2) stg_row<CXN, VEC>(p.rdstu[q] + o, uout, outc[j]);
-              }
           }
         }
         if (k == 1 && iv >= iv_b + R) {  // footprint plane of step iv - R fully consumed
@@ -535,6 +526,30 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN,
       for (uint32_t i = (iv >= iv_b + R ? iv - R : iv_b); i < iv; ++i) mbar_arrive(&emptyV[i % DV]);
       if (HAS_C)
         for (uint32_t i = (iv >= iv_b + CLAG ? iv - CLAG : iv_b); i < iv; ++i) mbar_arrive(&emptyC[i % DC]);
+    }
+    // Fused halo exchange (ST_HALO_PEER): the item's output planes that are a
+    // z-neighbour's halo planes go straight into the neighbour's buffer (peer memory over NVLink, or
+    // another slab on this device) as soon as the item is done -- each thread forwards the cells it
+    // stored itself (program order: its own stores are visible to its loads; they hit L2), so the hot
+    // z-loop above is the same code with or without the exchange.
+#pragma unroll 1
+    for (int q = 0; q < 2; ++q) {
+      if (!p.rdst[q]) continue;
+      const int c0 = max(it.zc0, p.rz0[q]), c1 = min(it.zc1, p.rz1[q]);
+#pragma unroll 1
+      for (int c = c0; c < c1; ++c) {
+        if ((p.dbg & 4) && c == it.zc1 - 1) continue;  // fault injection: a plane never written
+#pragma unroll
+        for (int j = 0; j < CY; ++j) {
+          const long long o = (long long)c * p.plane + col[j];
+#pragma unroll
+          for (int i = 0; i < CXN; ++i)
+            if (outc[j][i]) {
+              p.rdst[q][o + i] = __ldcg(p.dst + o + i);
+              if constexpr (WAVE && BT >= 2) p.rdstu[q][o + i] = __ldcg(p.dstu + o + i);
+            }
+        }
+      }
     }
   }
   // peer stores of another process's memory are ordered before the stream's completion signal

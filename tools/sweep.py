@@ -14,6 +14,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
 import paper_1410_3060_b200 as st  # noqa: E402
+from bench import ClockSampler  # noqa: E402
 import synth  # noqa: E402
 from synth import workloads  # noqa: E402
 
@@ -50,6 +51,8 @@ def main():
                     g.run(T)
                     g.sync()
                     ts = []
+                    clk = ClockSampler(torch.cuda.current_device())
+                    clk.__enter__()
                     for _ in range(a.reps):
                         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                         e0.record(s)
@@ -57,13 +60,16 @@ def main():
                         e1.record(s)
                         e1.synchronize()
                         ts.append(e0.elapsed_time(e1))
+                    clk.__exit__()
                     ms = statistics.median(ts)
+                    cs = clk.summary()
                     info = g.info()
                     g.close()
                     lups = w.nx * w.ny * w.nz * T
                     print(json.dumps({"workload": name, "variant": variant, "bt": info["bt"], "cfg": cfg,
                                       "zchunk": info["zchunk"], "tile": [info["tile_x"], info["tile_y"]],
-                                      "ms": round(ms, 3), "glups": round(lups / ms / 1e6, 2)}), flush=True)
+                                      "ms": round(ms, 3), "glups": round(lups / ms / 1e6, 2),
+                                      "sm_mhz": cs.get("sm_mhz"), "reasons": cs.get("reasons")}), flush=True)
                     torch.cuda.empty_cache()
 
 
