@@ -246,6 +246,7 @@ def main():
             try:
                 descs = st.exchange_peer_descriptors(g.peer_export())
                 g.peer_import(*st.peer_neighbours(descs, rank))
+                g.peer_handshake(timeout_ms=20000)  # peer stores + flag writes really arrive
             except st.StencilError as e:
                 ok, halo_note = 0, f"peer wiring failed on rank {rank}: {e}"
             flag = torch.tensor([ok], dtype=torch.int32, device=dev)

@@ -248,6 +248,15 @@ int stencil_plan_slab(int64_t nz, int R, int nranks, int rank, int bt, int64_t *
 int stencil_peer_export(stencil_ctx *h, void *desc, size_t desc_bytes);
 int stencil_peer_import(stencil_ctx *h, const void *below, const void *above);
 
+/*
+ * Optional check after stencil_peer_import (collective, before the first run): every rank stores a
+ * rank-tagged word into each neighbour's memory with a kernel (the fused halo stores' path) and
+ * with a stream-ordered flag write (the block signal's path), then polls its own memory from the
+ * host for the neighbours' words -- it never blocks the GPU.  ST_OK when both arrived, ST_E_STATE
+ * after timeout_ms (the caller can then fall back to ST_HALO_COPY on every rank).
+ */
+int stencil_peer_handshake(stencil_ctx *h, int timeout_ms);
+
 /* Library version string. */
 const char *stencil_version(void);
 

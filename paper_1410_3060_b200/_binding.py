@@ -30,6 +30,7 @@ EXPORTED_SYMBOLS = [
     "stencil_read", "stencil_read_planes", "stencil_write", "stencil_info", "stencil_set_timing",
     "stencil_kernel_time", "stencil_destroy", "stencil_last_error", "stencil_nccl_unique_id",
     "stencil_plan_slab", "stencil_version", "stencil_peer_export", "stencil_peer_import",
+    "stencil_peer_handshake",
 ]
 
 ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p)
@@ -101,6 +102,7 @@ def lib():
         "stencil_version": (ctypes.c_char_p, []),
         "stencil_peer_export": (I, [P, P, ctypes.c_size_t]),
         "stencil_peer_import": (I, [P, P, P]),
+        "stencil_peer_handshake": (I, [P, I]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -228,6 +230,10 @@ def stencil_peer_import(h, below: bytes | None, above: bytes | None):
     _check(lib().stencil_peer_import(h, b, a))
 
 
+def stencil_peer_handshake(h, timeout_ms=10000):
+    _check(lib().stencil_peer_handshake(h, timeout_ms))
+
+
 def peer_neighbours(descs, rank):
     """(below, above) descriptors of rank's z-neighbours from the all-gathered list (None at the ends)."""
     n = len(descs)
@@ -338,6 +344,7 @@ class Grid:
         if self._ipc and wire_peers:  # fused halo exchange across processes: wire the neighbours' memory
             descs = exchange_peer_descriptors(stencil_peer_export(self.h))
             stencil_peer_import(self.h, *peer_neighbours(descs, rank))
+            stencil_peer_handshake(self.h)
 
     @property
     def padded_shape(self):
@@ -364,6 +371,9 @@ class Grid:
 
     def peer_import(self, below, above):
         stencil_peer_import(self.h, below, above)
+
+    def peer_handshake(self, timeout_ms=10000):
+        stencil_peer_handshake(self.h, timeout_ms)
 
     def write(self, level, arr):
         if self._ipc and self._wired:  # neighbours store into this rank's halos: write between two barriers

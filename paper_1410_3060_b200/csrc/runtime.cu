@@ -712,6 +712,16 @@ int run_block(stencil_ctx* h, int b) {
   return rc;
 }
 
+// Handshake kernel: plain device stores into the neighbours' flag blocks (peer memory), the same path
+// the fused halo stores take.  Slot 2 / 3 of a flag block = word from the neighbour below / above.
+__global__ void peer_poke_kernel(uint64_t* below_flags, uint64_t* above_flags, uint64_t magic) {
+  if (below_flags) below_flags[3] = magic;  // I am the neighbour above of the rank below
+  if (above_flags) above_flags[2] = magic;
+  __threadfence_system();
+}
+
+uint64_t handshake_magic(int rank) { return 0x5EED000000000000ull + (uint64_t)rank; }
+
 // ST_HALO_PEER across processes: enqueue a wait until both neighbours have delivered every block run
 // so far (no remote store into this rank's memory is still in flight afterwards).
 int wait_peers(stencil_ctx* h) {
@@ -1002,6 +1012,49 @@ int stencil_peer_export(stencil_ctx* h, void* desc, size_t desc_bytes) {
   d.raw_flags = (uint64_t)(uintptr_t)h->flags;
   memset(desc, 0, ST_PEER_DESC_BYTES);
   memcpy(desc, &d, sizeof d);
+  return ST_OK;
+}
+
+int stencil_peer_handshake(stencil_ctx* h, int timeout_ms) {
+  int rc = check_handle(h);
+  if (rc) return rc;
+  if (!h->ipc || !h->peer_ready) { set_err("stencil_peer_handshake: import the neighbours first"); return ST_E_STATE; }
+  CK(cudaSetDevice(h->device), "cudaSetDevice");
+  const MemOps& m = memops();
+  if (!m.write) { set_err("stream memory operations unavailable"); return ST_E_CUDA; }
+  const uint64_t mine = handshake_magic(h->rank);
+  // data path: a kernel's stores into peer memory; signal path: a stream-ordered flag write
+  peer_poke_kernel<<<1, 1, 0, h->stream>>>(h->peer[0].on ? h->peer[0].flags : nullptr,
+                                          h->peer[1].on ? h->peer[1].flags : nullptr, mine);
+  CK(cudaGetLastError(), "handshake kernel");
+  for (int q = 0; q < 2; ++q)
+    if (h->peer[q].on) {
+      CUresult r = m.write((CUstream)h->stream, (CUdeviceptr)(h->peer[q].flags + 5 - q), (cuuint64_t)mine,
+                           CU_STREAM_WRITE_VALUE_DEFAULT);
+      if (r != CUDA_SUCCESS) { set_err("cuStreamWriteValue64 failed (%d)", (int)r); return ST_E_CUDA; }
+    }
+  CK(cudaStreamSynchronize(h->stream), "handshake");
+  // poll this rank's own flag block from the host (a private stream: nothing here can block forever)
+  cudaStream_t ps = nullptr;
+  CK(cudaStreamCreateWithFlags(&ps, cudaStreamNonBlocking), "handshake stream");
+  uint64_t got[6] = {0, 0, 0, 0, 0, 0};
+  bool ok = false;
+  for (int waited = 0;; waited += 1) {
+    cudaError_t e = cudaMemcpyAsync(got, h->flags, sizeof got, cudaMemcpyDeviceToHost, ps);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ps);
+    if (e != cudaSuccess) { cudaStreamDestroy(ps); return cuda_fail(h, e, "handshake poll"); }
+    ok = (!h->peer[0].on || (got[2] == handshake_magic(h->rank - 1) && got[4] == handshake_magic(h->rank - 1))) &&
+         (!h->peer[1].on || (got[3] == handshake_magic(h->rank + 1) && got[5] == handshake_magic(h->rank + 1)));
+    if (ok || waited >= timeout_ms) break;
+    usleep(1000);
+  }
+  cudaStreamDestroy(ps);
+  if (!ok) {
+    set_err("stencil_peer_handshake: neighbour stores did not arrive within %d ms (got %llx %llx %llx %llx)",
+            timeout_ms, (unsigned long long)got[2], (unsigned long long)got[3], (unsigned long long)got[4],
+            (unsigned long long)got[5]);
+    return ST_E_STATE;
+  }
   return ST_OK;
 }
 

@@ -145,6 +145,17 @@ def test_peer_ranks_as_handles_in_one_process(kind, n, T, P):
         assert all(len(d) == st.ST_PEER_DESC_BYTES for d in descs)
         for r, g in enumerate(gs):
             g.peer_import(*st.peer_neighbours(descs, r))
+        # handshake: rank 0 alone times out (its neighbour has not stored yet); once every rank has
+        # posted its words, every rank finds both neighbours' words
+        with pytest.raises(st.StencilError):
+            gs[0].peer_handshake(timeout_ms=20)
+        for g in gs[1:]:
+            try:
+                g.peer_handshake(timeout_ms=0)
+            except st.StencilError:
+                pass
+        for g in gs:
+            g.peer_handshake(timeout_ms=2000)
         for t in (T if isinstance(T, tuple) else (T,)):
             for g in gs:
                 g.run(t)
