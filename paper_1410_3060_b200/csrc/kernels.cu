@@ -218,33 +218,6 @@ cudaError_t launch_fill(double* base, long long pitch, long long plane, int zl, 
   return cudaGetLastError();
 }
 
-// Dense rows (X doubles each, nrows rows) -> the pitched device layout (row r at dst + r * pitch):
-// the second half of a staged host upload (one contiguous H2D copy at full PCIe speed, then this
-// on-device repack; a pitched cudaMemcpy2D from host runs at ~31 GB/s on B200 vs ~55 contiguous).
-__global__ void repack_kernel(const double* __restrict__ src, long long X, long long nrows,
-                              double* __restrict__ dst, long long pitch) {
-  const long long r = (long long)blockIdx.y * 4 + threadIdx.y;
-  if (r >= nrows) return;
-  const double* s = src + r * X;
-  double* d = dst + r * pitch;
-  for (long long x = (long long)blockIdx.x * blockDim.x + threadIdx.x; x < X; x += (long long)gridDim.x * blockDim.x)
-    d[x] = __ldcs(s + x);
-}
-
-cudaError_t launch_repack(const double* src, long long X, long long nrows, double* dst, long long pitch,
-                          cudaStream_t cs) {
-  if (nrows <= 0) return cudaSuccess;
-  long long gy = (nrows + 3) / 4;
-  // grid.y limit 65535: walk the rows in slices
-  for (long long r0 = 0; r0 < nrows; r0 += 4 * 65535LL) {
-    const long long n = std::min<long long>(nrows - r0, 4 * 65535LL);
-    gy = (n + 3) / 4;
-    dim3 block(128, 4), grid((unsigned)std::min<long long>((X + 127) / 128, 8), (unsigned)gy);
-    repack_kernel<<<grid, block, 0, cs>>>(src + r0 * X, X, n, dst + r0 * pitch, pitch);
-  }
-  return cudaGetLastError();
-}
-
 // ------------------------------------------------------------------------------------------------
 cudaError_t launch_naive(int kind, const KParams& p, cudaStream_t stream, LaunchInfo* info) {
   const int planes = p.zo1 - p.zo0;

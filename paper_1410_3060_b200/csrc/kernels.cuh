@@ -77,8 +77,4 @@ cudaError_t launch_fill(double* base, long long pitch, long long plane, int zl, 
                         long long GX, long long GY, long long GZ, int R, uint64_t seed, int stream,
                         int mode, double c, cudaStream_t cs);
 
-// Dense rows of X doubles (nrows of them, contiguous) -> pitched rows (dst + r * pitch).
-cudaError_t launch_repack(const double* src, long long X, long long nrows, double* dst, long long pitch,
-                          cudaStream_t cs);
-
 }  // namespace st

@@ -449,8 +449,10 @@ int create_common(stencil_ctx** out, int kind, int64_t nx, int64_t ny, int64_t n
 
 // Copy dense padded global host planes [store_z0, store_z1) of slab s into its device buffer raw.
 // Staged: chunks of planes go host -> a dense device staging buffer in one contiguous copy each, then
-// an on-device repack into the pitched layout (a pitched cudaMemcpy2D from host memory ran at ~31 GB/s
-// on B200, a contiguous copy at ~55).  Without a staging buffer (allocation failed) the 2-D copy is used.
+// a device-to-device pitched copy into the library layout (a pitched cudaMemcpy2D straight from host
+// memory ran at ~31 GB/s on B200, a contiguous copy at ~55 GB/s, the device-side 2-D copy at ~3.4 TB/s;
+// tools/pcie_probe.py).  Both copies run on copy engines, so an upload overlaps running kernels.
+// Without a staging buffer (allocation failed) the direct 2-D copy is used.
 constexpr int64_t kStagePlanes = 32;
 cudaError_t upload_planes(stencil_ctx* h, const Slab& s, double* raw, const double* host,
                           double* stage = nullptr) {
@@ -463,8 +465,9 @@ cudaError_t upload_planes(stencil_ctx* h, const Slab& s, double* raw, const doub
     const int64_t nz = std::min<int64_t>(kStagePlanes, s.zl - z0);
     cudaError_t e = cudaMemcpyAsync(stage, src + z0 * hplane, (size_t)(nz * hplane) * sizeof(double),
                                     cudaMemcpyHostToDevice, h->stream);
-    if (e == cudaSuccess)
-      e = st::launch_repack(stage, h->X, nz * h->Y, raw + h->xoff + z0 * h->plane, h->pitch, h->stream);
+    if (e == cudaSuccess)  // repack by the copy engine (~3.4 TB/s), so no SM is needed while kernels run
+      e = cudaMemcpy2DAsync(raw + h->xoff + z0 * h->plane, h->pitch * sizeof(double), stage, h->X * sizeof(double),
+                            h->X * sizeof(double), (size_t)(nz * h->Y), cudaMemcpyDeviceToDevice, h->stream);
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;

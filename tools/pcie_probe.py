@@ -1,4 +1,7 @@
-import torch, time
+import os
+import time
+
+import torch
 n = 514*514*514
 X=514; pitch=528
 h = torch.empty(n, dtype=torch.float64).pin_memory()
@@ -19,3 +22,14 @@ d2 = d.view(514*514, pitch)[:, :X]
 h2 = h.view(514*514, X)
 print("H2D 2D pitched GB/s", n*8/t(lambda: d2.copy_(h2, non_blocking=True))/1e9)
 print("D2H 2D pitched GB/s", n*8/t(lambda: h2.copy_(d2, non_blocking=True))/1e9)
+
+# device-to-device pitched copy through the copy engine (cudaMemcpy2DAsync), as the staged upload uses
+import ctypes
+rt = ctypes.CDLL("libcudart.so.12")
+dsrc = torch.empty(n, dtype=torch.float64, device="cuda")
+def d2d2():
+    rc = rt.cudaMemcpy2DAsync(ctypes.c_void_p(d.data_ptr()), ctypes.c_size_t(pitch * 8),
+                              ctypes.c_void_p(dsrc.data_ptr()), ctypes.c_size_t(X * 8), ctypes.c_size_t(X * 8),
+                              ctypes.c_size_t(514 * 514), ctypes.c_int(3), ctypes.c_void_p(s.cuda_stream))
+    assert rc == 0, rc
+print("D2D 2D pitched (copy engine) GB/s (read+write)", 2 * n * 8 / t(d2d2) / 1e9)
