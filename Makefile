@@ -11,7 +11,7 @@ CSRC      := paper_1410_3060_b200/csrc
 LIB       := paper_1410_3060_b200/libstencil.so
 OBJS      := build/kernels.o build/pipe.o build/runtime.o
 
-all: $(LIB) oracle/liboracle.so synth/libsynth.so
+all: $(LIB) oracle/liboracle.so synth/libsynth.so build/fp64_peak
 
 build:
 	mkdir -p build
@@ -27,6 +27,9 @@ build/runtime.o: $(CSRC)/runtime.cu $(CSRC)/kernels.cuh include/stencil.h | buil
 
 $(LIB): $(OBJS)
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -ldl
+
+build/fp64_peak: tools/fp64_peak.cu | build
+	$(NVCC) $(ARCH) -O3 -o $@ $<
 
 oracle/liboracle.so: oracle/oracle.c
 	gcc -O2 -ffp-contract=off -fno-fast-math -fopenmp -fPIC -shared -std=c11 -o $@ $<

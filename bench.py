@@ -105,6 +105,15 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
+def load_fp64_peak():
+    """Measured FP64 FMA throughput (tools/fp64_peak.cu -> profiles/fp64_peak.json), TFLOP/s."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "fp64_peak.json")))
+        return float(d["fp64_tflops"]), "measured (profiles/fp64_peak.json, tools/fp64_peak.cu)"
+    except Exception:
+        return 37.2, "nominal (64 FP64 FMA lanes per SM x 148 SMs x 1.965 GHz)"
+
+
 def pick_workload(name, n_gpus):
     w = workloads.BY_NAME.get(name) or {x.name.split("-")[0]: x
                                         for x in workloads.CONFIGS + workloads.EXTRA}.get(name)
@@ -302,13 +311,19 @@ def main():
     # per launch / average launch time when every launch is a full block; with z-slabs each block is
     # an edge + interior pair of launches)
     peak, peak_src = load_peaks()
+    fp64, fp64_src = load_fp64_peak()
     achieved = per_step_bytes * args.steps / (kern_ms / 1e3) / 1e9 if kern_ms else 0.0
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": load_traffic(w.name, bt), "peak_source": peak_src,
                 "bytes_per_cell_per_launch": block_bytes_per_cell(w.kind, bt), "bt": bt,
                 "avg_launch_ms": avg_launch_ms, "kernel_share_of_step": kern_ms / ms if ms else None,
                 "roof_glups_bt": peak / (block_bytes_per_cell(w.kind, bt) / bt),
-                "roof_glups_bt1": peak / block_bytes_per_cell(w.kind, 1)}
+                "roof_glups_bt1": peak / block_bytes_per_cell(w.kind, 1),
+                # BASELINE.json's second bound: FP64 peak / flops per LUP (the lower one is the roofline)
+                "fp64_tflops": fp64, "fp64_source": fp64_src, "flops_per_lup": FLOPS_PER_LUP[w.kind],
+                "roof_glups_fp64": fp64 * 1e3 / FLOPS_PER_LUP[w.kind],
+                "roof_glups": min(peak / (block_bytes_per_cell(w.kind, bt) / bt),
+                                  fp64 * 1e3 / FLOPS_PER_LUP[w.kind])}
 
     g.close()
     del g
