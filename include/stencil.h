@@ -77,9 +77,12 @@ enum {
   ST_VARIANT_STREAM = 2, /* 2.5-D z-streaming; with bt > 1 the time-skewed wavefront of
                             bt fused levels over overlapped xy tiles (P:569-602 transposed);
                             loads through registers, one CTA per tile and z-chunk */
-  ST_VARIANT_PIPE = 3    /* the same wavefront with TMA-fed shared-memory rings: a producer warp
+  ST_VARIANT_PIPE = 3,   /* the same wavefront with TMA-fed shared-memory rings: a producer warp
                             streams planes and coefficient fields ahead with cp.async.bulk.tensor +
                             mbarriers; persistent CTAs.  The default. */
+  ST_VARIANT_COOP = 4    /* small, latency-bound grids (their arrays fit in L2): all T steps of a
+                            stencil_run in ONE cooperative launch, a grid-wide barrier between
+                            sweeps.  Single slab only.  Auto-selected below a size threshold. */
 };
 
 /* Halo exchange between z-slabs. */

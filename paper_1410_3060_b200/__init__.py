@@ -10,7 +10,7 @@ can be tested), but creating a grid without a CUDA device raises StencilError.
 """
 from ._binding import (  # noqa: F401
     ST_7PT_CONST, ST_7PT_VAR, ST_25PT_WAVE, ST_25PT_VAR, ST_25PT_WAVE_A, WAVE_KINDS,
-    ST_VARIANT_AUTO, ST_VARIANT_NAIVE, ST_VARIANT_STREAM, ST_VARIANT_PIPE,
+    ST_VARIANT_AUTO, ST_VARIANT_NAIVE, ST_VARIANT_STREAM, ST_VARIANT_PIPE, ST_VARIANT_COOP,
     ST_OK, ST_E_INVAL, ST_E_NOMEM, ST_E_CUDA, ST_E_NCCL, ST_E_STATE,
     ST_HALO_COPY, ST_HALO_PEER, ST_PEER_DESC_BYTES,
     EXPORTED_SYMBOLS, LIB_PATH, StencilError, StOpts, StInfo,

@@ -16,7 +16,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("STENCIL_LIB") or os.path.join(_HERE, "libstencil.so")
 
 ST_7PT_CONST, ST_7PT_VAR, ST_25PT_WAVE, ST_25PT_VAR, ST_25PT_WAVE_A = 1, 2, 3, 4, 5
-ST_VARIANT_AUTO, ST_VARIANT_NAIVE, ST_VARIANT_STREAM, ST_VARIANT_PIPE = 0, 1, 2, 3
+ST_VARIANT_AUTO, ST_VARIANT_NAIVE, ST_VARIANT_STREAM, ST_VARIANT_PIPE, ST_VARIANT_COOP = 0, 1, 2, 3, 4
 ST_OK, ST_E_INVAL, ST_E_NOMEM, ST_E_CUDA, ST_E_NCCL, ST_E_STATE = 0, -1, -2, -3, -4, -5
 ST_HALO_COPY, ST_HALO_PEER = 0, 1
 ST_PEER_DESC_BYTES = 512

@@ -11,12 +11,17 @@
 //                 register rings of 2R+1 planes; x/y neighbours come from one shared-memory plane per
 //                 level (double-buffered, one __syncthreads per level per step) -- the GPU analog of
 //                 the layer condition: every V element is read from HBM once per block.
+//  coop_kernel    small grids (latency-bound, L2-resident): ALL T time steps in one cooperative launch,
+//                 a grid-wide barrier between sweeps (the naive sweep order of P:557-560 without a
+//                 kernel launch per step).
 //  fill_kernel    the seeded generator of synth/synth.h on the device.
 //
 // All kernels call the point functions of point.cuh, so their results are bitwise identical.
 #include "kernels.cuh"
 #include "point.cuh"
 #include "../../synth/synth.h"
+
+#include <cooperative_groups.h>
 
 #include <algorithm>
 
@@ -47,6 +52,90 @@ __global__ void __launch_bounds__(256) naive_kernel(const KParams p) {
   for (int k = 0; k < NC; ++k) W[k] = p.coef[k * p.cstride + i];
   const double u = Traits<KIND>::WAVE ? p.srcu[i] : 0.0;
   p.dst[i] = apply_point<KIND, R>(p.src[i], u, m, pl, W, p.s);
+}
+
+// ------------------------------------------------------------------------------------------------
+// coop: T sweeps in one cooperative launch.  Warps own rows (y, z) of the interior, lanes own x
+// (grid-stride); after a sweep every thread passes a grid-wide barrier and the roles of the two state
+// buffers swap -- for the Jacobi kinds dst is the other buffer, for the wave Omega^{t+1} overwrites
+// Omega^{t-1} in place (each cell reads its own U before writing it), so in both cases
+// (src, other) -> (other, src).  Bitwise equal to naive_kernel (same gathers, same point function).
+// 4 CTAs per SM for the 7-point kinds (more loads in flight per sweep), 2 for the 25-point kinds
+// (whose 25 gathers + 13 coefficients spill at 64 registers).
+template <int KIND>
+__global__ void __launch_bounds__(256, Traits<KIND>::R == 1 ? 4 : 2) coop_kernel(KParams p, int T) {
+  constexpr int R = Traits<KIND>::R, NC = Traits<KIND>::NCOEF;
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  const double* src = p.src;
+  double* oth = p.dst;  // == p.srcu for every kind (see run_coop)
+  const long long rows = (long long)p.ny * (p.zo1 - p.zo0);
+  const long long warps = (long long)gridDim.x * (blockDim.x / 32);
+  const long long w0 = (long long)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
+  for (int t = 0; t < T; ++t) {
+    for (long long row = w0; row < rows; row += warps) {
+      const int y = (int)(row % p.ny) + R, z = (int)(row / p.ny) + p.zo0;
+      const long long b = (long long)z * p.plane + (long long)y * p.pitch;
+      for (int x = lane + R; x < p.nx + R; x += 32) {
+        const long long i = b + x;
+        double m[3][R], pl[3][R];
+#pragma unroll
+        for (int r = 1; r <= R; ++r) {
+          m[0][r - 1] = src[i - r];
+          pl[0][r - 1] = src[i + r];
+          m[1][r - 1] = src[i - r * p.pitch];
+          pl[1][r - 1] = src[i + r * p.pitch];
+          m[2][r - 1] = src[i - r * p.plane];
+          pl[2][r - 1] = src[i + r * p.plane];
+        }
+        double W[NC > 0 ? NC : 1];
+#pragma unroll
+        for (int k = 0; k < NC; ++k) W[k] = p.coef[k * p.cstride + i];
+        const double u = Traits<KIND>::WAVE ? oth[i] : 0.0;
+        oth[i] = apply_point<KIND, R>(src[i], u, m, pl, W, p.s);
+      }
+    }
+    grid.sync();
+    double* tmp = const_cast<double*>(src);
+    src = oth;
+    oth = tmp;
+  }
+}
+
+// Largest cooperative grid of coop_kernel<KIND> on this device (0 if unsupported).
+template <int KIND>
+int coop_grid(int num_sms) {
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, coop_kernel<KIND>, 256, 0) != cudaSuccess) return 0;
+  return occ * num_sms;
+}
+
+template <int KIND>
+cudaError_t run_coop(const KParams& p0, int T, int num_sms, cudaStream_t stream, LaunchInfo* info) {
+  const int grid = coop_grid<KIND>(num_sms);  // every co-resident CTA: more loads in flight per sweep
+  if (grid <= 0) return cudaErrorCooperativeLaunchTooLarge;
+  KParams p = p0;
+  int Tv = T;
+  void* args[] = {(void*)&p, (void*)&Tv};
+  cudaError_t e = cudaLaunchCooperativeKernel((const void*)coop_kernel<KIND>, dim3(grid), dim3(256), args, 0, stream);
+  if (info) {
+    info->tile_x = 32; info->tile_y = 1; info->zchunk = 1; info->threads = 256; info->smem = 0;
+    info->ctas = grid;
+  }
+  return e;
+}
+
+cudaError_t launch_coop(int kind, const KParams& p, int T, int num_sms, cudaStream_t stream, LaunchInfo* info) {
+  if (p.zo1 <= p.zo0 || T <= 0) return cudaSuccess;
+  switch (kind) {
+    case K7C: return run_coop<K7C>(p, T, num_sms, stream, info);
+    case K7V: return run_coop<K7V>(p, T, num_sms, stream, info);
+    case K25W: return run_coop<K25W>(p, T, num_sms, stream, info);
+    case K25WA: return run_coop<K25WA>(p, T, num_sms, stream, info);
+    case K25V: return run_coop<K25V>(p, T, num_sms, stream, info);
+    default: return cudaErrorInvalidValue;
+  }
 }
 
 // ------------------------------------------------------------------------------------------------

@@ -69,6 +69,10 @@ cudaError_t launch_pipe(int kind, int b, const KParams& p, int zchunk_req, int n
                         cudaStream_t stream, LaunchInfo* info);
 int max_pipe_bt(int kind);
 
+// T time steps of the whole slab in ONE cooperative launch with a grid-wide barrier between sweeps
+// (ST_VARIANT_COOP, small latency-bound grids).  p.src = Omega^t, p.dst = p.srcu = the other buffer.
+cudaError_t launch_coop(int kind, const KParams& p, int T, int num_sms, cudaStream_t stream, LaunchInfo* info);
+
 // Seeded fill of the local planes of one array (synth/synth.h).  mode 0: U[-1,1) from `stream`
 // everywhere; mode 1: U[-1,1), interior cells from stream 1 and the rest from stream 0 (wave
 // Omega^{-1}); mode 2: U[0, c) from `stream`.  gz0 = global padded index of local plane 0;

@@ -268,6 +268,12 @@ int env_int(const char* name) {
   return v ? atoi(v) : 0;
 }
 
+// ST_VARIANT_AUTO picks the cooperative all-steps kernel when the handle's arrays (state levels +
+// coefficient fields) total at most this many bytes, i.e. stay L2-resident (126 MB): measured faster
+// than the pipe kernel for every kind up to 45 MB, slower from ~117 MB on (tools/coop_sweep.py,
+// DESIGN.md §6).
+constexpr double kCoopAutoBytes = 64.0 * 1024 * 1024;
+
 int default_bt(int kind) {
   switch (kind) {
     case ST_7PT_CONST: return 4;  // tools/sweep.py on B200
@@ -318,7 +324,7 @@ int create_common(stencil_ctx** out, int kind, int64_t nx, int64_t ny, int64_t n
   if (R < 0) { set_err("bad kind %d", kind); return ST_E_INVAL; }
   if (nx < 1 || ny < 1 || nz < 1) { set_err("extents must be >= 1 (got %lld %lld %lld)", (long long)nx, (long long)ny, (long long)nz); return ST_E_INVAL; }
   if (nx > (1 << 30) || ny > (1 << 30)) { set_err("extent too large"); return ST_E_INVAL; }
-  if (o.bt < 0 || o.variant < 0 || o.variant > ST_VARIANT_PIPE || o.zchunk < 0 || o.tile_cfg < 0) {
+  if (o.bt < 0 || o.variant < 0 || o.variant > ST_VARIANT_COOP || o.zchunk < 0 || o.tile_cfg < 0) {
     set_err("bad options (bt=%d variant=%d zchunk=%d tile_cfg=%d)", o.bt, o.variant, o.zchunk, o.tile_cfg);
     return ST_E_INVAL;
   }
@@ -330,6 +336,10 @@ int create_common(stencil_ctx** out, int kind, int64_t nx, int64_t ny, int64_t n
   }
   if (nz < o.nranks) { set_err("nz=%lld < nranks=%d", (long long)nz, o.nranks); return ST_E_INVAL; }
   if (o.halo != ST_HALO_COPY && o.halo != ST_HALO_PEER) { set_err("bad halo mode %d", o.halo); return ST_E_INVAL; }
+  if (o.variant == ST_VARIANT_COOP && o.nranks > 1) {
+    set_err("ST_VARIANT_COOP runs a single slab (nranks = 1)");
+    return ST_E_INVAL;
+  }
   if (o.halo == ST_HALO_PEER && o.variant != ST_VARIANT_AUTO && o.variant != ST_VARIANT_PIPE) {
     set_err("halo mode ST_HALO_PEER needs the pipe variant (got variant %d)", o.variant);
     return ST_E_INVAL;
@@ -370,7 +380,13 @@ int create_common(stencil_ctx** out, int kind, int64_t nx, int64_t ny, int64_t n
   CK(cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, dev), "device attribute");
 
   h->variant = o.variant == ST_VARIANT_AUTO ? ST_VARIANT_PIPE : o.variant;
-  int bt = h->variant == ST_VARIANT_NAIVE ? 1 : (o.bt ? o.bt : default_bt(kind));
+  if (o.variant == ST_VARIANT_AUTO && o.nranks == 1 && o.bt == 0 && o.zchunk == 0 && o.tile_cfg == 0) {
+    // small, latency-bound grids (L2-resident): one cooperative launch for all T steps
+    const double bytes = (2.0 + ncoef_of(kind)) * (double)(nx + 2 * R) * (double)(ny + 2 * R) *
+                         (double)(nz + 2 * R) * sizeof(double);
+    if (bytes <= kCoopAutoBytes) h->variant = ST_VARIANT_COOP;
+  }
+  int bt = (h->variant == ST_VARIANT_NAIVE || h->variant == ST_VARIANT_COOP) ? 1 : (o.bt ? o.bt : default_bt(kind));
   const int bt_cap = h->variant == ST_VARIANT_PIPE ? st::max_pipe_bt(kind)
                    : h->variant == ST_VARIANT_STREAM ? st::max_stream_bt(kind) : 1;
   bt = std::min(bt, std::max(1, bt_cap));
@@ -919,6 +935,24 @@ int stencil_run(stencil_ctx* h, int64_t T) {
   if (!g.ok) { set_err("handle used concurrently"); return ST_E_STATE; }
   const cudaError_t e = cudaSetDevice(h->device);
   if (e != cudaSuccess) return cuda_fail(h, e, "cudaSetDevice");
+  if (h->variant == ST_VARIANT_COOP) {  // all T steps in one cooperative launch
+    Slab& s = h->slabs.front();
+    st::KParams p = base_params(h, s);
+    p.src = h->at(s, h->lv0);
+    p.srcu = h->at(s, h->lv1);
+    p.dst = h->at(s, h->lv1);
+    cudaEvent_t ev_end = nullptr;
+    cudaEvent_t ev_begin = timing_begin(h, &ev_end);
+    const cudaError_t le = st::launch_coop(h->kind, p, (int)std::min<int64_t>(T, 1 << 30), h->num_sms, h->stream,
+                                           &h->last_launch);
+    if (ev_begin) cudaEventRecord(ev_end, h->stream);
+    if (le != cudaSuccess) return cuda_fail(h, le, "cooperative launch");
+    h->launches++;
+    if (T & 1) std::swap(h->lv0, h->lv1);
+    h->steps += T;
+    h->blocks += T;
+    return ST_OK;
+  }
   const int bt = h->variant == ST_VARIANT_NAIVE ? 1 : h->bt;
   int64_t left = T;
   while (left > 0 && rc == ST_OK) {
@@ -1020,7 +1054,7 @@ int stencil_write(stencil_ctx* h, int level, const double* in, int64_t in_elems)
 int stencil_info(const stencil_ctx* h, st_info* o) {
   if (!h || !o) { set_err("NULL handle or out"); return ST_E_INVAL; }
   memset(o, 0, sizeof *o);
-  o->kind = h->kind; o->R = h->R; o->bt = h->variant == ST_VARIANT_NAIVE ? 1 : h->bt;
+  o->kind = h->kind; o->R = h->R; o->bt = (h->variant == ST_VARIANT_NAIVE || h->variant == ST_VARIANT_COOP) ? 1 : h->bt;
   o->variant = h->variant; o->rank = h->rank; o->nranks = h->nranks; o->local_slabs = h->local;
   o->tile_x = h->last_launch.tile_x; o->tile_y = h->last_launch.tile_y; o->zchunk = h->last_launch.zchunk;
   o->nx = h->nx; o->ny = h->ny; o->nz = h->nz;

@@ -93,7 +93,8 @@ def test_shadow_scaled_per_cell(kind):  # needs non-negative weights: not the wa
 
 @pytest.mark.parametrize("kind", KINDS)
 def test_variants_bitwise_identical(kind):
-    """G4: naive == streaming == TMA-pipelined (every bt, tile configs, several z-chunks) bitwise."""
+    """G4: naive == streaming == TMA-pipelined (every bt, tile configs, several z-chunks) == cooperative
+    all-steps kernel, bitwise."""
     nx, ny, nz = SHAPES[kind]
     T = 7
     ref = gpu_run(kind, nx, ny, nz, T, seed=9, variant=st.ST_VARIANT_NAIVE)
@@ -101,6 +102,7 @@ def test_variants_bitwise_identical(kind):
              for zc in (0, 5, 1000)]
     plans += [(st.ST_VARIANT_PIPE, bt, zc, cfg) for bt in range(1, max_bt(kind) + 1) for zc in (0, 5, 1000)
               for cfg in range(N_CFG[kind])]
+    plans += [(st.ST_VARIANT_COOP, 1, 0, 0)]  # all T steps in one cooperative launch
     for variant, bt, zchunk, cfg in plans:
         got = gpu_run(kind, nx, ny, nz, T, seed=9, variant=variant, bt=bt, zchunk=zchunk, tile_cfg=cfg)
         assert got[2]["bt"] == bt
@@ -120,7 +122,8 @@ def test_degenerate_extents(kind):
         T = 5
         o_new, o_old = oracle.run(inp, T)
         for variant, bt in sorted({(st.ST_VARIANT_PIPE, 1), (st.ST_VARIANT_PIPE, max_bt(kind)),
-                                   (st.ST_VARIANT_STREAM, max_bt(kind, st.ST_VARIANT_STREAM))}):
+                                   (st.ST_VARIANT_STREAM, max_bt(kind, st.ST_VARIANT_STREAM)),
+                                   (st.ST_VARIANT_COOP, 1)}):
             g_new, g_old, _ = gpu_run(kind, nx, ny, nz, T, seed=4, bt=bt, variant=variant)
             assert_parity(kind, g_new, g_old, o_new, o_old, inp.R, 1e-13, inputs=inp)
 
