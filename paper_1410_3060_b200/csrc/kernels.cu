@@ -60,41 +60,63 @@ __global__ void __launch_bounds__(256) naive_kernel(const KParams p) {
 // buffers swap -- for the Jacobi kinds dst is the other buffer, for the wave Omega^{t+1} overwrites
 // Omega^{t-1} in place (each cell reads its own U before writing it), so in both cases
 // (src, other) -> (other, src).  Bitwise equal to naive_kernel (same gathers, same point function).
-// 4 CTAs per SM for the 7-point kinds (more loads in flight per sweep), 2 for the 25-point kinds
-// (whose 25 gathers + 13 coefficients spill at 64 registers).
+// 7-point kinds: one CTA per SM (1024 threads for 7c, 512 for 7v), two cells per lane whose operands are all loaded before
+// either is computed (the L2 round trips overlap); 25-point kinds: two 256-thread CTAs per SM, one
+// cell per lane (their 25 gathers + 13 coefficients need ~120 registers).  tools/coop_sweep.py.
 template <int KIND>
-__global__ void __launch_bounds__(256, Traits<KIND>::R == 1 ? 4 : 2) coop_kernel(KParams p, int T) {
-  constexpr int R = Traits<KIND>::R, NC = Traits<KIND>::NCOEF;
+struct CoopCfg {
+  static constexpr int THREADS = KIND == K7C ? 1024 : KIND == K7V ? 512 : 256;  // 7v: 14 gathers + 14 coefs
+  static constexpr int MINB = Traits<KIND>::R == 1 ? 1 : 2;
+  static constexpr int CB = Traits<KIND>::R == 1 ? 2 : 1;
+};
+
+template <int KIND>
+__global__ void __launch_bounds__(CoopCfg<KIND>::THREADS, CoopCfg<KIND>::MINB) coop_kernel(KParams p, int T) {
+  constexpr int R = Traits<KIND>::R, NC = Traits<KIND>::NCOEF, CB = CoopCfg<KIND>::CB;
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
   const double* src = p.src;
   double* oth = p.dst;  // == p.srcu for every kind (see run_coop)
-  const long long rows = (long long)p.ny * (p.zo1 - p.zo0);
+  const int nxc = (p.nx + 32 * CB - 1) / (32 * CB);  // x-chunks of 32*CB cells per row
+  const long long units = (long long)p.ny * (p.zo1 - p.zo0) * nxc;
   const long long warps = (long long)gridDim.x * (blockDim.x / 32);
   const long long w0 = (long long)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
   const int lane = threadIdx.x & 31;
   for (int t = 0; t < T; ++t) {
-    for (long long row = w0; row < rows; row += warps) {
+    for (long long u = w0; u < units; u += warps) {
+      const long long row = u / nxc;
+      const int xc = (int)(u - row * nxc);
       const int y = (int)(row % p.ny) + R, z = (int)(row / p.ny) + p.zo0;
       const long long b = (long long)z * p.plane + (long long)y * p.pitch;
-      for (int x = lane + R; x < p.nx + R; x += 32) {
-        const long long i = b + x;
-        double m[3][R], pl[3][R];
+      long long idx[CB];
+      bool ok[CB];
+      double c[CB], uo[CB], m[CB][3][R], pl[CB][3][R], W[CB][NC > 0 ? NC : 1];
+#pragma unroll
+      for (int q = 0; q < CB; ++q) {
+        const int x = R + xc * 32 * CB + q * 32 + lane;
+        ok[q] = x < p.nx + R;
+        idx[q] = b + (ok[q] ? x : R);  // out-of-range lanes gather a valid cell and store nothing
+      }
+#pragma unroll
+      for (int q = 0; q < CB; ++q) {
+        const long long i = idx[q];
 #pragma unroll
         for (int r = 1; r <= R; ++r) {
-          m[0][r - 1] = src[i - r];
-          pl[0][r - 1] = src[i + r];
-          m[1][r - 1] = src[i - r * p.pitch];
-          pl[1][r - 1] = src[i + r * p.pitch];
-          m[2][r - 1] = src[i - r * p.plane];
-          pl[2][r - 1] = src[i + r * p.plane];
+          m[q][0][r - 1] = src[i - r];
+          pl[q][0][r - 1] = src[i + r];
+          m[q][1][r - 1] = src[i - r * p.pitch];
+          pl[q][1][r - 1] = src[i + r * p.pitch];
+          m[q][2][r - 1] = src[i - r * p.plane];
+          pl[q][2][r - 1] = src[i + r * p.plane];
         }
-        double W[NC > 0 ? NC : 1];
 #pragma unroll
-        for (int k = 0; k < NC; ++k) W[k] = p.coef[k * p.cstride + i];
-        const double u = Traits<KIND>::WAVE ? oth[i] : 0.0;
-        oth[i] = apply_point<KIND, R>(src[i], u, m, pl, W, p.s);
+        for (int k = 0; k < NC; ++k) W[q][k] = p.coef[k * p.cstride + i];
+        c[q] = src[i];
+        uo[q] = Traits<KIND>::WAVE ? oth[i] : 0.0;
       }
+#pragma unroll
+      for (int q = 0; q < CB; ++q)
+        if (ok[q]) oth[idx[q]] = apply_point<KIND, R>(c[q], uo[q], m[q], pl[q], W[q], p.s);
     }
     grid.sync();
     double* tmp = const_cast<double*>(src);
@@ -107,8 +129,9 @@ __global__ void __launch_bounds__(256, Traits<KIND>::R == 1 ? 4 : 2) coop_kernel
 template <int KIND>
 int coop_grid(int num_sms) {
   int occ = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, coop_kernel<KIND>, 256, 0) != cudaSuccess) return 0;
-  return occ * num_sms;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, coop_kernel<KIND>, CoopCfg<KIND>::THREADS, 0) != cudaSuccess)
+    return 0;
+  return std::min(occ, CoopCfg<KIND>::MINB) * num_sms;
 }
 
 template <int KIND>
@@ -118,9 +141,11 @@ cudaError_t run_coop(const KParams& p0, int T, int num_sms, cudaStream_t stream,
   KParams p = p0;
   int Tv = T;
   void* args[] = {(void*)&p, (void*)&Tv};
-  cudaError_t e = cudaLaunchCooperativeKernel((const void*)coop_kernel<KIND>, dim3(grid), dim3(256), args, 0, stream);
+  cudaError_t e = cudaLaunchCooperativeKernel((const void*)coop_kernel<KIND>, dim3(grid),
+                                              dim3(CoopCfg<KIND>::THREADS), args, 0, stream);
   if (info) {
-    info->tile_x = 32; info->tile_y = 1; info->zchunk = 1; info->threads = 256; info->smem = 0;
+    info->tile_x = 32 * CoopCfg<KIND>::CB; info->tile_y = 1; info->zchunk = 1;
+    info->threads = CoopCfg<KIND>::THREADS; info->smem = 0;
     info->ctas = grid;
   }
   return e;

@@ -268,11 +268,10 @@ int env_int(const char* name) {
   return v ? atoi(v) : 0;
 }
 
-// ST_VARIANT_AUTO picks the cooperative all-steps kernel when the handle's arrays (state levels +
-// coefficient fields) total at most this many bytes, i.e. stay L2-resident (126 MB): measured faster
-// than the pipe kernel for every kind up to 45 MB, slower from ~117 MB on (tools/coop_sweep.py,
-// DESIGN.md §6).
-constexpr double kCoopAutoBytes = 64.0 * 1024 * 1024;
+// ST_VARIANT_AUTO picks the cooperative all-steps kernel for grids of at most this many padded cells
+// (tools/coop_sweep.py on B200, T = 10: faster than the pipe kernel for every kind at 66^3-72^3, for
+// 7c at 130^3 (214 vs 135 GLUP/s), 25w / 25v at 104^3; even with 7v at 130^3; slower for 7c at 194^3).
+constexpr double kCoopAutoCells = 3.0e6;
 
 int default_bt(int kind) {
   switch (kind) {
@@ -381,10 +380,9 @@ int create_common(stencil_ctx** out, int kind, int64_t nx, int64_t ny, int64_t n
 
   h->variant = o.variant == ST_VARIANT_AUTO ? ST_VARIANT_PIPE : o.variant;
   if (o.variant == ST_VARIANT_AUTO && o.nranks == 1 && o.bt == 0 && o.zchunk == 0 && o.tile_cfg == 0) {
-    // small, latency-bound grids (L2-resident): one cooperative launch for all T steps
-    const double bytes = (2.0 + ncoef_of(kind)) * (double)(nx + 2 * R) * (double)(ny + 2 * R) *
-                         (double)(nz + 2 * R) * sizeof(double);
-    if (bytes <= kCoopAutoBytes) h->variant = ST_VARIANT_COOP;
+    // small, latency-bound grids: one cooperative launch for all T steps
+    const double cells = (double)(nx + 2 * R) * (double)(ny + 2 * R) * (double)(nz + 2 * R);
+    if (cells <= kCoopAutoCells) h->variant = ST_VARIANT_COOP;
   }
   int bt = (h->variant == ST_VARIANT_NAIVE || h->variant == ST_VARIANT_COOP) ? 1 : (o.bt ? o.bt : default_bt(kind));
   const int bt_cap = h->variant == ST_VARIANT_PIPE ? st::max_pipe_bt(kind)

@@ -5,7 +5,7 @@ import paper_1410_3060_b200 as st
 import synth
 torch.cuda.set_device(0)
 s = torch.cuda.current_stream()
-for kind, n, T in [(1, 64, 10), (1, 96, 10), (1, 128, 10), (1, 192, 10), (2, 64, 10), (2, 128, 10), (3, 64, 10), (3, 96, 10), (4, 64, 10), (4, 96, 10), (2, 64, 100)]:
+for kind, n, T in [(1, 8, 1), (1, 8, 10), (1, 8, 50), (1, 64, 10), (1, 96, 10), (1, 128, 10), (1, 192, 10), (2, 64, 10), (2, 128, 10), (3, 64, 10), (3, 96, 10), (4, 64, 10), (4, 96, 10), (2, 64, 100)]:
     for variant, bt in [(4, 1), (3, 0)]:
         g = st.Grid(kind, n, n, n, seed=1, variant=variant, bt=bt)
         g.run(T); g.sync()
