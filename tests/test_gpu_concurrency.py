@@ -1,8 +1,7 @@
 """Distinct handles may be used concurrently (include/stencil.h conventions): grids created
 from host arrays in worker threads on their own streams while other grids run -- the pattern of
-bench.py's pipelined end-to-end measurement -- give bitwise the results of the sequential runs, and a
-handle is never shared between the threads here (one handle, one thread; see test_abi_cpu for the
-non-reentrancy guard)."""
+bench.py's pipelined end-to-end measurement -- give bitwise the results of the sequential runs.  (One handle is never used by two
+threads at once here: a handle is not reentrant; the library refuses that with ST_E_STATE.)"""
 import threading
 from concurrent.futures import ThreadPoolExecutor
 
