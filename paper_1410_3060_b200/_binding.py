@@ -260,7 +260,7 @@ def stencil_plan_slab(nz, R, nranks, rank, bt):
 
 
 def tuned_plan(kind, nx, ny, nz):
-    """(bt, tile_cfg, zchunk) that tools/tune.py measured fastest for this kind and shape, or None."""
+    """{variant, bt, tile_cfg, zchunk} that tools/tune.py measured fastest for this kind and shape, or None."""
     import json
     path = os.path.join(_HERE, "tuned.json")
     try:
@@ -313,6 +313,7 @@ class Grid:
             plan = tuned_plan(kind, nx, ny, nz)
             if plan:
                 bt, tile_cfg, zchunk = plan["bt"], plan["tile_cfg"], plan["zchunk"]
+                variant = plan.get("variant", variant)
         self.kind, self.nx, self.ny, self.nz = kind, nx, ny, nz
         self.R = RADIUS[kind]
         o = stencil_opts_default()

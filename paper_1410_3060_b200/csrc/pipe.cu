@@ -620,8 +620,10 @@ cudaError_t run_pipe(const KParams& p0, int zchunk_req, int num_sms, cudaStream_
     const long long slots = (long long)std::max(1, occ0) * num_sms;
     const int min_chunk = 24 * BT * C::R;  // keeps the 2*BT*R fill/drain planes of a chunk < ~8 %
     if (tiles * ((planes + min_chunk - 1) / min_chunk) >= 2 * slots) {
-      // large grid: ~8 work items per CTA for load balance, chunks >= min_chunk planes
-      const long long chunks = std::max<long long>(1, (8 * slots + tiles - 1) / tiles);
+      // large grid: ~4 work items per CTA for load balance (dynamic distribution), chunks >= min_chunk
+      // planes (tools/tune.py, session 2: 4 items beat 8 for the 25-point kinds -- each chunk re-reads
+      // its 2*BT*R halo planes -- and tie for the 7-point kinds)
+      const long long chunks = std::max<long long>(1, (4 * slots + tiles - 1) / tiles);
       zchunk = std::max((int)((planes + chunks - 1) / chunks), std::min(planes, min_chunk));
     } else {
       // small grid (latency-bound): about one work item per CTA slot
@@ -719,9 +721,9 @@ cudaError_t launch_pipe(int kind, int b, const KParams& p, int zchunk_req, int n
         if (cfg == 3) CFG(K25W, 1, 64, 16, 1, 4, 7, 3, 0, 1);
         if (cfg == 4) CFG(K25W, 1, 64, 14, 2, 2, 7, 3, 0, 1);  // round-1 default (rings shifted)
         if (cfg == 5) CFG(K25W, 1, 64, 14, 2, 2, 10, 6, 0, 1);
-        if (cfg == 6) CFGU(K25W, 1, 64, 14, 2, 2, 8, 4, 0, 1);
+        if (cfg == 6) CFGU(K25W, 1, 64, 14, 2, 2, 10, 6, 0, 1);
         if (cfg == 7) CFGU(K25W, 1, 64, 20, 2, 2, 8, 4, 0, 1);
-        CFGU(K25W, 1, 64, 14, 2, 2, 10, 6, 0, 1);              // C3: 165-169 -> 186-194 GLUP/s
+        CFGU(K25W, 1, 64, 14, 2, 2, 8, 4, 0, 1);               // C3: 165-169 -> 185-195 GLUP/s
       }
       break;
     case K25WA:
