@@ -341,7 +341,13 @@ def main():
         out = pin(np.empty_like(inp.V))
         del inp
         h2d = V.nbytes + (U.nbytes if U is not None else 0) + sum(c.nbytes for c in coeff if hasattr(c, "nbytes"))
-        d2h = out.nbytes if world == 1 else out.nbytes // world
+        d2h = out.nbytes
+        if world > 1:  # every rank uploads only the planes it stores and reads back the planes it owns
+            R = synth.RADIUS[w.kind]
+            pl = st.stencil_plan_slab(w.nz, R, world, rank, info["bt"])
+            planes = w.nz + 2 * R
+            h2d = h2d * (pl["store_z1"] - pl["store_z0"]) // planes
+            d2h = d2h * (pl["own_z1"] - pl["own_z0"]) // planes
 
         def make_grid(stream=None):
             return st.Grid(w.kind, w.nx, w.ny, w.nz, v0=V, u0=U, coeff=coeff, variant=args.variant,
