@@ -83,6 +83,33 @@ struct Item {
   int gx0, gy0, zc0, zc1, s_begin, s_end;
 };
 
+// Tensor memory (TMEM) as a per-thread coefficient window (WIN = -1 configurations): a warp may
+// access only the 32 TMEM lanes of its quadrant (warp % 4); thread i of the warp owns lane 32*q + i.
+// One row of a thread's cell block (NC coefficients x CX cells, <= 16 doubles) occupies 32 columns.
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&w)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+      "%14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};" ::"r"(taddr),
+      "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7]), "r"(w[8]), "r"(w[9]),
+      "r"(w[10]), "r"(w[11]), "r"(w[12]), "r"(w[13]), "r"(w[14]), "r"(w[15]), "r"(w[16]), "r"(w[17]), "r"(w[18]),
+      "r"(w[19]), "r"(w[20]), "r"(w[21]), "r"(w[22]), "r"(w[23]), "r"(w[24]), "r"(w[25]), "r"(w[26]), "r"(w[27]),
+      "r"(w[28]), "r"(w[29]), "r"(w[30]), "r"(w[31])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&w)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+      : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7]), "=r"(w[8]),
+        "=r"(w[9]), "=r"(w[10]), "=r"(w[11]), "=r"(w[12]), "=r"(w[13]), "=r"(w[14]), "=r"(w[15]), "=r"(w[16]),
+        "=r"(w[17]), "=r"(w[18]), "=r"(w[19]), "=r"(w[20]), "=r"(w[21]), "=r"(w[22]), "=r"(w[23]), "=r"(w[24]),
+        "=r"(w[25]), "=r"(w[26]), "=r"(w[27]), "=r"(w[28]), "=r"(w[29]), "=r"(w[30]), "=r"(w[31])
+      : "r"(taddr)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
 // Tiles write OXW = OX & ~3 output columns each (a multiple of the 4-double, 32-byte sector), starting
 // at raw column 16 (interior column R, 128-byte aligned in the device layout) + tx * OXW: every output
 // row segment covers whole sectors, so no sector is written partially by two tiles (partial-sector
@@ -209,10 +236,22 @@ struct PipeCfg {
   // Coefficients: levels 1..BT-WIN read them from the C ring in shared memory, which therefore keeps
   // each plane for CLAG = (BT-1-WIN)*R steps after its level-1 use; the last WIN levels read them from
   // a per-thread register window of L = WIN*R planes, filled from the ring when a plane leaves it.
-  static constexpr int CLAG = WAVE ? 0 : (BT - 1 - WIN) * R;
-  static constexpr int L = WIN * R;  // register-window planes
-  static_assert(WIN >= 0 && WIN <= BT - 1, "WIN in [0, BT-1]");
-  static_assert(!WIN || NC > 0, "register window only for variable kinds");
+  // WIN = -1: levels 2..BT read them from a per-thread window in TENSOR MEMORY instead (TW): level 1
+  // copies the coefficients it read from the ring into TMEM slot (step mod NSL), level k reads the slot
+  // written (k-1)*R steps earlier -- the ring frees each plane right after level 1 (CLAG = 0) and the
+  // shared-memory load traffic of levels >= 2 moves to the TMEM datapath.
+  static constexpr bool TW = WIN < 0;
+  static constexpr int WINR = TW ? 0 : WIN;
+  static constexpr int CLAG = (WAVE || TW) ? 0 : (BT - 1 - WIN) * R;
+  static constexpr int L = WINR * R;  // register-window planes
+  static_assert(WIN >= -1 && WIN <= BT - 1, "WIN in [-1, BT-1]");
+  static_assert(!WIN || NC > 0, "coefficient windows only for variable kinds");
+  static_assert(!TW || (!WAVE && BT >= 2 && 2 * NC * CX <= 32), "TMEM window: variable Jacobi kinds, bt >= 2");
+  static constexpr int NSL = (BT - 1) * R + 1;                 // TMEM window slots (planes)
+  static constexpr int TSLOT = CY * 32;                         // columns per slot (32 per cell row)
+  static constexpr int WPQ = (NCONS / 32 + 3) / 4;              // consumer warps per TMEM lane quadrant
+  static constexpr int TCOLS = NSL * TSLOT;                     // columns per warp
+  static_assert(!TW || WPQ * TCOLS <= 512, "TMEM window exceeds 512 columns");
   static_assert(!HAS_C || DC >= CLAG + 2, "C ring too shallow");
   static_assert((EXB * 8) % 16 == 0 && (FXB * 8) % 16 == 0, "TMA box rows must be 16-byte multiples");
   static_assert(FXB <= 256 && FY <= 256 && EXB <= 256, "TMA box dimension limit");
@@ -251,7 +290,17 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN,
     for (int i = 0; i < 4; ++i) { mbar_init(&itemFull[i], 1); mbar_init(&itemEmpty[i], NCONS / 32); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  __shared__ uint32_t tmem_base;
+  if constexpr (C::TW) {
+    if (tid < 32) {  // consumer warp 0 allocates all 512 columns (one CTA per SM)
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_base))
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  }
   __syncthreads();
+  if constexpr (C::TW) asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 
   if (tid >= NCONS) {
     // ---------------------------------------------------------------- producer warp
@@ -309,6 +358,9 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN,
   const int ly0 = (tid / LPR) * CY;  // first row
   const int lane = tid & 31;
   uint32_t iv = 0;
+  // this warp's TMEM window: lanes of quadrant warp % 4, columns [(warp / 4) * TCOLS, + TCOLS)
+  const uint32_t tbase = C::TW ? tmem_base + ((uint32_t)(((tid >> 5) & 3) * 32) << 16) + (uint32_t)((tid >> 7) * C::TCOLS)
+                               : 0u;
 
   for (uint32_t n = 0;; ++n) {
     const uint32_t qs = n & 3;
@@ -434,10 +486,32 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN,
           for (int i = 0; i < CXN; ++i) xr[RP + i] = ys[R + j][i];
           double Wrow[NC > 0 ? NC : 1][CXN];
           if constexpr (NC > 0) {
-            if (!(WIN && k > BT - WIN)) {
+            if (C::TW && k >= 2) {
+              // level k: the coefficients of plane s - k*R, stored by level 1 (k-1)*R steps ago
+              uint32_t w[32];
+              tmem_ld32(tbase + (uint32_t)(((iv - (uint32_t)((k - 1) * R)) % C::NSL) * C::TSLOT + j * 32), w);
+              tmem_wait_ld();
+#pragma unroll
+              for (int f = 0; f < NC; ++f)
+#pragma unroll
+                for (int i = 0; i < CXN; ++i) Wrow[f][i] = __hiloint2double(w[2 * (f * CXN + i) + 1], w[2 * (f * CXN + i)]);
+            } else if (!(C::WINR && k > BT - C::WINR)) {
 #pragma unroll
               for (int f = 0; f < NC; ++f)
                 lds_row<CXN, VEC>(Ck + C::CF0 + f * C::CFIELD + ly * EXB + x0, Wrow[f]);
+              if (C::TW && k == 1) {  // keep them for levels 2..BT
+                uint32_t w[32];
+#pragma unroll
+                for (int q = 0; q < 32; ++q) w[q] = 0u;
+#pragma unroll
+                for (int f = 0; f < NC; ++f)
+#pragma unroll
+                  for (int i = 0; i < CXN; ++i) {
+                    w[2 * (f * CXN + i)] = (uint32_t)__double2loint(Wrow[f][i]);
+                    w[2 * (f * CXN + i) + 1] = (uint32_t)__double2hiint(Wrow[f][i]);
+                  }
+                tmem_st32(tbase + (uint32_t)((iv % C::NSL) * C::TSLOT + j * 32), w);
+              }
             }
           }
           double urow[CXN];
@@ -461,7 +535,7 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN,
             if constexpr (NC > 0) {
 #pragma unroll
               for (int f = 0; f < NC; ++f)
-                W[f] = (WIN && k > BT - WIN) ? cwin[L > 0 ? (BT - k) * R : 0][j][i][f] : Wrow[f][i];
+                W[f] = (C::WINR && k > BT - C::WINR) ? cwin[L > 0 ? (BT - k) * R : 0][j][i][f] : Wrow[f][i];
             }
             double uo = 0.0;
             if constexpr (WAVE) uo = (k == 1) ? urow[i] : ring[k >= 2 ? k - 2 : 0][j][i][ri(0)];
@@ -495,6 +569,7 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN,
           if (lane == 0) mbar_arrive(&emptyV[(iv - R) % DV]);
         }
       }
+      if constexpr (C::TW) tmem_wait_st();  // this step's TMEM stores complete before later steps read them
       if constexpr (L > 0) {  // slide the window: drop plane s - BT*R, append plane s - (BT-WIN)*R
         // (before the item's first CLAG steps the window entry is never used; read a waited slot)
         const double* C1 = sC + (size_t)((iv >= iv_b + CLAG ? iv - CLAG : iv) % DC) * C::CSLOT + SHC;
@@ -554,6 +629,12 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN,
   }
   // peer stores of another process's memory are ordered before the stream's completion signal
   if (p.rfence) __threadfence_system();
+  if constexpr (C::TW) {  // all consumers are done with TMEM; warp 0 frees it
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    named_sync(1, NCONS);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (tid < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base) : "memory");
+  }
 }
 
 // ------------------------------------------------------------------------------------------------ host
@@ -662,7 +743,7 @@ cudaError_t run_pipe(const KParams& p0, int zchunk_req, int num_sms, cudaStream_
 int max_pipe_bt(int kind) {
   switch (kind) {
     case K7C: return 8;
-    case K7V: return 3;
+    case K7V: return 4;
     case K25W: return 1;
     case K25WA: return 1;
     case K25V: return 1;
@@ -706,12 +787,23 @@ cudaError_t launch_pipe(int kind, int b, const KParams& p, int zchunk_req, int n
           if (cfg == 1) CFG(K7V, 2, 32, 28, 2, 2, 4, 3, 1, 1);
           if (cfg == 2) CFG(K7V, 2, 32, 28, 1, 4, 4, 3, 0, 1);
           if (cfg == 3) CFG(K7V, 2, 32, 28, 1, 4, 4, 3, 1, 1);  // round-1 default (rings shifted)
+          if (cfg == 4) CFGU(K7V, 2, 32, 28, 2, 2, 4, 3, -1, 1);  // TMEM coefficient window
           CFGU(K7V, 2, 32, 28, 1, 4, 4, 3, 1, 1);                // C2: 148-151 -> 157-159 GLUP/s
         case 3:
           if (cfg == 1) CFG(K7V, 3, 32, 28, 1, 4, 4, 3, 1, 1);
           if (cfg == 2) CFG(K7V, 3, 32, 20, 1, 4, 4, 4, 0, 1);
           if (cfg == 3) CFGU(K7V, 3, 32, 28, 2, 2, 4, 3, 1, 1);
-          CFG(K7V, 3, 32, 28, 2, 2, 4, 3, 1, 1);
+          if (cfg == 4) CFGU(K7V, 3, 32, 28, 1, 2, 4, 3, 1, 1);
+          if (cfg == 5) CFG(K7V, 3, 32, 28, 1, 2, 4, 3, 1, 1);
+          if (cfg == 6) CFGU(K7V, 3, 32, 24, 1, 2, 4, 3, 1, 1);
+          if (cfg == 7) CFG(K7V, 3, 32, 28, 2, 2, 4, 3, 1, 1);   // session-1 default (register window)
+          if (cfg == 8) CFG(K7V, 3, 32, 28, 2, 2, 4, 3, -1, 1);
+          // TMEM coefficient window for levels 2..3 (WIN = -1): C2 bt=3 163-168 -> 184-192 GLUP/s
+          CFGU(K7V, 3, 32, 28, 2, 2, 4, 3, -1, 1);
+        case 4:  // TMEM coefficient window only (the ring would need (bt-1)*R more slots otherwise)
+          if (cfg == 1) CFGU(K7V, 4, 32, 28, 2, 2, 4, 2, -1, 1);
+          if (cfg == 2) CFG(K7V, 4, 32, 24, 2, 2, 4, 3, -1, 1);
+          CFGU(K7V, 4, 32, 24, 2, 2, 4, 3, -1, 1);
       }
       break;
     case K25W:

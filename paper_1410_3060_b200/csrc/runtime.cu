@@ -276,7 +276,7 @@ constexpr double kCoopAutoCells = 3.0e6;
 int default_bt(int kind) {
   switch (kind) {
     case ST_7PT_CONST: return 4;  // tools/sweep.py on B200
-    case ST_7PT_VAR: return 2;
+    case ST_7PT_VAR: return 3;  // TMEM coefficient window (session 2): 188 vs 154 GLUP/s at bt = 2
     default: return 1;
   }
 }
