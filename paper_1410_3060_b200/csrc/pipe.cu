@@ -17,7 +17,10 @@
 //    coefficients come from shared memory; levels >= 2 exchange their planes through a
 //    double-buffered shared plane and one named barrier (consumers only) per level;
 //  * persistent CTAs (one per SM) walk (tile, z-chunk) work items; the rings run on across items,
-//    so the producer prefetches the next item while consumers finish the current one.
+//    so the producer prefetches the next item while consumers finish the current one;
+//  * WIN = -1 configurations keep each thread's coefficients for levels 2..BT in TENSOR MEMORY
+//    (tcgen05.alloc / st / ld): the coefficient ring is released right after level 1 and the
+//    shared-memory traffic of levels >= 2 moves to the TMEM datapath.
 //
 // Results are bitwise identical to naive_kernel / stream_kernel (same point functions, point.cuh).
 #include "kernels.cuh"
@@ -253,6 +256,9 @@ struct PipeCfg {
   static constexpr int TCOLS = NSL * TSLOT;                     // columns per warp
   static_assert(!TW || WPQ * TCOLS <= 512, "TMEM window exceeds 512 columns");
   static_assert(!HAS_C || DC >= CLAG + 2, "C ring too shallow");
+  // a TMEM-window CTA allocates all 512 TMEM columns: its shared memory must keep a second CTA (of any
+  // TMEM-window kernel, e.g. on another stream) off the SM, or that CTA's tcgen05.alloc would wait
+  static_assert(!TW || SMEM > 116 * 1024, "TMEM-window configurations must occupy > half the shared memory");
   static_assert((EXB * 8) % 16 == 0 && (FXB * 8) % 16 == 0, "TMA box rows must be 16-byte multiples");
   static_assert(FXB <= 256 && FY <= 256 && EXB <= 256, "TMA box dimension limit");
 };
