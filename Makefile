@@ -11,7 +11,7 @@ CSRC      := paper_1410_3060_b200/csrc
 LIB       := paper_1410_3060_b200/libstencil.so
 OBJS      := build/kernels.o build/pipe.o build/runtime.o
 
-all: $(LIB) oracle/liboracle.so synth/libsynth.so build/fp64_peak
+all: $(LIB) oracle/liboracle.so synth/libsynth.so build/fp64_peak build/tmem_probe
 
 build:
 	mkdir -p build
@@ -29,6 +29,9 @@ $(LIB): $(OBJS)
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -ldl
 
 build/fp64_peak: tools/fp64_peak.cu | build
+	$(NVCC) $(ARCH) -O3 -o $@ $<
+
+build/tmem_probe: tools/tmem_probe.cu | build
 	$(NVCC) $(ARCH) -O3 -o $@ $<
 
 oracle/liboracle.so: oracle/oracle.c
