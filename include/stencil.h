@@ -179,6 +179,18 @@ int stencil_create(stencil_ctx **out, int kind, int64_t nx, int64_t ny, int64_t 
 int stencil_create_seeded(stencil_ctx **out, int kind, int64_t nx, int64_t ny, int64_t nz,
                           uint64_t seed, const double *scalars, const st_opts *opts);
 
+/*
+ * Host copy of the seeded input a stencil_create_seeded handle draws on the device (synth/synth.h,
+ * DESIGN.md readings Q6-Q9, Q21), same bits: writes the dense padded GLOBAL array
+ * (nz+2R)(ny+2R)(nx+2R) of one input into out (HOST pointer, out_elems >= that size).  No device is
+ * needed.  stream_id: 0 = V^0 (Omega^0 incl. ghosts, U[-1,1)); 1 = the wave's Omega^{-1} (interior
+ * from stream 1, ghosts from stream 0; ST_25PT_WAVE / _A only); 2 + i = coefficient field W_i of the
+ * variable kinds (U[0,1/7) / U[0,1/25)) or the alpha field of ST_25PT_WAVE_A (i = 0, U[0,0.2)).
+ * ST_E_INVAL for a stream the kind does not have, extents < 1, NULL or short out.
+ */
+int stencil_generate(int kind, int64_t nx, int64_t ny, int64_t nz, uint64_t seed, int stream_id, double *out,
+                     int64_t out_elems);
+
 /* Enqueue T >= 1 time steps (T < 1 -> ST_E_INVAL).  Asynchronous on opts->stream.
  * Multi-rank: collective; every rank calls it with the same T. */
 int stencil_run(stencil_ctx *h, int64_t T);

@@ -30,7 +30,7 @@ EXPORTED_SYMBOLS = [
     "stencil_read", "stencil_read_planes", "stencil_write", "stencil_info", "stencil_set_timing",
     "stencil_kernel_time", "stencil_destroy", "stencil_last_error", "stencil_nccl_unique_id",
     "stencil_plan_slab", "stencil_version", "stencil_peer_export", "stencil_peer_import",
-    "stencil_peer_handshake",
+    "stencil_peer_handshake", "stencil_generate",
 ]
 
 ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p)
@@ -103,6 +103,7 @@ def lib():
         "stencil_peer_export": (I, [P, P, ctypes.c_size_t]),
         "stencil_peer_import": (I, [P, P, P]),
         "stencil_peer_handshake": (I, [P, I]),
+        "stencil_generate": (I, [I, I64, I64, I64, ctypes.c_uint64, I, P, I64]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -228,6 +229,14 @@ def stencil_peer_import(h, below: bytes | None, above: bytes | None):
     b = None if below is None else ctypes.create_string_buffer(bytes(below), ST_PEER_DESC_BYTES)
     a = None if above is None else ctypes.create_string_buffer(bytes(above), ST_PEER_DESC_BYTES)
     _check(lib().stencil_peer_import(h, b, a))
+
+
+def stencil_generate(kind, nx, ny, nz, seed, stream_id) -> np.ndarray:
+    """Host copy of one seeded input (the device fill's bits), dense padded (nz+2R, ny+2R, nx+2R)."""
+    R = RADIUS.get(kind, 0)
+    out = np.empty((nz + 2 * R, ny + 2 * R, nx + 2 * R), dtype=np.float64)
+    _check(lib().stencil_generate(kind, nx, ny, nz, seed, stream_id, out.ctypes.data, out.size))
+    return out
 
 
 def stencil_peer_handshake(h, timeout_ms=10000):

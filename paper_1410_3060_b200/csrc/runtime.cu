@@ -15,6 +15,7 @@
 // announces the block; the neighbour's stream waits on that flag before its next block.
 #include "../../include/stencil.h"
 #include "kernels.cuh"
+#include "../../synth/synth.h"
 
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -1217,6 +1218,37 @@ int stencil_destroy(stencil_ctx* h) {
   if (!h->poisoned) wait_peers(h);  // no neighbour may still be storing into this rank's buffers
   release(h);
   delete h;
+  return ST_OK;
+}
+
+int stencil_generate(int kind, int64_t nx, int64_t ny, int64_t nz, uint64_t seed, int stream_id, double* out,
+                     int64_t out_elems) {
+  const int R = radius_of(kind);
+  if (R < 0) { set_err("bad kind %d", kind); return ST_E_INVAL; }
+  if (nx < 1 || ny < 1 || nz < 1) { set_err("extents must be >= 1"); return ST_E_INVAL; }
+  const int64_t X = nx + 2 * R, Y = ny + 2 * R, Z = nz + 2 * R;
+  if (!out || out_elems < X * Y * Z) { set_err("out must hold %lld doubles", (long long)(X * Y * Z)); return ST_E_INVAL; }
+  const int nf = ncoef_of(kind);
+  if (stream_id < 0 || (stream_id == 1 && !is_wave(kind)) || stream_id >= 2 + nf) {
+    set_err("kind %d has no input stream %d", kind, stream_id);
+    return ST_E_INVAL;
+  }
+  // the device fill's modes (st::launch_fill): 0 = U[-1,1) from the stream everywhere; 1 = wave
+  // Omega^{-1} (interior stream 1, the rest stream 0); 2 = U[0, c) from the stream
+  const int mode = stream_id == 0 ? 0 : stream_id == 1 ? 1 : 2;
+  const double c = kind == ST_7PT_VAR ? 1.0 / 7.0 : kind == ST_25PT_VAR ? 1.0 / 25.0 : 0.2;
+  const uint64_t key = synth_key(seed, mode == 1 ? SYNTH_STREAM_V : stream_id);
+  const uint64_t key_u = synth_key(seed, SYNTH_STREAM_U);
+  for (int64_t z = 0; z < Z; ++z)
+    for (int64_t y = 0; y < Y; ++y)
+      for (int64_t x = 0; x < X; ++x) {
+        const uint64_t idx = (uint64_t)((z * Y + y) * X + x);
+        double v;
+        if (mode == 2) v = synth_scaled(key, idx, c);
+        else if (mode == 1 && x >= R && x < X - R && y >= R && y < Y - R && z >= R && z < Z - R) v = synth_sym(key_u, idx);
+        else v = synth_sym(key, idx);
+        out[idx] = v;
+      }
   return ST_OK;
 }
 

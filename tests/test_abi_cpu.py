@@ -5,6 +5,7 @@ import os
 import re
 import subprocess
 
+import numpy as np
 import pytest
 
 import paper_1410_3060_b200 as st
@@ -97,3 +98,21 @@ def test_argument_validation_before_device():
     with pytest.raises(st.StencilError):
         st.stencil_run(None, 1)
     assert st.lib().stencil_destroy(None) == 0
+
+
+@pytest.mark.parametrize("kind", [1, 2, 3, 4, 5])
+def test_stencil_generate_equals_synth(kind):
+    """The library's host generator (the device fill's bits, no device needed) equals synth's inputs."""
+    import synth
+    n = (7, 5, 6)
+    inp = synth.make_inputs(kind, *n, seed=77)
+    assert np.array_equal(st.stencil_generate(kind, *n, 77, 0), inp.V)
+    if kind in synth.WAVE_KINDS:
+        assert np.array_equal(st.stencil_generate(kind, *n, 77, 1), inp.U)
+    for i, c in enumerate(inp.coef):
+        assert np.array_equal(st.stencil_generate(kind, *n, 77, 2 + i), c)
+    with pytest.raises(st.StencilError):
+        st.stencil_generate(kind, *n, 77, 2 + len(inp.coef))
+    if kind not in synth.WAVE_KINDS:
+        with pytest.raises(st.StencilError):
+            st.stencil_generate(kind, *n, 77, 1)
