@@ -42,6 +42,17 @@ def block_bytes_per_cell(kind, b):
     return 16 + 8 * synth.N_COEF_FIELDS[kind]
 
 
+def blocks_of(T, bt):
+    """Fused-block lengths stencil_run(T) uses (runtime.cu): full blocks of bt; a remainder shorter than
+    bt is merged with the last full block and split evenly."""
+    out, left = [], T
+    while left > 0:
+        b = (left + 1) // 2 if bt < left < 2 * bt else min(bt, left)
+        out.append(b)
+        left -= b
+    return out
+
+
 FLOPS_PER_LUP = {synth.K7C: 8, synth.K7V: 13, synth.K25W: 30, synth.K25V: 37, synth.K25WA: 30}
 
 
@@ -301,11 +312,7 @@ def main():
     # roofline of the dominant kernel (the z-streaming / fused-level kernel)
     bt = info["bt"]
     cells_local = w.nx * w.ny * (w.nz // world)
-    nblocks_full = w.T // bt
-    rem = w.T % bt
-    per_step_bytes = cells_local * (nblocks_full * block_bytes_per_cell(w.kind, bt)
-                                    + (block_bytes_per_cell(w.kind, rem) if rem else 0))
-    launches_per_step = nblocks_full + (1 if rem else 0)
+    per_step_bytes = cells_local * sum(block_bytes_per_cell(w.kind, b) for b in blocks_of(w.T, bt))
     avg_launch_ms = kern_ms / max(1, kern_launches)
     # achieved = algorithmic bytes of the timed launches / their summed device time (equivalently bytes
     # per launch / average launch time when every launch is a full block; with z-slabs each block is

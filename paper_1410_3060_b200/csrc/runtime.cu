@@ -955,7 +955,9 @@ int stencil_run(stencil_ctx* h, int64_t T) {
   const int bt = h->variant == ST_VARIANT_NAIVE ? 1 : h->bt;
   int64_t left = T;
   while (left > 0 && rc == ST_OK) {
-    const int b = (int)std::min<int64_t>(bt, left);
+    // a remainder shorter than bt is merged with the last full block and split evenly (T = 100 at
+    // bt = 3: ..., 3, 2, 2 instead of ..., 3, 3, 1): fewer levels in the least efficient launch
+    const int b = (left > bt && left < 2 * (int64_t)bt) ? (int)((left + 1) / 2) : (int)std::min<int64_t>(bt, left);
     rc = run_block(h, b);
     left -= b;
   }
