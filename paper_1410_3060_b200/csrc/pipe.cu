@@ -750,7 +750,7 @@ int max_pipe_bt(int kind) {
   switch (kind) {
     case K7C: return 8;
     case K7V: return 4;
-    case K25W: return 1;
+    case K25W: return 2;
     case K25WA: return 1;
     case K25V: return 1;
     default: return 0;
@@ -822,6 +822,10 @@ cudaError_t launch_pipe(int kind, int b, const KParams& p, int zchunk_req, int n
         if (cfg == 6) CFGU(K25W, 1, 64, 14, 2, 2, 10, 6, 0, 1);
         if (cfg == 7) CFGU(K25W, 1, 64, 20, 2, 2, 8, 4, 0, 1);
         CFGU(K25W, 1, 64, 14, 2, 2, 8, 4, 0, 1);               // C3: 165-169 -> 185-195 GLUP/s
+      }
+      if (b == 2) {  // the leapfrog with two fused levels: both time levels in, both out (32 B/cell)
+        if (cfg == 1) CFGU(K25W, 2, 32, 24, 2, 2, 7, 3, 0, 1);
+        CFG(K25W, 2, 32, 24, 2, 2, 7, 3, 0, 1);
       }
       break;
     case K25WA:
