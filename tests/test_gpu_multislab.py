@@ -192,3 +192,15 @@ def test_peer_import_validates():
     finally:
         a.close()
         b.close()
+
+
+@pytest.mark.parametrize("halo", [0, 1])
+@pytest.mark.parametrize("P", [2, 3])
+def test_wave_bt2_slabs(halo, P):
+    """The leapfrog at bt = 2 (four state buffers, BOTH time levels exchanged / forwarded after every
+    block) over z-slabs == one slab, bitwise, including a remainder block and a second run."""
+    n, T = (70, 20, 41), (5, 2)
+    ref = run(synth.K25W, n, T, bt=2, variant=st.ST_VARIANT_PIPE)
+    got = run(synth.K25W, n, T, nranks=P, local_slabs=P, bt=2, halo=halo)
+    assert got[2]["bt"] == 2 and ref[2]["bt"] == 2
+    assert np.array_equal(got[0], ref[0]) and np.array_equal(got[1], ref[1])
