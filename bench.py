@@ -149,9 +149,14 @@ def oracle_sample(w, target_s=12.0, max_steps=None):
     t0 = time.perf_counter()
     oracle.run_arrays(w.kind, w.nx, w.ny, w.nz, V, U, inp.coef, inp.scalars, steps, cores)
     dt = time.perf_counter() - t0
+    # SURVEY d.5: the same oracle on one host thread, one time step (reference for the core scaling)
+    t0 = time.perf_counter()
+    oracle.run_arrays(w.kind, w.nx, w.ny, w.nz, V, U, inp.coef, inp.scalars, 1, 1)
+    dt1 = time.perf_counter() - t0
     return {"value": cells * steps / dt / 1e9, "unit": METRIC, "cores": cores, "kind": "oracle",
             "sample": f"{steps} time step(s) of the full {w.nx}x{w.ny}x{w.nz} {synth.KIND_NAMES[w.kind]} "
                       f"grid ({cells * steps:.3g} LUPs, {dt:.2f} s)",
+            "value_1_thread": cells / dt1 / 1e9,
             "seconds": dt}
 
 
