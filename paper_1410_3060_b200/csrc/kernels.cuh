@@ -32,6 +32,14 @@ struct KParams {
                // skip level barriers; fault injection for the mutation tests (STENCIL_FAULT):
                // bit 2 = never write the last plane of a z-chunk, bit 3 = skip work item 0
   unsigned int* sched;  // pipe kernel: 2 zeroed device counters (next work item, CTAs done)
+  // Pipe kernel, several fused blocks in ONE launch (Jacobi kinds, single slab): nblk blocks; block i
+  // reads the buffer block i-1 wrote (odd blocks: V from dst_raw, stores to dst_alt = the src buffer);
+  // done[item] = dbase + i + 1 once item of block i is complete (dependency-driven scheduling).
+  int nblk;
+  unsigned int* done;
+  unsigned int dbase;
+  double* dst_alt;
+  const double* dst_raw;
   // Fused halo exchange (pipe kernel only): last-level output planes in local range
   // [rz0[q], rz1[q]) are also stored through rdst[q] (and rdstu[q], wave second level), a pointer into
   // a z-neighbour's buffer pre-offset so that the same element offset addresses the same global cell.
@@ -65,6 +73,7 @@ int max_stream_bt(int kind);
 // a producer warp streams planes of Omega^t and the coefficient fields into shared-memory rings
 // with cp.async.bulk.tensor + mbarriers; consumer warps run the same wavefront as stream_kernel.
 // cfg selects a tile configuration (0 = default for the kind and b).  Persistent: one CTA per SM.
+constexpr long long kMaxDoneItems = 1 << 18;  // per-item completion counters of a multi-block launch
 cudaError_t launch_pipe(int kind, int b, const KParams& p, int zchunk_req, int num_sms, int cfg,
                         cudaStream_t stream, LaunchInfo* info);
 int max_pipe_bt(int kind);

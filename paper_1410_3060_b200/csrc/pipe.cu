@@ -317,20 +317,49 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN,
       for (uint32_t n = 0;; ++n) {
         const uint32_t qs = n & 3;
         mbar_wait(&itemEmpty[qs], ((n >> 2) & 1) ^ 1);
-        int item = (int)atomicAdd(p.sched, 1u);
-        if (item >= items) item = -1;
-        itemq[qs] = item;
+        // ids run over all blocks of the launch: g = blk * items + item (p.nblk blocks, see below)
+        int g = (int)atomicAdd(p.sched, 1u);
+        if (g >= items * p.nblk) g = -1;
+        itemq[qs] = g;
         mbar_arrive(&itemFull[qs]);  // release: the id is visible to the consumers' acquire
-        if (item < 0) break;
+        if (g < 0) break;
+        const int blk = g / items, item = g - blk * items;
         if ((p.dbg & 8) && item == 0) continue;
         const Item it = decode<R, BT - 1, OX, OY>(item, ntx, nty, p);
+        if (blk > 0) {
+          // Dependency-driven scheduling across fused blocks (the paper's FIFO of ready tiles,
+          // P:786-805): an item of block blk reads the level block blk-1 wrote for its own and its
+          // 26 neighbouring items (x/y tiles, z-chunks: the trapezoid halo reaches R*BT <= one tile or
+          // chunk) and overwrites what they read, so it starts once all of them are done.  Ids are
+          // handed out in order and every CTA is resident, so the items waited for are in progress.
+          const int per = ntx * nty, zc = item / per, t = item - zc * per, ty = t / ntx, tx = t - ty * ntx;
+          const int nzc = items / per;
+          const unsigned int want = p.dbase + (unsigned int)blk;
+          for (int dz = -1; dz <= 1; ++dz)
+            for (int dy = -1; dy <= 1; ++dy)
+              for (int dx = -1; dx <= 1; ++dx) {
+                const int z2 = zc + dz, y2 = ty + dy, x2 = tx + dx;
+                if (z2 < 0 || z2 >= nzc || y2 < 0 || y2 >= nty || x2 < 0 || x2 >= ntx) continue;
+                const unsigned int* f = p.done + (z2 * per + y2 * ntx + x2);
+                unsigned int v;
+                for (;;) {
+                  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+                  if ((int)(v - want) >= 0) break;
+                  __nanosleep(256);
+                }
+              }
+          // the generic-proxy stores just observed must be visible to the TMA (async proxy) loads
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+        }
+        // Jacobi kinds alternate the two state buffers between blocks: mapA describes the other one
+        const CUtensorMap* mv = (!WAVE && (blk & 1)) ? &mapA : &mapV;
         const int xv = (it.gx0 - R + p.xoff) & ~1;  // footprint box
         const int xc = (it.gx0 + p.xoff) & ~1;      // level-1 extent box
         for (int s = it.s_begin; s <= it.s_end; ++s, ++iv) {
           const uint32_t sv = iv % DV, nv = iv / DV;
           mbar_wait(&emptyV[sv], (nv & 1) ^ 1);
           mbar_expect_tx(&fullV[sv], C::VELEMS * sizeof(double));
-          tma_load_3d(sV + (size_t)sv * C::VSLOT, &mapV, &fullV[sv], xv, it.gy0 - R, s);
+          tma_load_3d(sV + (size_t)sv * C::VSLOT, mv, &fullV[sv], xv, it.gy0 - R, s);
           if constexpr (HAS_C) {
             const uint32_t sc = iv % DC, nc = iv / DC;
             mbar_wait(&emptyC[sc], (nc & 1) ^ 1);
@@ -371,12 +400,24 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN,
   for (uint32_t n = 0;; ++n) {
     const uint32_t qs = n & 3;
     mbar_wait(&itemFull[qs], (n >> 2) & 1);
-    const int item = itemq[qs];
+    const int g = itemq[qs];
     __syncwarp();
     if (lane == 0) mbar_arrive(&itemEmpty[qs]);
-    if (item < 0) break;
-    if ((p.dbg & 8) && item == 0) continue;
+    if (g < 0) break;
+    const int blk = g / items, item = g - blk * items;
+    if ((p.dbg & 8) && item == 0) {  // fault injection: work item 0 never computed (still published)
+      if (p.nblk > 1) {
+        named_sync(1, NCONS);
+        if (tid == 0) {
+          __threadfence();
+          asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p.done + item), "r"(p.dbase + (unsigned int)blk + 1u)
+                       : "memory");
+        }
+      }
+      continue;
+    }
     const Item it = decode<R, BT - 1, OX, OY>(item, ntx, nty, p);
+    double* const dst = (!WAVE && (blk & 1)) ? p.dst_alt : p.dst;  // Jacobi buffers alternate per block
     bool outc[CY][CXN];
     unsigned act[CY][CXN];  // bit k: cell is interior and inside the level-k extent (computed at level k)
     long long col[CY];      // global offset of the block's first cell in each row
@@ -566,7 +607,7 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN,
           }
           if (k == BT && c >= it.zc0 && c < it.zc1 && !((p.dbg & 4) && c == it.zc1 - 1)) {
             const long long o = (long long)c * p.plane + col[j];
-            stg_row<CXN, VEC>(p.dst + o, vout, outc[j]);
+            stg_row<CXN, VEC>(dst + o, vout, outc[j]);
             if constexpr (WAVE && BT >= 2) stg_row<CXN, VEC>(p.dstu + o, uout, outc[j]);
           }
         }
@@ -626,10 +667,18 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN,
 #pragma unroll
           for (int i = 0; i < CXN; ++i)
             if (outc[j][i]) {
-              p.rdst[q][o + i] = __ldcg(p.dst + o + i);
+              p.rdst[q][o + i] = __ldcg(dst + o + i);
               if constexpr (WAVE && BT >= 2) p.rdstu[q][o + i] = __ldcg(p.dstu + o + i);
             }
         }
+      }
+    }
+    if (p.nblk > 1) {  // publish: this item of block blk is complete (all consumers' stores)
+      named_sync(1, NCONS);
+      if (tid == 0) {
+        __threadfence();
+        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p.done + item), "r"(p.dbase + (unsigned int)blk + 1u)
+                     : "memory");
       }
     }
   }
@@ -693,6 +742,7 @@ cudaError_t run_pipe(const KParams& p0, int zchunk_req, int num_sms, cudaStream_
     configured = true;
   }
   KParams p = p0;
+  if (p.nblk < 1) p.nblk = 1;
   const int planes = p.zo1 - p.zo0;
   if (planes <= 0) return cudaSuccess;
   if (p.xoff != 16 - C::R) return cudaErrorInvalidValue;  // decode() assumes interior column R at raw 16
@@ -725,6 +775,9 @@ cudaError_t run_pipe(const KParams& p0, int zchunk_req, int num_sms, cudaStream_
   memset(&mapA, 0, sizeof mapA);
   if (!make_map(&mapV, p.src_raw, 3, p.pitch, p.ny + 2 * C::R, p.zl, 1, p.plane, 0, C::FXB, C::FY, 1))
     return cudaErrorInvalidValue;
+  if (!C::WAVE && p.nblk > 1 &&  // multi-block launch: the V box of odd blocks comes from the other buffer
+      !make_map(&mapA, p.dst_raw, 3, p.pitch, p.ny + 2 * C::R, p.zl, 1, p.plane, 0, C::FXB, C::FY, 1))
+    return cudaErrorInvalidValue;
   if (C::HAS_C) {
     bool ok = C::WAVE ? make_map(&mapC, p.srcu_raw, 3, p.pitch, p.ny + 2 * C::R, p.zl, 1, p.plane, 0, C::EXB, TY, 1)
                       : make_map(&mapC, p.coef_raw, 4, p.pitch, p.ny + 2 * C::R, p.zl, C::NC, p.plane, p.cstride,
@@ -735,7 +788,8 @@ cudaError_t run_pipe(const KParams& p0, int zchunk_req, int num_sms, cudaStream_
   }
   int occ = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, C::THREADS, C::SMEM);
-  const int grid = (int)std::min<long long>(items, (long long)std::max(1, occ) * num_sms);
+  const int grid = (int)std::min<long long>(items * std::max(1, p.nblk), (long long)std::max(1, occ) * num_sms);
+  if (p.nblk > 1 && (C::WAVE || items > kMaxDoneItems || !p.done)) return cudaErrorInvalidValue;
   kern<<<grid, C::THREADS, C::SMEM, stream>>>(mapV, mapC, mapA, p, ntx, nty, (int)items);
   if (info) {
     info->tile_x = C::OXW; info->tile_y = C::OY; info->zchunk = zchunk; info->threads = C::THREADS;

@@ -159,6 +159,7 @@ struct stencil_ctx {
   int lv0 = 0, lv1 = 1;  // buffer index of Omega^t and Omega^{t-1} (same in every slab)
   double scal[6] = {0, 0, 0, 0, 0, 0};
   unsigned int* sched = nullptr;  // pipe kernel work counters (zero between launches)
+  unsigned int* done = nullptr;   // per-item completion counters of multi-block launches (lazy)
 
   std::vector<std::pair<void*, size_t>> allocs;
   int64_t steps = 0;
@@ -529,6 +530,7 @@ st::KParams base_params(stencil_ctx* h, const Slab& s) {
   p.dbg = env_int("STENCIL_DBG") | (env_int("STENCIL_FAULT") & 12);
   static const int walign = getenv("STENCIL_WALIGN") ? atoi(getenv("STENCIL_WALIGN")) : 0;
   p.walign = walign;
+  p.nblk = 1;
   return p;
 }
 
@@ -771,6 +773,47 @@ __global__ void peer_poke_kernel(uint64_t* below_flags, uint64_t* above_flags, u
 
 uint64_t handshake_magic(int rank) { return 0x5EED000000000000ull + (uint64_t)rank; }
 
+// Several full blocks of a single-slab Jacobi grid in ONE pipe-kernel launch (dependency-driven
+// scheduling across blocks, pipe.cu): the tail of block i can overlap the start of block i+1.
+// Opt-in (STENCIL_MULTIBLOCK=1): measured 1-5 % slower than one launch per block on B200 (C2 190.7 vs
+// 193.3, C4 49.9 vs 52.5 GLUP/s) -- an item of block i+1 waits for its z-neighbour chunk of block i,
+// which the zc-major item order runs last, so little of the tail overlaps (profiles/r01_summary.md).
+bool multiblock_ok(const stencil_ctx* h) {
+  return env_int("STENCIL_MULTIBLOCK") == 1 && h->variant == ST_VARIANT_PIPE && h->nranks == 1 && !is_wave(h->kind);
+}
+
+int run_blocks_fused(stencil_ctx* h, int nblk, int b) {
+  if (!h->done) {
+    const size_t bytes = (size_t)st::kMaxDoneItems * sizeof(unsigned int);
+    h->done = (unsigned int*)dev_alloc(h, bytes);
+    if (!h->done) { set_err("device allocation of %zu bytes failed (block counters)", bytes); return ST_E_NOMEM; }
+    CK(cudaMemsetAsync(h->done, 0, bytes, h->stream), "zero block counters");
+  }
+  Slab& s = h->slabs.front();
+  st::KParams p = base_params(h, s);
+  p.src = h->at(s, h->lv0);
+  p.srcu = h->at(s, h->lv1);
+  p.dst = h->at(s, h->lv1);
+  p.dst_alt = h->at(s, h->lv0);
+  p.src_raw = s.buf[h->lv0];
+  p.srcu_raw = s.buf[h->lv1];
+  p.dst_raw = s.buf[h->lv1];
+  p.nblk = nblk;
+  p.done = h->done;
+  p.dbase = (unsigned int)h->blocks;
+  cudaEvent_t ev_end = nullptr;
+  cudaEvent_t ev_begin = timing_begin(h, &ev_end);
+  const cudaError_t e = st::launch_pipe(h->kind, b, p, h->zchunk_req, h->num_sms, h->tile_cfg, h->stream,
+                                        &h->last_launch);
+  if (ev_begin) cudaEventRecord(ev_end, h->stream);
+  if (e != cudaSuccess) return cuda_fail(h, e, "multi-block kernel launch");
+  h->launches++;
+  if (nblk & 1) std::swap(h->lv0, h->lv1);
+  h->steps += (int64_t)nblk * b;
+  h->blocks += nblk;
+  return ST_OK;
+}
+
 // ST_HALO_PEER across processes: enqueue a wait until both neighbours have delivered every block run
 // so far (no remote store into this rank's memory is still in flight afterwards).
 int wait_peers(stencil_ctx* h) {
@@ -954,6 +997,18 @@ int stencil_run(stencil_ctx* h, int64_t T) {
   }
   const int bt = h->variant == ST_VARIANT_NAIVE ? 1 : h->bt;
   int64_t left = T;
+  if (multiblock_ok(h) && bt >= 1) {
+    // the leading run of full blocks (all but a merged remainder) in one launch
+    int64_t nfull = left / bt;
+    if (left % bt) nfull -= 1;  // the last full block is merged with the remainder (below)
+    const int64_t cap = 1 << 20;
+    while (nfull >= 2 && rc == ST_OK) {
+      const int64_t n = std::min<int64_t>(nfull, cap);
+      rc = run_blocks_fused(h, (int)n, bt);
+      left -= n * bt;
+      nfull -= n;
+    }
+  }
   while (left > 0 && rc == ST_OK) {
     // a remainder shorter than bt is merged with the last full block and split evenly (T = 100 at
     // bt = 3: ..., 3, 2, 2 instead of ..., 3, 3, 1): fewer levels in the least efficient launch

@@ -179,3 +179,18 @@ def test_error_codes_on_gpu():
         st.Grid(synth.K25V, 4000, 4000, 4000, seed=1)  # 15 x 32 GB: does not fit
     assert ei.value.code == st.ST_E_NOMEM
     assert "bytes" in st.stencil_last_error()
+
+
+@pytest.mark.parametrize("kind", [synth.K7C, synth.K7V, synth.K25V])
+def test_multiblock_launch_bitwise(kind, monkeypatch):
+    """All full blocks of a run in one pipe-kernel launch with dependency-driven scheduling across blocks
+    (STENCIL_MULTIBLOCK=1; opt-in) == one launch per block, bitwise, including remainder blocks, a
+    second run and the work-item-0 fault still terminating (its completion is published)."""
+    nx, ny, nz = SHAPES[kind]
+    for bt, T in ((1, 5), (max_bt(kind), 3 * max_bt(kind) + 1)):
+        ref = gpu_run(kind, nx, ny, nz, T, seed=5, variant=st.ST_VARIANT_PIPE, bt=bt, zchunk=7)
+        monkeypatch.setenv("STENCIL_MULTIBLOCK", "1")
+        got = gpu_run(kind, nx, ny, nz, T, seed=5, variant=st.ST_VARIANT_PIPE, bt=bt, zchunk=7)
+        monkeypatch.delenv("STENCIL_MULTIBLOCK")
+        assert np.array_equal(got[0], ref[0]), bt
+        assert got[2]["launches"] < ref[2]["launches"]
