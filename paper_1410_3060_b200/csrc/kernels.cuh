@@ -36,6 +36,7 @@ struct KParams {
   // reads the buffer block i-1 wrote (odd blocks: V from dst_raw, stores to dst_alt = the src buffer);
   // done[item] = dbase + i + 1 once item of block i is complete (dependency-driven scheduling).
   int nblk;
+  int nzc;  // z-chunks per tile (set by the launcher)
   unsigned int* done;
   unsigned int dbase;
   double* dst_alt;

@@ -128,7 +128,9 @@ __device__ __forceinline__ Item decode(int item, int ntx, int nty, const KParams
   // walign = 0 (experiment): OX-wide written tiles, grid shifted by dx so the origin is still even
   const int dx = p.walign ? 0 : ((R - R * H + p.xoff) & 1);
   const int per = ntx * nty;
-  const int zc = item / per, t = item - zc * per;
+  // multi-block launches order a block's items tile-major (the chunks of a tile consecutively), so the
+  // items an item of the next block depends on come early; otherwise z-chunk-major
+  const int zc = p.nblk > 1 ? item % p.nzc : item / per, t = p.nblk > 1 ? item / p.nzc : item - zc * per;
   const int ty = t / ntx, tx = t - ty * ntx;
   Item it;
   it.gx0 = R + tx * OXW - WOFF - R * H - dx;
@@ -332,15 +334,14 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN,
           // 26 neighbouring items (x/y tiles, z-chunks: the trapezoid halo reaches R*BT <= one tile or
           // chunk) and overwrites what they read, so it starts once all of them are done.  Ids are
           // handed out in order and every CTA is resident, so the items waited for are in progress.
-          const int per = ntx * nty, zc = item / per, t = item - zc * per, ty = t / ntx, tx = t - ty * ntx;
-          const int nzc = items / per;
+          const int per = ntx * nty, nzc = p.nzc, zc = item % nzc, t = item / nzc, ty = t / ntx, tx = t - ty * ntx;
           const unsigned int want = p.dbase + (unsigned int)blk;
           for (int dz = -1; dz <= 1; ++dz)
             for (int dy = -1; dy <= 1; ++dy)
               for (int dx = -1; dx <= 1; ++dx) {
                 const int z2 = zc + dz, y2 = ty + dy, x2 = tx + dx;
                 if (z2 < 0 || z2 >= nzc || y2 < 0 || y2 >= nty || x2 < 0 || x2 >= ntx) continue;
-                const unsigned int* f = p.done + (z2 * per + y2 * ntx + x2);
+                const unsigned int* f = p.done + ((y2 * ntx + x2) * nzc + z2);  // tile-major ids
                 unsigned int v;
                 for (;;) {
                   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
@@ -769,6 +770,7 @@ cudaError_t run_pipe(const KParams& p0, int zchunk_req, int num_sms, cudaStream_
   }
   p.zchunk = zchunk;
   const int nzc = (planes + zchunk - 1) / zchunk;
+  p.nzc = nzc;
   const long long items = tiles * nzc;
   CUtensorMap mapV, mapC, mapA;
   memset(&mapC, 0, sizeof mapC);

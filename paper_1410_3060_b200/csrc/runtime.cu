@@ -775,9 +775,9 @@ uint64_t handshake_magic(int rank) { return 0x5EED000000000000ull + (uint64_t)ra
 
 // Several full blocks of a single-slab Jacobi grid in ONE pipe-kernel launch (dependency-driven
 // scheduling across blocks, pipe.cu): the tail of block i can overlap the start of block i+1.
-// Opt-in (STENCIL_MULTIBLOCK=1): measured 1-5 % slower than one launch per block on B200 (C2 190.7 vs
-// 193.3, C4 49.9 vs 52.5 GLUP/s) -- an item of block i+1 waits for its z-neighbour chunk of block i,
-// which the zc-major item order runs last, so little of the tail overlaps (profiles/r01_summary.md).
+// Opt-in (STENCIL_MULTIBLOCK=1): measured 1-7 % slower than one launch per block on B200 (C2 ~189 vs
+// 193, C4 49 vs 52.5 GLUP/s): the kernels run at the 1 kW power cap, where the idle tails of per-block
+// launches cost no throughput and filling them lowers the SM clock (profiles/r01_summary.md).
 bool multiblock_ok(const stencil_ctx* h) {
   return env_int("STENCIL_MULTIBLOCK") == 1 && h->variant == ST_VARIANT_PIPE && h->nranks == 1 && !is_wave(h->kind);
 }
