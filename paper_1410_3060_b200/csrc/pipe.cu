@@ -666,11 +666,21 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN,
         for (int j = 0; j < CY; ++j) {
           const long long o = (long long)c * p.plane + col[j];
 #pragma unroll
-          for (int i = 0; i < CXN; ++i)
-            if (outc[j][i]) {
-              p.rdst[q][o + i] = __ldcg(dst + o + i);
-              if constexpr (WAVE && BT >= 2) p.rdstu[q][o + i] = __ldcg(p.dstu + o + i);
+          for (int i = 0; i < CXN; i += (VEC ? 2 : 1)) {
+            if (VEC && outc[j][i] && outc[j][i + 1 < CXN ? i + 1 : i]) {  // 16-byte aligned pair (see stg_row)
+              *reinterpret_cast<double2*>(p.rdst[q] + o + i) = __ldcg(reinterpret_cast<const double2*>(dst + o + i));
+              if constexpr (WAVE && BT >= 2)
+                *reinterpret_cast<double2*>(p.rdstu[q] + o + i) =
+                    __ldcg(reinterpret_cast<const double2*>(p.dstu + o + i));
+              continue;
             }
+#pragma unroll
+            for (int e = 0; e < (VEC ? 2 : 1); ++e)
+              if (i + e < CXN && outc[j][i + e]) {
+                p.rdst[q][o + i + e] = __ldcg(dst + o + i + e);
+                if constexpr (WAVE && BT >= 2) p.rdstu[q][o + i + e] = __ldcg(p.dstu + o + i + e);
+              }
+          }
         }
       }
     }
