@@ -823,10 +823,13 @@ int max_pipe_bt(int kind) {
   }
 }
 
-// Tile configurations <KIND, BT, TX, TY, CY, DV, DC> (level-1 extent TX x TY, strips of CY cells,
-// ring depths).  Shared memory per CTA stays below the 227 KB opt-in limit (DESIGN.md §5 lists each
-// budget).  At BT = 1 the coefficient box equals the output tile, and TX = 32 / 64 puts its rows on
-// 128-byte lines (the interior column x = R is 128-byte aligned in the device layout).
+// Tile configurations <KIND, BT, TX, TY, CX, CY, DV, DC, WIN, MINB>: level-1 extent TX x TY, cell
+// blocks of CX x CY per consumer thread, V / coefficient ring depths, coefficient window of the levels
+// >= 2 (0: shared ring, k > 0: register window for the last k levels, -1: TMEM window), CTAs per SM.
+// The last entry of each (kind, bt) is the default (tile_cfg 0); the others are the alternatives the
+// sweeps in profiles/ compare (all bitwise equal, test G4).  Shared memory per CTA stays below the
+// 227 KB opt-in limit (DESIGN.md §5 lists each budget).  At BT = 1 the coefficient box equals the output
+// tile, and TX = 32 / 64 puts its rows on 128-byte lines (interior column x = R is 128-byte aligned).
 cudaError_t launch_pipe(int kind, int b, const KParams& p, int zchunk_req, int num_sms, int cfg,
                         cudaStream_t stream, LaunchInfo* info) {
   // CFG(kind, BT, TX, TY, CX, CY, DV, DC, WIN, MINB)
