@@ -462,7 +462,10 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN,
     const int s = s0 + u;
     if (UNR && s > it.s_end) break;
     {
-      const int buf = s & 1;
+      // level planes alternate with the CTA's step counter, not the plane index: across an item boundary
+      // s jumps, and two consecutive steps on the same buffer would let a fast thread overwrite a plane
+      // a slower thread is still reading (the named barrier follows the write)
+      const int buf = (int)(iv & 1u);
       // Level 0: plane s of Omega^t -> register rings.
       const uint32_t sv = iv % DV;
       mbar_wait(&fullV[sv], (iv / DV) & 1);
