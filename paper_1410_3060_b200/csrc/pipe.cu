@@ -258,6 +258,10 @@ struct PipeCfg {
   static constexpr int TCOLS = NSL * TSLOT;                     // columns per warp
   static_assert(!TW || WPQ * TCOLS <= 512, "TMEM window exceeds 512 columns");
   static_assert(!HAS_C || DC >= CLAG + 2, "C ring too shallow");
+  // MERGE: C ring as deep as the V ring and consumed in the same step it arrives (CLAG = 0): slot i of
+  // both rings is filled under ONE full barrier and freed with the V slot (one wait, one arrive less
+  // per step and thread)
+  static constexpr bool MERGE = HAS_C && CLAG == 0 && DC == DV;
   // a TMEM-window CTA allocates all 512 TMEM columns: its shared memory must keep a second CTA (of any
   // TMEM-window kernel, e.g. on another stream) off the SM, or that CTA's tcgen05.alloc would wait
   static_assert(!TW || SMEM > 116 * 1024, "TMEM-window configurations must occupy > half the shared memory");
@@ -359,18 +363,21 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN,
         for (int s = it.s_begin; s <= it.s_end; ++s, ++iv) {
           const uint32_t sv = iv % DV, nv = iv / DV;
           mbar_wait(&emptyV[sv], (nv & 1) ^ 1);
-          mbar_expect_tx(&fullV[sv], C::VELEMS * sizeof(double));
+          mbar_expect_tx(&fullV[sv], (C::VELEMS + (C::MERGE ? C::CFIELD * C::NCF : 0)) * sizeof(double));
           tma_load_3d(sV + (size_t)sv * C::VSLOT, mv, &fullV[sv], xv, it.gy0 - R, s);
           if constexpr (HAS_C) {
             const uint32_t sc = iv % DC, nc = iv / DC;
-            mbar_wait(&emptyC[sc], (nc & 1) ^ 1);
-            mbar_expect_tx(&fullC[sc], (C::CFIELD * C::NCF) * sizeof(double));  // bytes the TMA boxes move
+            uint64_t* fc = C::MERGE ? &fullV[sv] : &fullC[sc];
+            if constexpr (!C::MERGE) {
+              mbar_wait(&emptyC[sc], (nc & 1) ^ 1);
+              mbar_expect_tx(&fullC[sc], (C::CFIELD * C::NCF) * sizeof(double));  // bytes the TMA boxes move
+            }
             if constexpr (WAVE) {
-              tma_load_3d(sC + (size_t)sc * C::CSLOT, &mapC, &fullC[sc], xc, it.gy0, s - R);
+              tma_load_3d(sC + (size_t)sc * C::CSLOT, &mapC, fc, xc, it.gy0, s - R);
               if constexpr (NC > 0)  // the wave's alpha field behind Omega^{t-1} in the same slot
-                tma_load_4d(sC + (size_t)sc * C::CSLOT + C::CF0, &mapA, &fullC[sc], xc, it.gy0, s - R, 0);
+                tma_load_4d(sC + (size_t)sc * C::CSLOT + C::CF0, &mapA, fc, xc, it.gy0, s - R, 0);
             } else {
-              tma_load_4d(sC + (size_t)sc * C::CSLOT, &mapC, &fullC[sc], xc, it.gy0, s - R, 0);
+              tma_load_4d(sC + (size_t)sc * C::CSLOT, &mapC, fc, xc, it.gy0, s - R, 0);
             }
           }
         }
@@ -488,7 +495,7 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN,
       // physical index of logical ring entry q (all ring reads below happen after this step's update
       // of the ring they read)
       auto ri = [u](int q) { return UNR ? (u + 1 + q) % RL : q; };
-      if constexpr (HAS_C) mbar_wait(&fullC[iv % DC], (iv / DC) & 1);
+      if constexpr (HAS_C && !C::MERGE) mbar_wait(&fullC[iv % DC], (iv / DC) & 1);
 
 #pragma unroll
       for (int k = 1; k <= BT; ++k) {
@@ -638,7 +645,7 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN,
             }
           }
       }
-      if (HAS_C && iv >= iv_b + CLAG) {  // C plane of step iv - CLAG fully consumed
+      if (HAS_C && !C::MERGE && iv >= iv_b + CLAG) {  // C plane of step iv - CLAG fully consumed
         __syncwarp();
         if (lane == 0) mbar_arrive(&emptyC[(iv - CLAG) % DC]);
       }
@@ -650,7 +657,7 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN,
     __syncwarp();
     if (lane == 0) {
       for (uint32_t i = (iv >= iv_b + R ? iv - R : iv_b); i < iv; ++i) mbar_arrive(&emptyV[i % DV]);
-      if (HAS_C)
+      if (HAS_C && !C::MERGE)
         for (uint32_t i = (iv >= iv_b + CLAG ? iv - CLAG : iv_b); i < iv; ++i) mbar_arrive(&emptyC[i % DC]);
     }
     // Fused halo exchange (ST_HALO_PEER): the item's output planes that are a
@@ -893,7 +900,8 @@ cudaError_t launch_pipe(int kind, int b, const KParams& p, int zchunk_req, int n
         if (cfg == 5) CFG(K25W, 1, 64, 14, 2, 2, 10, 6, 0, 1);
         if (cfg == 6) CFGU(K25W, 1, 64, 14, 2, 2, 10, 6, 0, 1);
         if (cfg == 7) CFGU(K25W, 1, 64, 20, 2, 2, 8, 4, 0, 1);
-        CFGU(K25W, 1, 64, 14, 2, 2, 8, 4, 0, 1);               // C3: 165-169 -> 185-195 GLUP/s
+        if (cfg == 8) CFGU(K25W, 1, 64, 14, 2, 2, 8, 4, 0, 1);
+        CFGU(K25W, 1, 64, 14, 2, 2, 8, 8, 0, 1);  // merged V/U rings; C3: 165-169 (round 1) -> 185-196 GLUP/s
       }
       if (b == 2) {  // the leapfrog with two fused levels: both time levels in, both out (32 B/cell)
         if (cfg == 1) CFGU(K25W, 2, 32, 24, 2, 2, 7, 3, 0, 1);
@@ -905,7 +913,8 @@ cudaError_t launch_pipe(int kind, int b, const KParams& p, int zchunk_req, int n
         if (cfg == 1) CFG(K25WA, 1, 64, 16, 1, 4, 7, 3, 0, 1);
         if (cfg == 2) CFG(K25WA, 1, 64, 14, 2, 2, 7, 3, 0, 1);  // round-1 default (rings shifted)
         if (cfg == 3) CFGU(K25WA, 1, 64, 20, 2, 2, 8, 4, 0, 1);
-        CFGU(K25WA, 1, 64, 14, 2, 2, 8, 4, 0, 1);               // C3A: 148-152 -> 160 GLUP/s
+        if (cfg == 4) CFGU(K25WA, 1, 64, 14, 2, 2, 8, 4, 0, 1);
+        CFGU(K25WA, 1, 64, 14, 2, 2, 8, 8, 0, 1);  // merged rings; C3A: 148-152 (round 1) -> 172-179 GLUP/s
       }
       break;
     case K25V:
