@@ -110,6 +110,41 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&w)[32]) {
       : "r"(taddr)
       : "memory");
 }
+// Distributed shared memory (cluster-pair tiles): the partner CTA's copy of a local
+// shared-memory address, a 128-bit load from it, a remote mbarrier arrive, and a barrier over every
+// thread of the cluster.
+__device__ __forceinline__ uint32_t dsmem_addr(const void* local, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(local)), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ double2 ld_dsmem2(uint32_t addr) {
+  double2 v;
+  asm volatile("ld.shared::cluster.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr) : "memory");
+  return v;
+}
+__device__ __forceinline__ double ld_dsmem1(uint32_t addr) {
+  double v;
+  asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(addr) : "memory");
+  return v;
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t remote_bar) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote_bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "LAB_WAITC:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+      "@P1 bra DONEC;\n\t"
+      "bra LAB_WAITC;\n"
+      "DONEC:\n\t}" ::"r"(smem_u32(b)),
+      "r"(parity), "r"(0x989680u)
+      : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release;\n\tbarrier.cluster.wait.acquire;" ::: "memory");
+}
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
@@ -196,7 +231,8 @@ __device__ __forceinline__ void stg_row(double* p, const double* v, const bool* 
 // cell is computed at level 1, and the level-BT output tile is
 // OX x OY = (TX - 2R(BT-1)) x (TY - 2R(BT-1)).  The Omega^t box (footprint) is E1 grown by R on each
 // side; the coefficient (or wave U) box is E1 itself.  DV / DC = ring depths (planes).
-template <int KIND, int BT, int TX, int TY, int CX, int CY, int DV, int DC, int WIN, int MINB, bool UNR>
+template <int KIND, int BT, int TX, int TY, int CX, int CY, int DV, int DC, int WIN, int MINB, bool UNR,
+          int CLU>
 struct PipeCfg {
   using TR = Traits<KIND>;
   static constexpr int R = TR::R, NC = TR::NCOEF, RL = 2 * R + 1;
@@ -209,6 +245,12 @@ struct PipeCfg {
   static constexpr int THREADS = NCONS + 32;
   static constexpr int FX = TX + 2 * R, FY = TY + 2 * R;         // Omega^t footprint
   static constexpr int OX = TX - 2 * R * (BT - 1), OY = TY - 2 * R * (BT - 1);
+  // CLU = 2: a cluster of two CTAs works on one tile of TX x 2TY level-1 cells, CTA r
+  // owning rows [r*TY, (r+1)*TY) at EVERY level: the trapezoid shrinks only at the pair's outer rows, and
+  // level-k rows across the internal boundary are read from the partner's shared memory (DSMEM).
+  // OYP = output rows of the pair (= OY for a single CTA).
+  static_assert(CLU == 1 || CLU == 2, "cluster of 1 or 2 CTAs");
+  static constexpr int OYP = CLU * TY - 2 * R * (BT - 1);
   static constexpr int OXW = OX & ~3, WOFF = (OX - OXW) / 2;  // written output columns, offset
   static_assert(OXW > 0 && (WOFF + R * (BT - 1)) % 2 == 0, "level-1 extent origin must be even");
   // fields of the C ring: the wave's Omega^{t-1} (field 0), then the NC coefficient fields
@@ -233,7 +275,7 @@ struct PipeCfg {
   static constexpr int NPL = BT - 1;                      // shared level planes (double-buffered)
   static constexpr size_t SMEM = sizeof(double) * ((size_t)DV * VSLOT + (HAS_C ? (size_t)DC * CSLOT : 0) +
                                                    (size_t)NPL * 2 * PELEMS) +
-                                 sizeof(uint64_t) * (2 * (DV + DC) + 8) + 4 * sizeof(int) + 128;
+                                 sizeof(uint64_t) * (2 * (DV + DC) + 8 + 2 * NPL) + 4 * sizeof(int) + 128;
   static_assert(TY % CY == 0 && TX % CX == 0 && (CX == 1 || CX % 2 == 0), "cell blocks");
   static_assert(OX > 0 && OY > 0, "tile too small for BT");
   static_assert(NCONS % 32 == 0, "whole consumer warps");
@@ -269,11 +311,12 @@ struct PipeCfg {
   static_assert(FXB <= 256 && FY <= 256 && EXB <= 256, "TMA box dimension limit");
 };
 
-template <int KIND, int BT, int TX, int TY, int CX, int CY, int DV, int DC, int WIN, int MINB, bool UNR>
-__global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN, MINB, UNR>::THREADS, MINB)
+template <int KIND, int BT, int TX, int TY, int CX, int CY, int DV, int DC, int WIN, int MINB, bool UNR,
+          int CLU>
+__global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN, MINB, UNR, CLU>::THREADS, MINB)
     pipe_kernel(const __grid_constant__ CUtensorMap mapV, const __grid_constant__ CUtensorMap mapC,
                 const __grid_constant__ CUtensorMap mapA, const KParams p, int ntx, int nty, int items) {
-  using C = PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN, MINB, UNR>;
+  using C = PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN, MINB, UNR, CLU>;
   constexpr int R = C::R, NC = C::NC, RL = C::RL, NCONS = C::NCONS, FXB = C::FXB, EXB = C::EXB;
   constexpr int L = C::L;
   constexpr bool WAVE = C::WAVE, HAS_C = C::HAS_C;
@@ -294,12 +337,18 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN,
   uint64_t* itemFull = bars + 2 * (DV + DC);
   uint64_t* itemEmpty = itemFull + 4;
   volatile int* itemq = reinterpret_cast<volatile int*>(itemEmpty + 4);
+  // CLU = 2: per (level, buffer) "the partner's plane is written" barriers, arrived on by the partner
+  uint64_t* xbar = reinterpret_cast<uint64_t*>(const_cast<int*>(itemq) + 4);
+  uint32_t crank = 0;
+  if constexpr (CLU == 2) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
 
   const int tid = threadIdx.x;
   if (tid == 0) {
     for (int i = 0; i < DV; ++i) { mbar_init(&fullV[i], 1); mbar_init(&emptyV[i], NCONS / 32); }
     for (int i = 0; i < DC; ++i) { mbar_init(&fullC[i], 1); mbar_init(&emptyC[i], NCONS / 32); }
     for (int i = 0; i < 4; ++i) { mbar_init(&itemFull[i], 1); mbar_init(&itemEmpty[i], NCONS / 32); }
+    if constexpr (CLU == 2)
+      for (int i = 0; i < 2 * C::NPL; ++i) mbar_init(&xbar[i], NCONS / 32);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __shared__ uint32_t tmem_base;
@@ -313,6 +362,7 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN,
   }
   __syncthreads();
   if constexpr (C::TW) asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  if constexpr (CLU == 2) cluster_sync_all();  // the partner's barriers exist before any remote arrive
 
   if (tid >= NCONS) {
     // ---------------------------------------------------------------- producer warp
@@ -324,14 +374,20 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN,
         const uint32_t qs = n & 3;
         mbar_wait(&itemEmpty[qs], ((n >> 2) & 1) ^ 1);
         // ids run over all blocks of the launch: g = blk * items + item (p.nblk blocks, see below)
-        int g = (int)atomicAdd(p.sched, 1u);
+        int g;
+        if constexpr (CLU == 2) {  // both CTAs of a cluster walk the same static item sequence
+          g = (int)(blockIdx.x / 2) + (int)n * (int)(gridDim.x / 2);
+        } else {
+          g = (int)atomicAdd(p.sched, 1u);
+        }
         if (g >= items * p.nblk) g = -1;
         itemq[qs] = g;
         mbar_arrive(&itemFull[qs]);  // release: the id is visible to the consumers' acquire
         if (g < 0) break;
         const int blk = g / items, item = g - blk * items;
         if ((p.dbg & 8) && item == 0) continue;
-        const Item it = decode<R, BT - 1, OX, OY>(item, ntx, nty, p);
+        Item it = decode<R, BT - 1, OX, C::OYP>(item, ntx, nty, p);
+        it.gy0 += (int)crank * TY;
         if (blk > 0) {
           // Dependency-driven scheduling across fused blocks (the paper's FIFO of ready tiles,
           // P:786-805): an item of block blk reads the level block blk-1 wrote for its own and its
@@ -384,12 +440,14 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN,
       }
       // every CTA has drawn its terminating id before the last one gets here: reset for the next launch
       __threadfence();
-      if (atomicAdd(p.sched + 1, 1u) == gridDim.x - 1) {
+      if (CLU == 1 && atomicAdd(p.sched + 1, 1u) == gridDim.x - 1) {
         p.sched[0] = 0;
         p.sched[1] = 0;
         __threadfence();
       }
     }
+    // the whole producer warp: no CTA of a cluster exits while its partner may still read its memory
+    if constexpr (CLU == 2) cluster_sync_all();
     return;
   }
 
@@ -424,7 +482,8 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN,
       }
       continue;
     }
-    const Item it = decode<R, BT - 1, OX, OY>(item, ntx, nty, p);
+    Item it = decode<R, BT - 1, OX, C::OYP>(item, ntx, nty, p);
+    it.gy0 += (int)crank * TY;  // this CTA's rows of a cluster-pair tile
     double* const dst = (!WAVE && (blk & 1)) ? p.dst_alt : p.dst;  // Jacobi buffers alternate per block
     bool outc[CY][CXN];
     unsigned act[CY][CXN];  // bit k: cell is interior and inside the level-k extent (computed at level k)
@@ -439,9 +498,12 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN,
         const bool inter = gx >= R && gx < p.nx + R && gy >= R && gy < p.ny + R;
         act[j][i] = 0;
 #pragma unroll
-        for (int k = 1; k <= BT; ++k)
-          if (inter && lx >= (k - 1) * R && lx < TX - (k - 1) * R && ly >= (k - 1) * R && ly < TY - (k - 1) * R)
-            act[j][i] |= 1u << k;
+        for (int k = 1; k <= BT; ++k) {
+          // a cluster pair's trapezoid shrinks only at its outer rows
+          const int ylo = (CLU == 2 && crank == 1) ? 0 : (k - 1) * R;
+          const int yhi = (CLU == 2 && crank == 0) ? TY : TY - (k - 1) * R;
+          if (inter && lx >= (k - 1) * R && lx < TX - (k - 1) * R && ly >= ylo && ly < yhi) act[j][i] |= 1u << k;
+        }
         const int oxw = p.walign ? C::OXW : OX, woff = (OX - oxw) / 2;
         outc[j][i] = ((act[j][i] >> BT) & 1u) && lx >= woff + R * (BT - 1) && lx < woff + R * (BT - 1) + oxw;
       }
@@ -521,6 +583,16 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN,
             sts_row<CXN, VEC>(P + (ly0 + j) * TX + x0, v);
           }
           if (!(p.dbg & 2)) named_sync(1, NCONS);
+          if constexpr (CLU == 2) {
+            // tell the partner this CTA's level-(k-1) rows of this step are written, and wait for the
+            // partner's (the barrier of plane (k, buf) completes once every second step)
+            uint64_t* xb = &xbar[(k - 2) * 2 + buf];
+            if (lane == 0) mbar_arrive_remote(dsmem_addr(xb, crank ^ 1u));
+            // only warps that read rows across the boundary wait (the partner's rows they read are
+            // written by the partner's boundary warps, which wait the same way before overwriting)
+            const bool edge = crank == 0 ? (ly0 + CY + R > TY) : (ly0 - R < 0);
+            if (__any_sync(0xffffffffu, edge)) mbar_wait_cluster(xb, (iv >> 1) & 1u);
+          }
           Sb = P;
           SS = TX;
         }
@@ -530,7 +602,26 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN,
 #pragma unroll
         for (int q = 0; q < CY + 2 * R; ++q) {
           int row = ly0 - R + q;
-          if (k > 1) row = min(max(row, 0), TY - 1);  // level planes have no halo rows
+          if (k > 1) {
+            if (CLU == 2 && ((crank == 0 && row >= TY) || (crank == 1 && row < 0))) {
+              // across the pair's internal boundary: the partner's copy of the same level plane
+              const int prow = crank == 0 ? row - TY : row + TY;
+              const uint32_t ra = dsmem_addr(Sb + prow * SS + x0, crank ^ 1u);
+              if constexpr (VEC && CXN % 2 == 0) {
+#pragma unroll
+                for (int i = 0; i < CXN / 2; ++i) {
+                  const double2 v = ld_dsmem2(ra + 16u * (uint32_t)i);
+                  ys[q][2 * i] = v.x;
+                  ys[q][2 * i + 1] = v.y;
+                }
+              } else {
+#pragma unroll
+                for (int i = 0; i < CXN; ++i) ys[q][i] = ld_dsmem1(ra + 8u * (uint32_t)i);
+              }
+              continue;
+            }
+            row = min(max(row, 0), TY - 1);  // level planes have no halo rows (outer side: discarded)
+          }
           lds_row<CXN, VEC>(Sb + row * SS + x0, ys[q]);
         }
 #pragma unroll
@@ -711,6 +802,7 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN,
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     if (tid < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base) : "memory");
   }
+  if constexpr (CLU == 2) cluster_sync_all();  // the partner may still read this CTA's level planes
 }
 
 // ------------------------------------------------------------------------------------------------ host
@@ -752,10 +844,11 @@ bool make_map(CUtensorMap* m, const double* base, int rank, long long pitch, lon
   return r == CUDA_SUCCESS;
 }
 
-template <int KIND, int BT, int TX, int TY, int CX, int CY, int DV, int DC, int WIN = 0, int MINB = 1, bool UNR = false>
+template <int KIND, int BT, int TX, int TY, int CX, int CY, int DV, int DC, int WIN = 0, int MINB = 1, bool UNR = false,
+          int CLU = 1>
 cudaError_t run_pipe(const KParams& p0, int zchunk_req, int num_sms, cudaStream_t stream, LaunchInfo* info) {
-  using C = PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN, MINB, UNR>;
-  auto kern = pipe_kernel<KIND, BT, TX, TY, CX, CY, DV, DC, WIN, MINB, UNR>;
+  using C = PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN, MINB, UNR, CLU>;
+  auto kern = pipe_kernel<KIND, BT, TX, TY, CX, CY, DV, DC, WIN, MINB, UNR, CLU>;
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
@@ -769,7 +862,7 @@ cudaError_t run_pipe(const KParams& p0, int zchunk_req, int num_sms, cudaStream_
   if (p.xoff != 16 - C::R) return cudaErrorInvalidValue;  // decode() assumes interior column R at raw 16
   const int oxw = p.walign ? C::OXW : C::OX;
   const int dx = p.walign ? 0 : ((C::R - C::R * (BT - 1) + p.xoff) & 1);
-  const int ntx = (p.nx + dx + oxw - 1) / oxw, nty = (p.ny + C::OY - 1) / C::OY;
+  const int ntx = (p.nx + dx + oxw - 1) / oxw, nty = (p.ny + C::OYP - 1) / C::OYP;
   const long long tiles = (long long)ntx * nty;
   int zchunk = zchunk_req;
   if (zchunk <= 0) {
@@ -810,11 +903,31 @@ cudaError_t run_pipe(const KParams& p0, int zchunk_req, int num_sms, cudaStream_
   }
   int occ = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, C::THREADS, C::SMEM);
-  const int grid = (int)std::min<long long>(items * std::max(1, p.nblk), (long long)std::max(1, occ) * num_sms);
-  if (p.nblk > 1 && (C::WAVE || items > kMaxDoneItems || !p.done)) return cudaErrorInvalidValue;
-  kern<<<grid, C::THREADS, C::SMEM, stream>>>(mapV, mapC, mapA, p, ntx, nty, (int)items);
+  int grid = (int)std::min<long long>(items * std::max(1, p.nblk), (long long)std::max(1, occ) * num_sms);
+  if (p.nblk > 1 && (C::WAVE || CLU != 1 || items > kMaxDoneItems || !p.done)) return cudaErrorInvalidValue;
+  if constexpr (CLU == 1) {
+    kern<<<grid, C::THREADS, C::SMEM, stream>>>(mapV, mapC, mapA, p, ntx, nty, (int)items);
+  } else {
+    // clusters of CLU CTAs along x of the grid (consecutive blockIdx.x), static item schedule per cluster
+    grid = (int)std::min<long long>((long long)items * CLU, (long long)std::max(1, occ) * num_sms / CLU * CLU);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(C::THREADS);
+    cfg.dynamicSmemBytes = C::SMEM;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CLU;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const int it32 = (int)items;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, mapV, mapC, mapA, p, ntx, nty, it32);
+    if (e != cudaSuccess) return e;
+  }
   if (info) {
-    info->tile_x = C::OXW; info->tile_y = C::OY; info->zchunk = zchunk; info->threads = C::THREADS;
+    info->tile_x = C::OXW; info->tile_y = C::OYP; info->zchunk = zchunk; info->threads = C::THREADS;
     info->smem = (int)C::SMEM; info->ctas = grid;
   }
   return cudaGetLastError();
@@ -848,6 +961,9 @@ cudaError_t launch_pipe(int kind, int b, const KParams& p, int zchunk_req, int n
   // CFGU: the same with the z-loop unrolled by the ring length (rings rotate by renaming)
 #define CFGU(K, B, TX, TY, CX, CY, DV, DC, W, M) \
   return run_pipe<K, B, TX, TY, CX, CY, DV, DC, W, M, true>(p, zchunk_req, num_sms, stream, info)
+  // CFGC: unrolled, cluster pair (two CTAs share one TX x 2TY tile through DSMEM)
+#define CFGC(K, B, TX, TY, CX, CY, DV, DC, W, M) \
+  return run_pipe<K, B, TX, TY, CX, CY, DV, DC, W, M, true, 2>(p, zchunk_req, num_sms, stream, info)
   // Consumer-thread counts are kept at <= 224 (+ 32 producer = 256 threads) where registers matter:
   // ptxas budgets registers for blocks rounded up to 128 threads (288-thread blocks get 168).
   switch (kind) {
@@ -883,11 +999,13 @@ cudaError_t launch_pipe(int kind, int b, const KParams& p, int zchunk_req, int n
           if (cfg == 6) CFGU(K7V, 3, 32, 24, 1, 2, 4, 3, 1, 1);
           if (cfg == 7) CFG(K7V, 3, 32, 28, 2, 2, 4, 3, 1, 1);   // session-1 default (register window)
           if (cfg == 8) CFG(K7V, 3, 32, 28, 2, 2, 4, 3, -1, 1);
+          if (cfg == 9) CFGC(K7V, 3, 32, 28, 2, 2, 4, 3, -1, 1);  // cluster pair: 32 x 56 tile
           // TMEM coefficient window for levels 2..3 (WIN = -1): C2 bt=3 163-168 -> 184-192 GLUP/s
           CFGU(K7V, 3, 32, 28, 2, 2, 4, 3, -1, 1);
         case 4:  // TMEM coefficient window only (the ring would need (bt-1)*R more slots otherwise)
           if (cfg == 1) CFGU(K7V, 4, 32, 28, 2, 2, 4, 2, -1, 1);
           if (cfg == 2) CFG(K7V, 4, 32, 24, 2, 2, 4, 3, -1, 1);
+          if (cfg == 3) CFGC(K7V, 4, 32, 24, 2, 2, 4, 3, -1, 1);  // cluster pair: 32 x 48 tile
           CFGU(K7V, 4, 32, 24, 2, 2, 4, 3, -1, 1);
       }
       break;
@@ -928,6 +1046,7 @@ cudaError_t launch_pipe(int kind, int b, const KParams& p, int zchunk_req, int n
   }
 #undef CFG
 #undef CFGU
+#undef CFGC
   return cudaErrorInvalidValue;
 }
 

@@ -24,7 +24,7 @@ def max_bt(kind, variant=st.ST_VARIANT_PIPE):
     return {synth.K7C: 8, synth.K7V: 4, synth.K25W: 2, synth.K25V: 1, synth.K25WA: 1}[kind]
 
 
-N_CFG = {synth.K7C: 1, synth.K7V: 9, synth.K25W: 9, synth.K25V: 4, synth.K25WA: 5}  # pipe tile configurations
+N_CFG = {synth.K7C: 1, synth.K7V: 10, synth.K25W: 9, synth.K25V: 4, synth.K25WA: 5}  # pipe tile configurations
 
 
 @pytest.mark.parametrize("kind", KINDS)
