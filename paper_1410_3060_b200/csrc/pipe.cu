@@ -142,6 +142,18 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* b, uint32_t parity) 
       "r"(parity), "r"(0x989680u)
       : "memory");
 }
+// one thread: bulk-copy `bytes` of this CTA's shared memory into the partner's, completing `bytes` of
+// transactions on the partner's mbarrier (async proxy: no release fence on the issuing thread)
+__device__ __forceinline__ void bulk_copy_to_peer(uint32_t dst_remote, const void* src_local, uint32_t bytes,
+                                                  uint32_t mbar_remote) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst_remote),
+      "r"(smem_u32(src_local)), "r"(bytes), "r"(mbar_remote)
+      : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory"); }
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release;\n\tbarrier.cluster.wait.acquire;" ::: "memory");
 }
@@ -251,6 +263,14 @@ struct PipeCfg {
   // OYP = output rows of the pair (= OY for a single CTA).
   static_assert(CLU == 1 || CLU == 2, "cluster of 1 or 2 CTAs");
   static constexpr int OYP = CLU * TY - 2 * R * (BT - 1);
+  // The boundary row of level k (computed at z-step s) is needed by the partner's level k+1 one step
+  // later (R = 1): it is staged in shared memory and pushed with ONE async bulk copy per level and step
+  // (cp.async.bulk.shared::cluster, completion on the partner's mbarrier) -- a step of slack hides the
+  // cross-SM latency, and no compute thread issues a cluster-scope release.  Staging: 4 slots (the
+  // issuing thread only waits for copies two steps old), receive: 4 slots (a partner can run at most
+  // two steps ahead of the pushes it needs).
+  static_assert(CLU == 1 || R == 1, "cluster pairs: 7-point kinds (one boundary row per level)");
+  static constexpr int XROW = TX * R;
   static constexpr int OXW = OX & ~3, WOFF = (OX - OXW) / 2;  // written output columns, offset
   static_assert(OXW > 0 && (WOFF + R * (BT - 1)) % 2 == 0, "level-1 extent origin must be even");
   // fields of the C ring: the wave's Omega^{t-1} (field 0), then the NC coefficient fields
@@ -274,8 +294,9 @@ struct PipeCfg {
   static constexpr int PELEMS = TX * TY;                  // one level plane (levels 1..BT-1)
   static constexpr int NPL = BT - 1;                      // shared level planes (double-buffered)
   static constexpr size_t SMEM = sizeof(double) * ((size_t)DV * VSLOT + (HAS_C ? (size_t)DC * CSLOT : 0) +
-                                                   (size_t)NPL * 2 * PELEMS) +
-                                 sizeof(uint64_t) * (2 * (DV + DC) + 8 + 2 * NPL) + 4 * sizeof(int) + 128;
+                                                   (size_t)NPL * 2 * PELEMS + (CLU == 2 ? (size_t)NPL * 8 * TX * R : 0)) +
+                                 sizeof(uint64_t) * (2 * (DV + DC) + 8 + (CLU == 2 ? 4 * NPL + 8 : 0)) +
+                                 (CLU == 2 ? 8 : 4) * sizeof(int) + 128;
   static_assert(TY % CY == 0 && TX % CX == 0 && (CX == 1 || CX % 2 == 0), "cell blocks");
   static_assert(OX > 0 && OY > 0, "tile too small for BT");
   static_assert(NCONS % 32 == 0, "whole consumer warps");
@@ -327,7 +348,10 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN,
   double* sV = reinterpret_cast<double*>(smem_raw);
   double* sC = sV + (size_t)DV * C::VSLOT;
   double* sP = sC + (HAS_C ? (size_t)DC * C::CSLOT : 0);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + (size_t)C::NPL * 2 * C::PELEMS);
+  // CLU = 2: staging [level][4][XROW] and receive [level][4][XROW] rows (16-byte aligned: XROW even)
+  double* sTx = sP + (size_t)C::NPL * 2 * C::PELEMS;
+  double* sRx = sTx + (CLU == 2 ? (size_t)C::NPL * 4 * C::XROW : 0);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sRx + (CLU == 2 ? (size_t)C::NPL * 4 * C::XROW : 0));
   uint64_t* fullV = bars;
   uint64_t* emptyV = bars + DV;
   uint64_t* fullC = bars + 2 * DV;
@@ -337,8 +361,12 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN,
   uint64_t* itemFull = bars + 2 * (DV + DC);
   uint64_t* itemEmpty = itemFull + 4;
   volatile int* itemq = reinterpret_cast<volatile int*>(itemEmpty + 4);
-  // CLU = 2: per (level, buffer) "the partner's plane is written" barriers, arrived on by the partner
-  uint64_t* xbar = reinterpret_cast<uint64_t*>(const_cast<int*>(itemq) + 4);
+  // CLU = 2: receive barriers [level][4]: this CTA's expect_tx arrive + the partner's copy bytes
+  uint64_t* rxb = reinterpret_cast<uint64_t*>(const_cast<int*>(itemq) + 4);
+  // CLU = 2: rank 0's producer draws the work items and hands them to rank 1's producer (DSMEM queue)
+  uint64_t* cfull = rxb + 4 * C::NPL;
+  uint64_t* cempty = cfull + 4;
+  volatile int* cid = reinterpret_cast<volatile int*>(cempty + 4);
   uint32_t crank = 0;
   if constexpr (CLU == 2) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
 
@@ -347,8 +375,10 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN,
     for (int i = 0; i < DV; ++i) { mbar_init(&fullV[i], 1); mbar_init(&emptyV[i], NCONS / 32); }
     for (int i = 0; i < DC; ++i) { mbar_init(&fullC[i], 1); mbar_init(&emptyC[i], NCONS / 32); }
     for (int i = 0; i < 4; ++i) { mbar_init(&itemFull[i], 1); mbar_init(&itemEmpty[i], NCONS / 32); }
-    if constexpr (CLU == 2)
-      for (int i = 0; i < 2 * C::NPL; ++i) mbar_init(&xbar[i], NCONS / 32);
+    if constexpr (CLU == 2) {
+      for (int i = 0; i < 4 * C::NPL; ++i) mbar_init(&rxb[i], 1);
+      for (int i = 0; i < 4; ++i) { mbar_init(&cfull[i], 1); mbar_init(&cempty[i], 1); }
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __shared__ uint32_t tmem_base;
@@ -375,12 +405,25 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN,
         mbar_wait(&itemEmpty[qs], ((n >> 2) & 1) ^ 1);
         // ids run over all blocks of the launch: g = blk * items + item (p.nblk blocks, see below)
         int g;
-        if constexpr (CLU == 2) {  // both CTAs of a cluster walk the same static item sequence
-          g = (int)(blockIdx.x / 2) + (int)n * (int)(gridDim.x / 2);
+        if constexpr (CLU == 2) {
+          // both CTAs of a cluster take the same items: rank 0 draws from the global counter and
+          // passes the id through a 4-entry queue in rank 1's shared memory
+          if (crank == 0) {
+            mbar_wait(&cempty[qs], ((n >> 2) & 1) ^ 1);
+            g = (int)atomicAdd(p.sched, 1u);
+            if (g >= items * p.nblk) g = -1;
+            asm volatile("st.shared::cluster.s32 [%0], %1;" ::"r"(dsmem_addr((const void*)&cid[qs], 1u)), "r"(g)
+                         : "memory");
+            mbar_arrive_remote(dsmem_addr(&cfull[qs], 1u));
+          } else {
+            mbar_wait_cluster(&cfull[qs], (n >> 2) & 1);
+            g = cid[qs];
+            mbar_arrive_remote(dsmem_addr(&cempty[qs], 0u));
+          }
         } else {
           g = (int)atomicAdd(p.sched, 1u);
+          if (g >= items * p.nblk) g = -1;
         }
-        if (g >= items * p.nblk) g = -1;
         itemq[qs] = g;
         mbar_arrive(&itemFull[qs]);  // release: the id is visible to the consumers' acquire
         if (g < 0) break;
@@ -440,7 +483,7 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN,
       }
       // every CTA has drawn its terminating id before the last one gets here: reset for the next launch
       __threadfence();
-      if (CLU == 1 && atomicAdd(p.sched + 1, 1u) == gridDim.x - 1) {
+      if ((CLU == 1 || crank == 0) && atomicAdd(p.sched + 1, 1u) == gridDim.x / CLU - 1) {
         p.sched[0] = 0;
         p.sched[1] = 0;
         __threadfence();
@@ -584,14 +627,17 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN,
           }
           if (!(p.dbg & 2)) named_sync(1, NCONS);
           if constexpr (CLU == 2) {
-            // tell the partner this CTA's level-(k-1) rows of this step are written, and wait for the
-            // partner's (the barrier of plane (k, buf) completes once every second step)
-            uint64_t* xb = &xbar[(k - 2) * 2 + buf];
-            if (lane == 0) mbar_arrive_remote(dsmem_addr(xb, crank ^ 1u));
-            // only warps that read rows across the boundary wait (the partner's rows they read are
-            // written by the partner's boundary warps, which wait the same way before overwriting)
-            const bool edge = crank == 0 ? (ly0 + CY + R > TY) : (ly0 - R < 0);
-            if (__any_sync(0xffffffffu, edge)) mbar_wait_cluster(xb, (iv >> 1) & 1u);
+            // the boundary row of level k-1 (computed this step, staged, ordered by the barrier
+            // above) goes to the partner; this CTA expects the partner's row of this step in slot iv % 4
+            if (tid == 0) {
+              const uint32_t rslot = (uint32_t)(k - 2) * 4u + (iv & 3u);
+              asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+              mbar_expect_tx(&rxb[rslot], (uint32_t)(C::XROW * sizeof(double)));
+              bulk_copy_to_peer(dsmem_addr(sRx + (size_t)rslot * C::XROW, crank ^ 1u),
+                                sTx + (size_t)((k - 2) * 4 + (iv & 3u)) * C::XROW,
+                                (uint32_t)(C::XROW * sizeof(double)), dsmem_addr(&rxb[rslot], crank ^ 1u));
+              bulk_wait_read<2 * C::NPL>();  // copies of two steps ago have read their staging slots
+            }
           }
           Sb = P;
           SS = TX;
@@ -604,19 +650,15 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN,
           int row = ly0 - R + q;
           if (k > 1) {
             if (CLU == 2 && ((crank == 0 && row >= TY) || (crank == 1 && row < 0))) {
-              // across the pair's internal boundary: the partner's copy of the same level plane
-              const int prow = crank == 0 ? row - TY : row + TY;
-              const uint32_t ra = dsmem_addr(Sb + prow * SS + x0, crank ^ 1u);
-              if constexpr (VEC && CXN % 2 == 0) {
-#pragma unroll
-                for (int i = 0; i < CXN / 2; ++i) {
-                  const double2 v = ld_dsmem2(ra + 16u * (uint32_t)i);
-                  ys[q][2 * i] = v.x;
-                  ys[q][2 * i + 1] = v.y;
-                }
+              // across the pair's internal boundary: the partner's level-(k-1) row of this plane,
+              // computed and pushed by it one step ago (receive slot (iv - 1) % 4)
+              if (iv > 0) {
+                const uint32_t rslot = (uint32_t)(k - 2) * 4u + ((iv - 1u) & 3u);
+                mbar_wait_cluster(&rxb[rslot], ((iv - 1u) >> 2) & 1u);
+                lds_row<CXN, VEC>(sRx + (size_t)rslot * C::XROW + x0, ys[q]);
               } else {
 #pragma unroll
-                for (int i = 0; i < CXN; ++i) ys[q][i] = ld_dsmem1(ra + 8u * (uint32_t)i);
+                for (int i = 0; i < CXN; ++i) ys[q][i] = 0.0;  // the kernel's first step: never a valid plane
               }
               continue;
             }
@@ -693,6 +735,8 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN,
             // the store predicate below already implies the select's condition (outc -> act bit BT,
             // c in [zc0, zc1) -> zv), so the select is skipped there.
             const double v = (k == BT) ? vc : (zv && ((act[j][i] >> k) & 1u)) ? vc : ring[k - 1][j][i][ri(R)];
+            if (CLU == 2 && k < BT && (crank == 0 ? ly == TY - 1 : ly == 0))  // stage the boundary row
+              sTx[(size_t)((k - 1) * 4 + (iv & 3u)) * C::XROW + x0 + i] = v;
             if (k < BT) {
               if constexpr (UNR) {
                 ring[k < BT ? k : 0][j][i][u % RL] = v;

@@ -15,6 +15,7 @@ torch.cuda.set_device(0)
 N = int(sys.argv[1]) if len(sys.argv) > 1 else 10
 cases = [(synth.K7V, (256, 200, 160), 12, dict(variant=3)), (synth.K7V, (256, 200, 160), 12, dict(variant=3, zchunk=5)),
          (synth.K7V, (256, 200, 160), 12, dict(variant=3, bt=4, zchunk=7)),
+         (synth.K7V, (256, 200, 160), 12, dict(variant=3, bt=3, tile_cfg=9, zchunk=7)),  # cluster pairs
          (synth.K25W, (256, 120, 100), 6, dict(variant=3, zchunk=9)), (synth.K25V, (192, 100, 90), 5, dict(variant=3, zchunk=9)),
          (synth.K7C, (200, 200, 200), 17, dict(variant=3, zchunk=6))]
 bad = 0
