@@ -264,11 +264,11 @@ struct PipeCfg {
   static_assert(CLU == 1 || CLU == 2, "cluster of 1 or 2 CTAs");
   static constexpr int OYP = CLU * TY - 2 * R * (BT - 1);
   // The boundary row of level k (computed at z-step s) is needed by the partner's level k+1 one step
-  // later (R = 1): it is staged in shared memory and pushed with ONE async bulk copy per level and step
-  // (cp.async.bulk.shared::cluster, completion on the partner's mbarrier) -- a step of slack hides the
-  // cross-SM latency, and no compute thread issues a cluster-scope release.  Staging: 4 slots (the
-  // issuing thread only waits for copies two steps old), receive: 4 slots (a partner can run at most
-  // two steps ahead of the pushes it needs).
+  // later (R = 1): the rows of levels 1..BT-1 are staged in shared memory and pushed together with ONE
+  // async bulk copy per step after the last level's barrier (cp.async.bulk.shared::cluster, completion
+  // on the partner's mbarrier) -- a step of slack hides the cross-SM latency, and no compute thread
+  // issues a cluster-scope release.  Staging: 4 slots (the issuing thread only waits for copies two
+  // steps old), receive: 4 slots (a partner can run at most two steps ahead of the pushes it needs).
   static_assert(CLU == 1 || R == 1, "cluster pairs: 7-point kinds (one boundary row per level)");
   static constexpr int XROW = TX * R;
   static constexpr int OXW = OX & ~3, WOFF = (OX - OXW) / 2;  // written output columns, offset
@@ -295,7 +295,7 @@ struct PipeCfg {
   static constexpr int NPL = BT - 1;                      // shared level planes (double-buffered)
   static constexpr size_t SMEM = sizeof(double) * ((size_t)DV * VSLOT + (HAS_C ? (size_t)DC * CSLOT : 0) +
                                                    (size_t)NPL * 2 * PELEMS + (CLU == 2 ? (size_t)NPL * 8 * TX * R : 0)) +
-                                 sizeof(uint64_t) * (2 * (DV + DC) + 8 + (CLU == 2 ? 4 * NPL + 8 : 0)) +
+                                 sizeof(uint64_t) * (2 * (DV + DC) + 8 + (CLU == 2 ? 4 + 8 : 0)) +
                                  (CLU == 2 ? 8 : 4) * sizeof(int) + 128;
   static_assert(TY % CY == 0 && TX % CX == 0 && (CX == 1 || CX % 2 == 0), "cell blocks");
   static_assert(OX > 0 && OY > 0, "tile too small for BT");
@@ -348,7 +348,7 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN,
   double* sV = reinterpret_cast<double*>(smem_raw);
   double* sC = sV + (size_t)DV * C::VSLOT;
   double* sP = sC + (HAS_C ? (size_t)DC * C::CSLOT : 0);
-  // CLU = 2: staging [level][4][XROW] and receive [level][4][XROW] rows (16-byte aligned: XROW even)
+  // CLU = 2: staging [4][level][XROW] and receive [4][level][XROW] rows (16-byte aligned: XROW even)
   double* sTx = sP + (size_t)C::NPL * 2 * C::PELEMS;
   double* sRx = sTx + (CLU == 2 ? (size_t)C::NPL * 4 * C::XROW : 0);
   uint64_t* bars = reinterpret_cast<uint64_t*>(sRx + (CLU == 2 ? (size_t)C::NPL * 4 * C::XROW : 0));
@@ -361,10 +361,10 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN,
   uint64_t* itemFull = bars + 2 * (DV + DC);
   uint64_t* itemEmpty = itemFull + 4;
   volatile int* itemq = reinterpret_cast<volatile int*>(itemEmpty + 4);
-  // CLU = 2: receive barriers [level][4]: this CTA's expect_tx arrive + the partner's copy bytes
+  // CLU = 2: receive barriers [4 slots]: this CTA's expect_tx arrive + the partner's copy bytes
   uint64_t* rxb = reinterpret_cast<uint64_t*>(const_cast<int*>(itemq) + 4);
   // CLU = 2: rank 0's producer draws the work items and hands them to rank 1's producer (DSMEM queue)
-  uint64_t* cfull = rxb + 4 * C::NPL;
+  uint64_t* cfull = rxb + 4;
   uint64_t* cempty = cfull + 4;
   volatile int* cid = reinterpret_cast<volatile int*>(cempty + 4);
   uint32_t crank = 0;
@@ -376,7 +376,7 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN,
     for (int i = 0; i < DC; ++i) { mbar_init(&fullC[i], 1); mbar_init(&emptyC[i], NCONS / 32); }
     for (int i = 0; i < 4; ++i) { mbar_init(&itemFull[i], 1); mbar_init(&itemEmpty[i], NCONS / 32); }
     if constexpr (CLU == 2) {
-      for (int i = 0; i < 4 * C::NPL; ++i) mbar_init(&rxb[i], 1);
+      for (int i = 0; i < 4; ++i) mbar_init(&rxb[i], 1);
       for (int i = 0; i < 4; ++i) { mbar_init(&cfull[i], 1); mbar_init(&cempty[i], 1); }
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -627,16 +627,16 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN,
           }
           if (!(p.dbg & 2)) named_sync(1, NCONS);
           if constexpr (CLU == 2) {
-            // the boundary row of level k-1 (computed this step, staged, ordered by the barrier
-            // above) goes to the partner; this CTA expects the partner's row of this step in slot iv % 4
-            if (tid == 0) {
-              const uint32_t rslot = (uint32_t)(k - 2) * 4u + (iv & 3u);
+            if (k == BT && tid == 0) {
+              // the boundary rows of levels 1..BT-1 (computed this step, staged, ordered by the barrier
+              // above) go to the partner in one copy; this CTA expects the partner's rows of this step
+              const uint32_t slot = iv & 3u;
+              constexpr uint32_t bytes = (uint32_t)(C::NPL * C::XROW * sizeof(double));
               asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-              mbar_expect_tx(&rxb[rslot], (uint32_t)(C::XROW * sizeof(double)));
-              bulk_copy_to_peer(dsmem_addr(sRx + (size_t)rslot * C::XROW, crank ^ 1u),
-                                sTx + (size_t)((k - 2) * 4 + (iv & 3u)) * C::XROW,
-                                (uint32_t)(C::XROW * sizeof(double)), dsmem_addr(&rxb[rslot], crank ^ 1u));
-              bulk_wait_read<2 * C::NPL>();  // copies of two steps ago have read their staging slots
+              mbar_expect_tx(&rxb[slot], bytes);
+              bulk_copy_to_peer(dsmem_addr(sRx + (size_t)slot * C::NPL * C::XROW, crank ^ 1u),
+                                sTx + (size_t)slot * C::NPL * C::XROW, bytes, dsmem_addr(&rxb[slot], crank ^ 1u));
+              bulk_wait_read<2>();  // copies of two steps ago have read their staging slots
             }
           }
           Sb = P;
@@ -653,9 +653,9 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN,
               // across the pair's internal boundary: the partner's level-(k-1) row of this plane,
               // computed and pushed by it one step ago (receive slot (iv - 1) % 4)
               if (iv > 0) {
-                const uint32_t rslot = (uint32_t)(k - 2) * 4u + ((iv - 1u) & 3u);
-                mbar_wait_cluster(&rxb[rslot], ((iv - 1u) >> 2) & 1u);
-                lds_row<CXN, VEC>(sRx + (size_t)rslot * C::XROW + x0, ys[q]);
+                const uint32_t slot = (iv - 1u) & 3u;
+                mbar_wait_cluster(&rxb[slot], ((iv - 1u) >> 2) & 1u);
+                lds_row<CXN, VEC>(sRx + ((size_t)slot * C::NPL + (k - 2)) * C::XROW + x0, ys[q]);
               } else {
 #pragma unroll
                 for (int i = 0; i < CXN; ++i) ys[q][i] = 0.0;  // the kernel's first step: never a valid plane
@@ -736,7 +736,7 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN,
             // c in [zc0, zc1) -> zv), so the select is skipped there.
             const double v = (k == BT) ? vc : (zv && ((act[j][i] >> k) & 1u)) ? vc : ring[k - 1][j][i][ri(R)];
             if (CLU == 2 && k < BT && (crank == 0 ? ly == TY - 1 : ly == 0))  // stage the boundary row
-              sTx[(size_t)((k - 1) * 4 + (iv & 3u)) * C::XROW + x0 + i] = v;
+              sTx[((size_t)(iv & 3u) * C::NPL + (k - 1)) * C::XROW + x0 + i] = v;
             if (k < BT) {
               if constexpr (UNR) {
                 ring[k < BT ? k : 0][j][i][u % RL] = v;
