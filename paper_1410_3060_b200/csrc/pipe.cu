@@ -1050,6 +1050,7 @@ cudaError_t launch_pipe(int kind, int b, const KParams& p, int zchunk_req, int n
           if (cfg == 1) CFGU(K7V, 4, 32, 28, 2, 2, 4, 2, -1, 1);
           if (cfg == 2) CFG(K7V, 4, 32, 24, 2, 2, 4, 3, -1, 1);
           if (cfg == 3) CFGC(K7V, 4, 32, 24, 2, 2, 4, 3, -1, 1);  // cluster pair: 32 x 48 tile
+          if (cfg == 4) CFGC(K7V, 4, 32, 28, 2, 2, 4, 2, -1, 1);  // cluster pair: 32 x 56 tile
           CFGU(K7V, 4, 32, 24, 2, 2, 4, 3, -1, 1);
       }
       break;

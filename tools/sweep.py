@@ -69,7 +69,8 @@ def main():
                     print(json.dumps({"workload": name, "variant": variant, "bt": info["bt"], "cfg": cfg,
                                       "zchunk": info["zchunk"], "tile": [info["tile_x"], info["tile_y"]],
                                       "ms": round(ms, 3), "glups": round(lups / ms / 1e6, 2),
-                                      "sm_mhz": cs.get("sm_mhz"), "reasons": cs.get("reasons")}), flush=True)
+                                      "sm_mhz": cs.get("sm_mhz"), "power_w": cs.get("power_w"),
+                                      "reasons": cs.get("reasons")}), flush=True)
                     torch.cuda.empty_cache()
 
 
