@@ -340,6 +340,12 @@ def main():
                 "roof_glups_fp64": fp64 * 1e3 / FLOPS_PER_LUP[w.kind],
                 "roof_glups": min(peak / (block_bytes_per_cell(w.kind, bt) / bt),
                                   fp64 * 1e3 / FLOPS_PER_LUP[w.kind])}
+    # SURVEY 8(d) anti-gaming rule: the fraction of the bt = 1 roofline and the measured DRAM bytes per
+    # lattice update (ncu, one launch of bt levels over the local grid) next to the compulsory B_C / bt
+    roofline["frac_of_roof_bt1"] = value / world / roofline["roof_glups_bt1"]
+    roofline["compulsory_bytes_per_lup"] = block_bytes_per_cell(w.kind, bt) / bt
+    tr = roofline["traffic"]
+    roofline["dram_bytes_per_lup"] = tr / (cells_local * bt) if tr else None
 
     g.close()
     del g
