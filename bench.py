@@ -129,12 +129,16 @@ def load_fp64_peak():
         return 37.2, "nominal (64 FP64 FMA lanes per SM x 148 SMs x 1.965 GHz)"
 
 
-def pick_workload(name, n_gpus):
+def pick_workload(name, n_gpus, scaling="weak"):
+    """The workload of an N-GPU run.  weak: per-GPU work fixed (the global nz grows with N; C5 uses
+    BASELINE.json's weak variant 1024 x 1024 x 256N); strong: the configuration's global grid split over N."""
     w = workloads.BY_NAME.get(name) or {x.name.split("-")[0]: x
                                         for x in workloads.CONFIGS + workloads.EXTRA}.get(name)
     if w is None:
         raise SystemExit(f"unknown workload {name}")
-    if n_gpus > 1:
+    if n_gpus > 1 and scaling == "weak":
+        if w is workloads.C5:
+            return workloads.weak_c5(n_gpus)
         w = workloads.Workload(f"{w.name}-weak-x{n_gpus}", w.kind, w.nx, w.ny, w.nz * n_gpus, w.T)
     return w
 
@@ -223,6 +227,9 @@ def main():
     ap.add_argument("--slabs", type=int, default=1,
                     help="single GPU only: run the z-slab plan with this many slabs on the one device "
                          "(loopback halo copies; measures the multi-GPU plan's overhead)")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="N > 1: weak = per-GPU work fixed (default; C5: 1024x1024x256N), strong = the "
+                         "configuration's global grid split over the N GPUs")
     ap.add_argument("--halo", default="peer", choices=["copy", "peer"],
                     help="z-slab halo exchange: copy = edge kernels + NCCL send/recv (device copies in "
                          "loopback) overlapped with the interior kernel; peer = fused into the kernel, "
@@ -247,7 +254,7 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     n = world
-    w = pick_workload(args.workload, n)
+    w = pick_workload(args.workload, n, args.scaling)
     nccl_id = None
     if world > 1:
         obj = [st.stencil_nccl_unique_id() if rank == 0 else None]
@@ -433,7 +440,7 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": METRIC, "n_gpus": n, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (synth/ counter-based generator, seed 14103060, drawn on the device)",
             "config": {"workload": w.name, "kind": synth.KIND_NAMES[w.kind], "nx": w.nx, "ny": w.ny,
                        "nz": w.nz, "T": w.T, "bt": bt, "variant": info["variant"],
