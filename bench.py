@@ -37,9 +37,9 @@ METRIC = "GLUP/s"
 # compulsory HBM bytes per lattice cell per fused block of b levels:
 # state read once + written once per block, coefficients read once per block, no write-allocate.
 def block_bytes_per_cell(kind, b):
-    if kind in synth.WAVE_KINDS:  # b = 1: read V, U, write U in place; b >= 2: both levels in & out
-        return (24 if b == 1 else 32) + 8 * synth.N_COEF_FIELDS[kind]
-    return 16 + 8 * synth.N_COEF_FIELDS[kind]
+    """Compulsory HBM bytes per lattice cell per fused block of b levels (paper_1410_3060_b200.model)."""
+    from paper_1410_3060_b200 import model
+    return model.code_balance(kind, b) * b
 
 
 def blocks_of(T, bt):
@@ -53,7 +53,7 @@ def blocks_of(T, bt):
     return out
 
 
-FLOPS_PER_LUP = {synth.K7C: 8, synth.K7V: 13, synth.K25W: 30, synth.K25V: 37, synth.K25WA: 30}
+from paper_1410_3060_b200.model import FLOPS_PER_LUP  # noqa: E402
 
 
 def load_peaks():
