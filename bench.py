@@ -85,11 +85,22 @@ class ClockSampler:
         except Exception:
             self.nv = None
 
+    def _power_w(self):
+        # Instantaneous board power (NVML_FI_DEV_POWER_INSTANT, mW).  nvmlDeviceGetPowerUsage is a 1-s
+        # moving average: it lags a sub-second timed region and under-reads the 1 kW cap.
+        try:
+            v = self.nv.nvmlDeviceGetFieldValues(self.h, [self.nv.NVML_FI_DEV_POWER_INSTANT])[0]
+            if v.nvmlReturn == 0:
+                return v.value.uiVal / 1000.0
+        except Exception:
+            pass
+        return self.nv.nvmlDeviceGetPowerUsage(self.h) / 1000.0
+
     def _run(self):
         while not self._stop.is_set():
             try:
                 self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
-                self.power.append(self.nv.nvmlDeviceGetPowerUsage(self.h) / 1000.0)
+                self.power.append(self._power_w())
                 r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
                 for bit, name in self.REASONS.items():
                     if r & bit and name != "gpu_idle":
