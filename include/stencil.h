@@ -131,7 +131,7 @@ typedef struct {
 
 typedef struct {
   int kind, R, bt, variant, rank, nranks, local_slabs;
-  int tile_x, tile_y, zchunk;     /* output tile of the last launch; z planes per work item */
+  int tile_x, tile_y, zchunk;     /* output tile of the bt-deep launches; z planes per work item */
   int64_t nx, ny, nz;             /* global interior extents */
   int64_t own_z0, own_z1;         /* padded planes [own_z0, own_z1) this handle owns (global index) */
   int64_t pitch, plane;           /* device row pitch and plane stride, in doubles */

@@ -49,6 +49,9 @@ struct KParams {
   double* rdstu[2];
   int rz0[2], rz1[2];
   int rfence;
+  int tband;   // pipe kernel, single-block launches: tile order within a z-chunk (STENCIL_TILE_BAND;
+               // 0 = row-major, w > 0 = bands of w tile columns walked row by row, so y-neighbours are w
+               // ids apart instead of ntx)
   int walign;  // pipe kernel: tiles write sector-aligned output segments (STENCIL_WALIGN=1; default 0:
                // measured slower under the power cap for OX % 4 != 0, profiles/r01_summary.md)
 };

@@ -178,7 +178,15 @@ __device__ __forceinline__ Item decode(int item, int ntx, int nty, const KParams
   // multi-block launches order a block's items tile-major (the chunks of a tile consecutively), so the
   // items an item of the next block depends on come early; otherwise z-chunk-major
   const int zc = p.nblk > 1 ? item % p.nzc : item / per, t = p.nblk > 1 ? item / p.nzc : item - zc * per;
-  const int ty = t / ntx, tx = t - ty * ntx;
+  int ty, tx;
+  if (p.tband > 0 && p.nblk <= 1) {
+    const int w = p.tband, band = t / (w * nty), r = t - band * w * nty, wb = min(w, ntx - band * w);
+    ty = r / wb;
+    tx = band * w + (r - ty * wb);
+  } else {
+    ty = t / ntx;
+    tx = t - ty * ntx;
+  }
   Item it;
   it.gx0 = R + tx * OXW - WOFF - R * H - dx;
   it.gy0 = ty * OY + R - R * H;

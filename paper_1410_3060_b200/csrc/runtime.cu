@@ -530,6 +530,7 @@ st::KParams base_params(stencil_ctx* h, const Slab& s) {
   p.dbg = env_int("STENCIL_DBG") | (env_int("STENCIL_FAULT") & 12);
   static const int walign = getenv("STENCIL_WALIGN") ? atoi(getenv("STENCIL_WALIGN")) : 0;
   p.walign = walign;
+  p.tband = getenv("STENCIL_TILE_BAND") ? atoi(getenv("STENCIL_TILE_BAND")) : 0;
   p.nblk = 1;
   return p;
 }
@@ -644,14 +645,17 @@ int launch_range(stencil_ctx* h, Slab& s, int b, int d0, int d1, int64_t z0, int
   cudaEvent_t ev_end = nullptr;
   cudaEvent_t ev_begin = timing_begin(h, &ev_end);
   cudaError_t e;
+  st::LaunchInfo li{};
   if (h->variant == ST_VARIANT_NAIVE)
-    e = st::launch_naive(h->kind, p, h->stream, &h->last_launch);
+    e = st::launch_naive(h->kind, p, h->stream, &li);
   else if (h->variant == ST_VARIANT_STREAM)
-    e = st::launch_stream(h->kind, b, p, h->zchunk_req, h->num_sms, h->stream, &h->last_launch);
+    e = st::launch_stream(h->kind, b, p, h->zchunk_req, h->num_sms, h->stream, &li);
   else
-    e = st::launch_pipe(h->kind, b, p, h->zchunk_req, h->num_sms, h->tile_cfg, h->stream, &h->last_launch);
+    e = st::launch_pipe(h->kind, b, p, h->zchunk_req, h->num_sms, h->tile_cfg, h->stream, &li);
   if (ev_begin) cudaEventRecord(ev_end, h->stream);
   if (e != cudaSuccess) return cuda_fail(h, e, "kernel launch");
+  // st_info reports the plan's full-depth launches; a remainder block's plan only until one has run
+  if (b == h->bt || h->last_launch.tile_x == 0) h->last_launch = li;
   h->launches++;
   return ST_OK;
 }
