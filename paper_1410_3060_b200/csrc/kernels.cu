@@ -151,8 +151,167 @@ cudaError_t run_coop(const KParams& p0, int T, int num_sms, cudaStream_t stream,
   return e;
 }
 
-cudaError_t launch_coop(int kind, const KParams& p, int T, int num_sms, cudaStream_t stream, LaunchInfo* info) {
-  if (p.zo1 <= p.zo0 || T <= 0) return cudaSuccess;
+// ------------------------------------------------------------------------------------------------
+// coop_tb: the cooperative kernel with temporal blocking in shared memory (7-point Jacobi kinds).
+// Every CTA owns an output block of BX x BY x BZ interior cells; per ROUND it loads the block grown by
+// H = R*BTL cells on every side (from L2: the grids this runs on are L2-resident) into shared memory,
+// runs L <= BTL levels there -- level k updates the region shrunk by k*R, so the block's own cells are
+// exact after L levels (the overlapped-tile trapezoid of P:600-612, in all three dimensions) -- and
+// writes the block back; one grid-wide barrier per round instead of one per sweep.  Cells that are not
+// interior keep their (fixed ghost) value at every level; cells beyond the padded extent are loaded as
+// 0 and only ever feed ghost cells, whose value is not computed.  Same point function, same operands
+// as naive_kernel: bitwise equal (test G4).  Buffers alternate per round (`swaps` = rounds).
+template <int KIND, int BX, int BY, int BZ, int BTL>
+struct TbCfg {
+  static constexpr int R = Traits<KIND>::R, H = R * BTL;
+  static constexpr int SX = BX + 2 * H, SY = BY + 2 * H, SZ = BZ + 2 * H, N = SX * SY * SZ;
+  static constexpr int THREADS = 1024;
+  static constexpr size_t SMEM = 2 * sizeof(double) * (size_t)N;
+  static_assert(SX <= 32 && SY <= THREADS / 32, "warp = one y row of the grown block, lane = x");
+  static_assert(SMEM <= 227 * 1024, "two grown blocks must fit in shared memory");
+};
+
+// One level of a round: warp w updates y row lo + w of the region shrunk by lo = k*R, lane = x, walking z
+// (the column's centre and z-neighbours rotate through registers: 5 shared loads per 7-point update).
+template <int KIND, int SX, int SY, int SZ>
+__device__ __forceinline__ void tb_level(const double* __restrict__ A, double* __restrict__ B, int lo, int ox,
+                                         int oy, int oz, const KParams& p, int warp, int lane) {
+  constexpr int R = Traits<KIND>::R, NC = Traits<KIND>::NCOEF, SXY = SX * SY;
+  static_assert(R == 1, "7-point kinds");
+  const int sy = lo + warp, sx = lo + lane;
+  if (sy >= SY - lo || sx >= SX - lo) return;
+  const int gy = oy + sy, gx = ox + sx;
+  const bool xyint = gy >= R && gy < p.ny + R && gx >= R && gx < p.nx + R;
+  int i = (lo * SY + sy) * SX + sx;
+  double zm = A[i - SXY], zc = A[i];
+  const long long g0 = (long long)gy * p.pitch + gx;
+#pragma unroll 4
+  for (int sz = lo; sz < SZ - lo; ++sz, i += SXY) {
+    const double zp = A[i + SXY];
+    const double m[3][1] = {{A[i - 1]}, {A[i - SX]}, {zm}}, pl[3][1] = {{A[i + 1]}, {A[i + SX]}, {zp}};
+    const int gz = oz + sz;
+    const bool upd = xyint && gz >= p.zi0 && gz < p.zi1;
+    double W[NC > 0 ? NC : 1];
+    const long long gi = upd ? (long long)gz * p.plane + g0 : 0;
+#pragma unroll
+    for (int f = 0; f < NC; ++f) W[f] = __ldg(p.coef + f * p.cstride + gi);
+    B[i] = upd ? apply_point<KIND, R>(zc, 0.0, m, pl, W, p.s) : zc;
+    zm = zc;
+    zc = zp;
+  }
+}
+
+template <int KIND, int BX, int BY, int BZ, int BTL>
+__global__ void __launch_bounds__(1024, 1) coop_tb_kernel(KParams p, int T) {
+  using C = TbCfg<KIND, BX, BY, BZ, BTL>;
+  constexpr int R = C::R, H = C::H, SX = C::SX, SY = C::SY, SZ = C::SZ, SXY = SX * SY;
+  static_assert(!Traits<KIND>::WAVE, "Jacobi kinds");
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(16) double tb_smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nzi = p.zi1 - p.zi0;
+  const int nbx = (p.nx + BX - 1) / BX, nby = (p.ny + BY - 1) / BY, nbz = (nzi + BZ - 1) / BZ;
+  const int nblocks = nbx * nby * nbz;
+  const int GX = p.nx + 2 * R, GY = p.ny + 2 * R;
+  const double* src = p.src;
+  double* dst = p.dst;
+  for (int t = 0; t < T; t += BTL) {
+    const int L = min(BTL, T - t);
+    for (int b = blockIdx.x; b < nblocks; b += gridDim.x) {
+      const int bz = b / (nbx * nby), byx = b - bz * nbx * nby, by = byx / nbx, bx = byx - by * nbx;
+      // padded coordinates of grown-block cell (0, 0, 0): x, y global; z local plane
+      const int ox = R + bx * BX - H, oy = R + by * BY - H, oz = p.zi0 + bz * BZ - H;
+      // grown block -> shared memory with asynchronous copies (cp.async, zero-filled outside the padded
+      // extent): all of a warp's rows are in flight at once
+      if (warp < SY && lane < SX) {
+        const int gy = oy + warp, gx = ox + lane;
+        const bool xyok = gy >= 0 && gy < GY && gx >= 0 && gx < GX;
+        for (int sz = 0; sz < SZ; ++sz) {
+          const int gz = oz + sz;
+          const bool ok = xyok && gz >= 0 && gz < p.zl;
+          const double* g = ok ? src + ((long long)gz * p.plane + (long long)gy * p.pitch + gx) : src;
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(
+                           static_cast<uint32_t>(__cvta_generic_to_shared(tb_smem + sz * SXY + warp * SX + lane))),
+                       "l"(g), "r"(ok ? 8 : 0)
+                       : "memory");
+        }
+      }
+      asm volatile("cp.async.wait_all;" ::: "memory");
+      __syncthreads();
+      double* A = tb_smem;
+      double* B = tb_smem + C::N;
+#pragma unroll 1
+      for (int k = 1; k <= L; ++k) {
+        tb_level<KIND, SX, SY, SZ>(A, B, k * R, ox, oy, oz, p, warp, lane);
+        __syncthreads();
+        double* tmp = A;
+        A = B;
+        B = tmp;
+      }
+      if (warp < BY && lane < BX) {
+        const int sy = H + warp, gy = oy + sy, gx = ox + H + lane;
+        if (gy < p.ny + R && gx < p.nx + R)
+          for (int sz = H; sz < H + BZ && oz + sz < p.zi1; ++sz)
+            dst[(long long)(oz + sz) * p.plane + (long long)gy * p.pitch + gx] = A[sz * SXY + sy * SX + H + lane];
+      }
+      __syncthreads();  // the next block's load overwrites this one's shared memory
+    }
+    grid.sync();
+    double* tmp = const_cast<double*>(src);
+    src = dst;
+    dst = tmp;
+  }
+}
+
+template <int KIND, int BX, int BY, int BZ, int BTL>
+cudaError_t run_coop_tb(const KParams& p0, int T, int num_sms, cudaStream_t stream, LaunchInfo* info, int* swaps) {
+  using C = TbCfg<KIND, BX, BY, BZ, BTL>;
+  auto kern = coop_tb_kernel<KIND, BX, BY, BZ, BTL>;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  static int occ = 0;  // per instantiation; the device's SM layout does not change
+  if (occ < 1 && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, C::THREADS, C::SMEM) != cudaSuccess || occ < 1))
+    return cudaErrorCooperativeLaunchTooLarge;
+  const long long nblocks = (long long)((p0.nx + BX - 1) / BX) * ((p0.ny + BY - 1) / BY) *
+                            ((p0.zi1 - p0.zi0 + BZ - 1) / BZ);
+  const int grid = (int)std::min<long long>(nblocks, (long long)occ * num_sms);
+  KParams p = p0;
+  int Tv = T;
+  void* args[] = {(void*)&p, (void*)&Tv};
+  cudaError_t e = cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(C::THREADS), args, C::SMEM, stream);
+  if (info) {
+    info->tile_x = BX; info->tile_y = BY; info->zchunk = BZ;
+    info->threads = C::THREADS; info->smem = (int)C::SMEM; info->ctas = grid;
+  }
+  if (swaps) *swaps = (T + BTL - 1) / BTL;
+  return e;
+}
+
+// Output blocks of the temporally blocked cooperative kernel: (16, 16, 8) cells, 5 levels per round
+// (grown block 26 x 26 x 18, 195 KB for the two copies).  Measured (tools/coop_sweep.py, B200): C1 7c
+// 64^3 T = 10 37.9 us vs 36.3 us for one sweep per barrier -- the 2.5x redundant level work of the
+// grown blocks costs what the 8 saved grid barriers gain; 15 % faster on one-block grids (8^3, T = 50);
+// 7v 1.7x slower (its coefficients come from L2 at every level).  Not the default (tile_cfg 2).
+constexpr int kTbBX = 16, kTbBY = 16, kTbBZ = 8, kTbBT = 5;
+
+cudaError_t launch_coop(int kind, const KParams& p, int T, int num_sms, int cfg, cudaStream_t stream, LaunchInfo* info,
+                        int* swaps) {
+  if (swaps) *swaps = T;
+  if (p.zo1 <= p.zo0 || T <= 0) {
+    if (swaps) *swaps = 0;
+    return cudaSuccess;
+  }
+  // cfg 0 / 1: one sweep per grid barrier; cfg 2: temporal blocking in shared memory (7-point Jacobi kinds)
+  if (cfg == 2) {
+    if (kind == K7C) return run_coop_tb<K7C, kTbBX, kTbBY, kTbBZ, kTbBT>(p, T, num_sms, stream, info, swaps);
+    if (kind == K7V) return run_coop_tb<K7V, kTbBX, kTbBY, kTbBZ, kTbBT>(p, T, num_sms, stream, info, swaps);
+    return cudaErrorInvalidValue;
+  }
   switch (kind) {
     case K7C: return run_coop<K7C>(p, T, num_sms, stream, info);
     case K7V: return run_coop<K7V>(p, T, num_sms, stream, info);

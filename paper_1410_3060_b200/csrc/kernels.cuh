@@ -84,7 +84,11 @@ int max_pipe_bt(int kind);
 
 // T time steps of the whole slab in ONE cooperative launch with a grid-wide barrier between sweeps
 // (ST_VARIANT_COOP, small latency-bound grids).  p.src = Omega^t, p.dst = p.srcu = the other buffer.
-cudaError_t launch_coop(int kind, const KParams& p, int T, int num_sms, cudaStream_t stream, LaunchInfo* info);
+// cfg 0 / 1 = one sweep per grid barrier; 2 = temporal blocking in shared memory, one grid barrier per
+// round of 5 levels (7-point Jacobi kinds; measured no faster at C1, kernels.cu).
+// *swaps = how many times the two state buffers swapped roles (T, or the number of rounds).
+cudaError_t launch_coop(int kind, const KParams& p, int T, int num_sms, int cfg, cudaStream_t stream, LaunchInfo* info,
+                        int* swaps);
 
 // Seeded fill of the local planes of one array (synth/synth.h).  mode 0: U[-1,1) from `stream`
 // everywhere; mode 1: U[-1,1), interior cells from stream 1 and the rest from stream 0 (wave

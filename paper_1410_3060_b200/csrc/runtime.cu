@@ -989,12 +989,13 @@ int stencil_run(stencil_ctx* h, int64_t T) {
     p.dst = h->at(s, h->lv1);
     cudaEvent_t ev_end = nullptr;
     cudaEvent_t ev_begin = timing_begin(h, &ev_end);
-    const cudaError_t le = st::launch_coop(h->kind, p, (int)std::min<int64_t>(T, 1 << 30), h->num_sms, h->stream,
-                                           &h->last_launch);
+    int swaps = 0;
+    const cudaError_t le = st::launch_coop(h->kind, p, (int)std::min<int64_t>(T, 1 << 30), h->num_sms, h->tile_cfg,
+                                           h->stream, &h->last_launch, &swaps);
     if (ev_begin) cudaEventRecord(ev_end, h->stream);
     if (le != cudaSuccess) return cuda_fail(h, le, "cooperative launch");
     h->launches++;
-    if (T & 1) std::swap(h->lv0, h->lv1);
+    if (swaps & 1) std::swap(h->lv0, h->lv1);
     h->steps += T;
     h->blocks += T;
     return ST_OK;

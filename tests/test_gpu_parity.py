@@ -102,7 +102,11 @@ def test_variants_bitwise_identical(kind):
              for zc in (0, 5, 1000)]
     plans += [(st.ST_VARIANT_PIPE, bt, zc, cfg) for bt in range(1, max_bt(kind) + 1) for zc in (0, 5, 1000)
               for cfg in range(N_CFG[kind])]
-    plans += [(st.ST_VARIANT_COOP, 1, 0, 0)]  # all T steps in one cooperative launch
+    # all T steps in one cooperative launch: one sweep per grid barrier; 7-point Jacobi kinds also with
+    # temporal blocking in shared memory (rounds of 5 + 2 levels)
+    plans += [(st.ST_VARIANT_COOP, 1, 0, 0)]
+    if kind in (synth.K7C, synth.K7V):
+        plans += [(st.ST_VARIANT_COOP, 1, 0, 2)]
     for variant, bt, zchunk, cfg in plans:
         got = gpu_run(kind, nx, ny, nz, T, seed=9, variant=variant, bt=bt, zchunk=zchunk, tile_cfg=cfg)
         assert got[2]["bt"] == bt
@@ -121,11 +125,25 @@ def test_degenerate_extents(kind):
         inp = synth.make_inputs(kind, nx, ny, nz, seed=4)
         T = 5
         o_new, o_old = oracle.run(inp, T)
-        for variant, bt in sorted({(st.ST_VARIANT_PIPE, 1), (st.ST_VARIANT_PIPE, max_bt(kind)),
-                                   (st.ST_VARIANT_STREAM, max_bt(kind, st.ST_VARIANT_STREAM)),
-                                   (st.ST_VARIANT_COOP, 1)}):
-            g_new, g_old, _ = gpu_run(kind, nx, ny, nz, T, seed=4, bt=bt, variant=variant)
+        for variant, bt, cfg in sorted({(st.ST_VARIANT_PIPE, 1, 0), (st.ST_VARIANT_PIPE, max_bt(kind), 0),
+                                        (st.ST_VARIANT_STREAM, max_bt(kind, st.ST_VARIANT_STREAM), 0),
+                                        (st.ST_VARIANT_COOP, 1, 0)} |
+                                       ({(st.ST_VARIANT_COOP, 1, 2)} if kind in (synth.K7C, synth.K7V) else set())):
+            g_new, g_old, _ = gpu_run(kind, nx, ny, nz, T, seed=4, bt=bt, variant=variant, tile_cfg=cfg)
             assert_parity(kind, g_new, g_old, o_new, o_old, inp.R, 1e-13, inputs=inp)
+
+
+@pytest.mark.parametrize("kind", [synth.K7C, synth.K7V])
+@pytest.mark.parametrize("T", [1, 5, 12])
+def test_coop_temporal_blocking_bitwise(kind, T):
+    """G4 for the temporally blocked cooperative kernel (tile_cfg 2 forces it) on a grid with more
+    output blocks (16 x 16 x 8) than SMs, so each CTA runs several blocks per round, ragged in every
+    axis; rounds of 5 levels with a remainder round (T = 12)."""
+    nx, ny, nz = 100, 90, 50
+    ref = gpu_run(kind, nx, ny, nz, T, seed=21, variant=st.ST_VARIANT_NAIVE)
+    got = gpu_run(kind, nx, ny, nz, T, seed=21, variant=st.ST_VARIANT_COOP, tile_cfg=2)
+    assert got[2]["tile_x"] == 16 and got[2]["zchunk"] == 8
+    assert np.array_equal(got[0], ref[0])
 
 
 def test_repeatable_bitwise():
