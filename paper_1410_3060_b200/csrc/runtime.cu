@@ -491,6 +491,7 @@ cudaError_t upload_planes(stencil_ctx* h, const Slab& s, double* raw, const doub
 
 // Staging buffer for upload_planes (released with release_stage; stream-ordered reuse is safe).
 double* acquire_stage(stencil_ctx* h) {
+  if (env_int("STENCIL_NO_STAGE")) return nullptr;  // experiment knob: direct pitched host copies
   const size_t bytes = (size_t)(kStagePlanes * h->X * h->Y) * sizeof(double);
   void* p = nullptr;
   if (h->alloc) p = h->alloc(bytes, (void*)h->stream, h->alloc_user);
