@@ -448,6 +448,9 @@ def main():
         cpu.pop("seconds", None)
 
     if rank == 0:
+        clocks = clk.summary()
+        if clocks.get("power_w"):  # board energy per lattice update on this GPU (cf. the paper's Table 1)
+            clocks["energy_nj_per_lup"] = round(clocks["power_w"] / (value / world), 3)
         line = {
             "metric": METRIC, "value": value, "unit": METRIC, "n_gpus": n, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
@@ -468,7 +471,7 @@ def main():
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,
-            "clocks": clk.summary(),
+            "clocks": clocks,
         }
         print(json.dumps(line))
     if world > 1:
