@@ -289,19 +289,10 @@ def main():
         if world > 1 and halo == st.ST_HALO_PEER:
             # wire the neighbours' memory (CUDA IPC); if any rank cannot, every rank falls back to the
             # NCCL halo exchange together (a half-wired job would wait forever on a flag)
-            ok = 1
-            try:
-                descs = st.exchange_peer_descriptors(g.peer_export())
-                g.peer_import(*st.peer_neighbours(descs, rank))
-                g.peer_handshake(timeout_ms=20000)  # peer stores + flag writes really arrive
-            except st.StencilError as e:
-                ok, halo_note = 0, f"peer wiring failed on rank {rank}: {e}"
-            flag = torch.tensor([ok], dtype=torch.int32, device=dev)
-            dist.all_reduce(flag, op=dist.ReduceOp.MIN)
-            if not int(flag.item()):
+            ok, halo_note = g.wire_peers(timeout_ms=20000)
+            if not ok:
                 g.close()
                 halo, args.halo = st.ST_HALO_COPY, "copy"
-                halo_note = halo_note or "peer wiring failed on another rank"
                 g = st.Grid(w.kind, w.nx, w.ny, w.nz, seed=synth.DEFAULT_SEED, variant=args.variant,
                             bt=args.bt, zchunk=args.zchunk, rank=rank, nranks=world, nccl_id=nccl_id)
     stream = g.stream

@@ -259,6 +259,35 @@ def exchange_peer_descriptors(desc: bytes, group=None):
     return out
 
 
+def wire_peer_halos(export, import_, handshake, rank, timeout_ms=20000, group=None):
+    """Wire ST_HALO_PEER across processes, safely for a collective: every rank takes part in both
+    all-gathers whatever fails locally (a rank that skipped one would leave the others waiting), and
+    all ranks return the same verdict -- (True, None) only if every rank exported, imported and passed
+    the handshake; else (False, the first failure's message).  export() -> bytes, import_(below,
+    above) and handshake(timeout_ms) are the handle's operations (Grid.peer_*)."""
+    import torch.distributed as dist
+    note = None
+    desc = None
+    try:
+        desc = export()
+    except StencilError as e:
+        note = f"peer export failed on rank {rank}: {e}"
+    descs = exchange_peer_descriptors(desc, group)
+    if note is None and any(d is None for d in descs):
+        note = "peer export failed on another rank"
+    if note is None:
+        try:
+            import_(*peer_neighbours(descs, rank))
+            handshake(timeout_ms)  # the neighbours' peer stores and flag writes really arrive
+        except StencilError as e:
+            note = f"peer wiring failed on rank {rank}: {e}"
+    notes = [None] * dist.get_world_size(group)
+    dist.all_gather_object(notes, note, group=group)
+    # the verdict names the rank where wiring first failed (not a rank that only saw the consequence)
+    bad = sorted((n for n in notes if n is not None), key=lambda n: "another rank" in n)
+    return (not bad), (bad[0] if bad else None)
+
+
 def stencil_plan_slab(nz, R, nranks, rank, bt):
     a, b, c, d = (ctypes.c_int64() for _ in range(4))
     e = ctypes.c_int()
@@ -352,9 +381,11 @@ class Grid:
         self._ipc = halo == ST_HALO_PEER and nranks > 1 and local_slabs == 1
         self._wired = wire_peers
         if self._ipc and wire_peers:  # fused halo exchange across processes: wire the neighbours' memory
-            descs = exchange_peer_descriptors(stencil_peer_export(self.h))
-            stencil_peer_import(self.h, *peer_neighbours(descs, rank))
-            stencil_peer_handshake(self.h)
+            ok, note = self.wire_peers()
+            if not ok:
+                stencil_destroy(self.h)
+                self.h = None
+                raise StencilError(ST_E_STATE, note)
 
     @property
     def padded_shape(self):
@@ -384,6 +415,12 @@ class Grid:
 
     def peer_handshake(self, timeout_ms=10000):
         stencil_peer_handshake(self.h, timeout_ms)
+
+    def wire_peers(self, timeout_ms=20000, group=None):
+        """Collective: wire the z-neighbours' memory (ST_HALO_PEER across processes); returns the
+        verdict every rank agrees on, (ok, first failure's message)."""
+        return wire_peer_halos(self.peer_export, self.peer_import, self.peer_handshake, self.rank,
+                               timeout_ms, group)
 
     def write(self, level, arr):
         if self._ipc and self._wired:  # neighbours store into this rank's halos: write between two barriers

@@ -25,7 +25,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, out_dir):
+def _worker(rank, world, port, out_dir, mode):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -34,11 +34,14 @@ def _worker(rank, world, port, out_dir):
         import paper_1410_3060_b200 as st
         import synth
         torch.cuda.set_device(0)
-        g = st.Grid(synth.K7V, 24, 20, 16, seed=3, rank=rank, nranks=world, halo=st.ST_HALO_PEER,
-                    wire_peers=False)
-        descs = st.exchange_peer_descriptors(g.peer_export())
-        g.peer_import(*st.peer_neighbours(descs, rank))
-        g.peer_handshake(timeout_ms=20000)
+        if mode == "grid":  # Grid wires itself: export, all-gather, import, handshake, agreed verdict
+            g = st.Grid(synth.K7V, 24, 20, 16, seed=3, rank=rank, nranks=world, halo=st.ST_HALO_PEER)
+        else:  # the same steps by hand
+            g = st.Grid(synth.K7V, 24, 20, 16, seed=3, rank=rank, nranks=world, halo=st.ST_HALO_PEER,
+                        wire_peers=False)
+            descs = st.exchange_peer_descriptors(g.peer_export())
+            g.peer_import(*st.peer_neighbours(descs, rank))
+            g.peer_handshake(timeout_ms=20000)
         info = g.info()
         dist.barrier()
         g.close()  # no block was run: nothing to wait for
@@ -51,9 +54,9 @@ def _worker(rank, world, port, out_dir):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_ipc_wiring_and_handshake_two_processes(tmp_path, world):
+@pytest.mark.parametrize("world,mode", [(2, "manual"), (3, "manual"), (2, "grid"), (3, "grid")])
+def test_ipc_wiring_and_handshake_two_processes(tmp_path, world, mode):
     port = _free_port()
-    mp.spawn(_worker, args=(world, port, str(tmp_path)), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, port, str(tmp_path), mode), nprocs=world, join=True)
     res = [open(tmp_path / f"r{r}.txt").read() for r in range(world)]
     assert all(r.startswith("ok halo=1") for r in res), res

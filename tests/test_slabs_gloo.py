@@ -127,3 +127,50 @@ def test_peer_descriptor_exchange_gloo(tmp_path, world):
         below, above, n, size = np.load(tmp_path / f"d{r}.npy")
         assert below == (r - 1 if r > 0 else -1) and above == (r + 1 if r < world - 1 else -1)
         assert n == world and size == st.ST_PEER_DESC_BYTES
+
+
+def _wire_worker(rank, world, port, fail, out_dir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    calls = []
+    try:
+        def export():
+            if fail == ("export", rank):
+                raise st.StencilError(st.ST_E_CUDA, "injected export failure")
+            return bytes([rank]) * st.ST_PEER_DESC_BYTES
+
+        def import_(below, above):
+            calls.append("import")
+            if fail == ("import", rank):
+                raise st.StencilError(st.ST_E_CUDA, "injected import failure")
+
+        def handshake(timeout_ms):
+            calls.append("handshake")
+        ok, note = st.wire_peer_halos(export, import_, handshake, rank, timeout_ms=100)
+        with open(os.path.join(out_dir, f"w{rank}.txt"), "w") as f:
+            f.write(f"{int(ok)}|{note}|{','.join(calls)}")
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("fail", [None, ("export", 1), ("import", 0), ("export", 2)])
+def test_peer_wiring_failure_is_agreed_gloo(tmp_path, fail):
+    """ST_HALO_PEER wiring is collective-safe: when one rank's export or import fails, every rank still
+    takes part in every collective (no hang) and all ranks return the same verdict, so bench.py can
+    fall back to the NCCL halo exchange on all ranks together."""
+    world = 3
+    port = _free_port()
+    mp.spawn(_wire_worker, args=(world, port, fail, str(tmp_path)), nprocs=world, join=True)
+    res = [open(tmp_path / f"w{r}.txt").read().split("|") for r in range(world)]
+    oks = {r[0] for r in res}
+    notes = {r[1] for r in res}
+    assert len(oks) == 1 and len(notes) == 1  # one verdict, one message, on every rank
+    if fail is None:
+        assert oks == {"1"} and notes == {"None"}
+        assert all(r[2] == "import,handshake" for r in res)
+    else:
+        assert oks == {"0"}
+        assert f"rank {fail[1]}" in next(iter(notes))
+        if fail[0] == "export":  # nobody imports when a descriptor is missing
+            assert all(r[2] == "" for r in res)
