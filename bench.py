@@ -246,6 +246,8 @@ def main():
                          "loopback) overlapped with the interior kernel; peer = fused into the kernel, "
                          "which stores the neighbours' halo planes straight into their memory (CUDA IPC "
                          "over NVLink across processes)")
+    ap.add_argument("--alt-bt", type=int, default=-1,
+                    help="also time the plan at this time-block depth (-1: the default bt + 1; 0: off)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -360,6 +362,35 @@ def main():
     del g
     torch.cuda.empty_cache()
 
+    # Alternative plan at a deeper time block (single GPU, default plan only): its measured rate next to
+    # its own (higher) roofline, so a reader sees both sides of the b_t choice
+    alt = None
+    alt_bt = args.alt_bt if args.alt_bt >= 0 else (bt + 1 if args.bt == 0 else 0)
+    if world == 1 and slabs == 1 and alt_bt > bt:
+        try:
+            ga = st.Grid(w.kind, w.nx, w.ny, w.nz, seed=synth.DEFAULT_SEED, variant=args.variant, bt=alt_bt)
+        except st.StencilError:
+            ga = None
+        if ga is not None and ga.info()["bt"] == alt_bt:
+            ga.run(w.T)
+            ga.sync()
+            ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with ClockSampler(local) as clk_a:
+                ea.record(ga.stream)
+                for _ in range(args.steps):
+                    ga.run(w.T)
+                eb.record(ga.stream)
+                eb.synchronize()
+            va = w.nx * w.ny * w.nz * w.T * args.steps / (ea.elapsed_time(eb) / 1e3) / 1e9
+            roof_a = min(peak / (block_bytes_per_cell(w.kind, alt_bt) / alt_bt), fp64 * 1e3 / FLOPS_PER_LUP[w.kind])
+            ia = ga.info()
+            alt = {"bt": alt_bt, "value": va, "roof_glups_bt": roof_a, "frac": va / roof_a,
+                   "tile": [ia["tile_x"], ia["tile_y"]], "sm_mhz": clk_a.summary().get("sm_mhz"),
+                   "note": "same workload, next deeper time block; not the headline plan"}
+        if ga is not None:
+            ga.close()
+        torch.cuda.empty_cache()
+
     # e2e: through the public API with HOST buffers: create from pinned host inputs (H2D), run T,
     # read the newest level (D2H), every step.
     e2e = None
@@ -459,6 +490,7 @@ def main():
                        "l2": "inputs larger than L2 (no flush needed)",
                        "luops_per_step": w.nx * w.ny * w.nz * w.T},
             "roofline": roofline,
+            "alt_plan": alt,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,

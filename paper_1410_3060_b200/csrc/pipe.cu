@@ -1055,11 +1055,12 @@ cudaError_t launch_pipe(int kind, int b, const KParams& p, int zchunk_req, int n
           // TMEM coefficient window for levels 2..3 (WIN = -1): C2 bt=3 163-168 -> 184-192 GLUP/s
           CFGU(K7V, 3, 32, 28, 2, 2, 4, 3, -1, 1);
         case 4:  // TMEM coefficient window only (the ring would need (bt-1)*R more slots otherwise)
-          if (cfg == 1) CFGU(K7V, 4, 32, 28, 2, 2, 4, 2, -1, 1);
+          if (cfg == 1) CFGU(K7V, 4, 32, 24, 2, 2, 4, 3, -1, 1);  // session-2 default
           if (cfg == 2) CFG(K7V, 4, 32, 24, 2, 2, 4, 3, -1, 1);
           if (cfg == 3) CFGC(K7V, 4, 32, 24, 2, 2, 4, 3, -1, 1);  // cluster pair: 32 x 48 tile
           if (cfg == 4) CFGC(K7V, 4, 32, 28, 2, 2, 4, 2, -1, 1);  // cluster pair: 32 x 56 tile
-          CFGU(K7V, 4, 32, 24, 2, 2, 4, 3, -1, 1);
+          // 7 consumer warps, 2-slot coefficient ring (lookahead 1): 199 -> 202 GLUP/s (session 3)
+          CFGU(K7V, 4, 32, 28, 2, 2, 4, 2, -1, 1);
       }
       break;
     case K25W:
