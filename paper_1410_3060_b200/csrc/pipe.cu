@@ -979,7 +979,7 @@ cudaError_t run_pipe(const KParams& p0, int zchunk_req, int num_sms, cudaStream_
     if (e != cudaSuccess) return e;
   }
   if (info) {
-    info->tile_x = C::OXW; info->tile_y = C::OYP; info->zchunk = zchunk; info->threads = C::THREADS;
+    info->tile_x = oxw; info->tile_y = C::OYP; info->zchunk = zchunk; info->threads = C::THREADS;
     info->smem = (int)C::SMEM; info->ctas = grid;
   }
   return cudaGetLastError();
