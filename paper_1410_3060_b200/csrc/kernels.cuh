@@ -28,8 +28,9 @@ struct KParams {
   const double* srcu_raw;
   const double* coef_raw;
   int xoff;
-  int dbg;     // experiment knob (STENCIL_DBG): bit 0 = skip all compute in the pipe kernel, bit 1 =
-               // skip level barriers; fault injection for the mutation tests (STENCIL_FAULT):
+  int dbg;     // experiment knob (STENCIL_DBG): bit 0 = discard every level's results in the pipe
+               // kernel (the straight-line arithmetic still runs: results are wrong), bit 1 = skip level
+               // barriers; fault injection for the mutation tests (STENCIL_FAULT):
                // bit 2 = never write the last plane of a z-chunk, bit 3 = skip work item 0
   unsigned int* sched;  // pipe kernel: 2 zeroed device counters (next work item, CTAs done)
   // Pipe kernel, several fused blocks in ONE launch (Jacobi kinds, single slab): nblk blocks; block i
