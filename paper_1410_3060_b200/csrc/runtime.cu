@@ -464,46 +464,95 @@ int create_common(stencil_ctx** out, int kind, int64_t nx, int64_t ny, int64_t n
 }
 
 // Copy dense padded global host planes [store_z0, store_z1) of slab s into its device buffer raw.
-// Staged: chunks of planes go host -> a dense device staging buffer in one contiguous copy each, then
-// a device-to-device pitched copy into the library layout (a pitched cudaMemcpy2D straight from host
-// memory ran at ~31 GB/s on B200, a contiguous copy at ~55 GB/s, the device-side 2-D copy at ~3.4 TB/s;
-// tools/pcie_probe.py).  Both copies run on copy engines, so an upload overlaps running kernels.
-// Without a staging buffer (allocation failed) the direct 2-D copy is used.
+// Staged: chunks of planes go host -> a dense device staging slot in one contiguous copy each (55 GB/s,
+// the PCIe peak), then a device-to-device pitched copy into the library layout (a pitched cudaMemcpy2D
+// straight from host memory ran at ~31 GB/s on B200; tools/pcie_probe.py).  Two slots: the repack of
+// chunk i runs on an auxiliary stream while chunk i+1 crosses PCIe (on a busy GPU the repack competes
+// with the kernels for HBM and would otherwise stall the upload).  Without staging memory (allocation
+// failed, or STENCIL_NO_STAGE) the direct 2-D copy is used.
 constexpr int64_t kStagePlanes = 32;
-cudaError_t upload_planes(stencil_ctx* h, const Slab& s, double* raw, const double* host,
-                          double* stage = nullptr) {
-  const double* src = host + (size_t)s.store_z0 * h->X * h->Y;
-  if (!stage)
-    return cudaMemcpy2DAsync(raw + h->xoff, h->pitch * sizeof(double), src, h->X * sizeof(double),
-                             h->X * sizeof(double), (size_t)h->Y * s.zl, cudaMemcpyHostToDevice, h->stream);
-  const int64_t hplane = h->X * h->Y;
-  for (int64_t z0 = 0; z0 < s.zl; z0 += kStagePlanes) {
-    const int64_t nz = std::min<int64_t>(kStagePlanes, s.zl - z0);
-    cudaError_t e = cudaMemcpyAsync(stage, src + z0 * hplane, (size_t)(nz * hplane) * sizeof(double),
-                                    cudaMemcpyHostToDevice, h->stream);
-    if (e == cudaSuccess)  // repack by the copy engine (~3.4 TB/s), so no SM is needed while kernels run
-      e = cudaMemcpy2DAsync(raw + h->xoff + z0 * h->plane, h->pitch * sizeof(double), stage, h->X * sizeof(double),
-                            h->X * sizeof(double), (size_t)(nz * h->Y), cudaMemcpyDeviceToDevice, h->stream);
-    if (e != cudaSuccess) return e;
-  }
-  return cudaSuccess;
-}
+struct Stager {
+  stencil_ctx* h;
+  double* slot[2] = {nullptr, nullptr};
+  size_t bytes = 0;
+  cudaStream_t aux = nullptr;
+  cudaEvent_t h2d[2] = {nullptr, nullptr}, d2d[2] = {nullptr, nullptr};
+  int64_t n = 0;  // chunks issued
 
-// Staging buffer for upload_planes (released with release_stage; stream-ordered reuse is safe).
-double* acquire_stage(stencil_ctx* h) {
-  if (env_int("STENCIL_NO_STAGE")) return nullptr;  // experiment knob: direct pitched host copies
-  const size_t bytes = (size_t)(kStagePlanes * h->X * h->Y) * sizeof(double);
-  void* p = nullptr;
-  if (h->alloc) p = h->alloc(bytes, (void*)h->stream, h->alloc_user);
-  else if (cudaMalloc(&p, bytes) != cudaSuccess) { cudaGetLastError(); p = nullptr; }
-  return (double*)p;
-}
-void release_stage(stencil_ctx* h, double* p) {
-  if (!p) return;
-  const size_t bytes = (size_t)(kStagePlanes * h->X * h->Y) * sizeof(double);
-  if (h->free_fn) h->free_fn(p, bytes, (void*)h->stream, h->alloc_user);
-  else { cudaStreamSynchronize(h->stream); cudaFree(p); }
-}
+  explicit Stager(stencil_ctx* hh) : h(hh) {
+    if (env_int("STENCIL_NO_STAGE")) return;  // experiment knob: direct pitched host copies
+    bytes = (size_t)(kStagePlanes * h->X * h->Y) * sizeof(double);
+    for (int i = 0; i < 2; ++i) slot[i] = alloc_one();
+    if (slot[1] && (cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking) != cudaSuccess ||
+                    cudaEventCreateWithFlags(&h2d[0], cudaEventDisableTiming) != cudaSuccess ||
+                    cudaEventCreateWithFlags(&h2d[1], cudaEventDisableTiming) != cudaSuccess ||
+                    cudaEventCreateWithFlags(&d2d[0], cudaEventDisableTiming) != cudaSuccess ||
+                    cudaEventCreateWithFlags(&d2d[1], cudaEventDisableTiming) != cudaSuccess)) {
+      cudaGetLastError();
+      drop_aux();
+    }
+  }
+  double* alloc_one() {
+    void* p = nullptr;
+    if (h->alloc) p = h->alloc(bytes, (void*)h->stream, h->alloc_user);
+    else if (cudaMalloc(&p, bytes) != cudaSuccess) { cudaGetLastError(); p = nullptr; }
+    return (double*)p;
+  }
+  void drop_aux() {
+    for (int i = 0; i < 2; ++i) {
+      if (h2d[i]) cudaEventDestroy(h2d[i]);
+      if (d2d[i]) cudaEventDestroy(d2d[i]);
+      h2d[i] = d2d[i] = nullptr;
+    }
+    if (aux) cudaStreamDestroy(aux);
+    aux = nullptr;
+  }
+  cudaError_t upload(const Slab& s, double* raw, const double* host) {
+    const double* src = host + (size_t)s.store_z0 * h->X * h->Y;
+    if (!slot[0])
+      return cudaMemcpy2DAsync(raw + h->xoff, h->pitch * sizeof(double), src, h->X * sizeof(double),
+                               h->X * sizeof(double), (size_t)h->Y * s.zl, cudaMemcpyHostToDevice, h->stream);
+    const int64_t hplane = h->X * h->Y;
+    for (int64_t z0 = 0; z0 < s.zl; z0 += kStagePlanes, ++n) {
+      const int64_t nz = std::min<int64_t>(kStagePlanes, s.zl - z0);
+      const int k = aux ? (int)(n & 1) : 0;
+      cudaError_t e = cudaSuccess;
+      if (aux && n >= 2) e = cudaStreamWaitEvent(h->stream, d2d[k], 0);  // slot k's previous repack is done
+      if (e == cudaSuccess)
+        e = cudaMemcpyAsync(slot[k], src + z0 * hplane, (size_t)(nz * hplane) * sizeof(double), cudaMemcpyHostToDevice,
+                            h->stream);
+      cudaStream_t rs = h->stream;
+      if (e == cudaSuccess && aux) {
+        e = cudaEventRecord(h2d[k], h->stream);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(aux, h2d[k], 0);
+        rs = aux;
+      }
+      if (e == cudaSuccess)  // repack by the copy engine (~3.4 TB/s)
+        e = cudaMemcpy2DAsync(raw + h->xoff + z0 * h->plane, h->pitch * sizeof(double), slot[k], h->X * sizeof(double),
+                              h->X * sizeof(double), (size_t)(nz * h->Y), cudaMemcpyDeviceToDevice, rs);
+      if (e == cudaSuccess && aux) e = cudaEventRecord(d2d[k], aux);
+      if (e != cudaSuccess) return e;
+    }
+    return finish();  // later work on h->stream (and the caller's device copies) sees the planes
+  }
+  cudaError_t finish() {
+    if (!aux) return cudaSuccess;
+    for (int k = 0; k < 2 && k < n; ++k) {
+      cudaError_t e = cudaStreamWaitEvent(h->stream, d2d[k], 0);
+      if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+  }
+  ~Stager() {
+    finish();  // the slots are released in h->stream order, after the last repack that reads them
+    for (int i = 0; i < 2; ++i) {
+      if (!slot[i]) continue;
+      if (h->free_fn) h->free_fn(slot[i], bytes, (void*)h->stream, h->alloc_user);
+      else { cudaStreamSynchronize(h->stream); cudaFree(slot[i]); }
+    }
+    drop_aux();  // destroying a stream / event with work pending is safe (released on completion)
+  }
+};
 
 void fail_create(stencil_ctx* h) {
   if (!h) return;
@@ -888,10 +937,11 @@ int stencil_create(stencil_ctx** out, int kind, int64_t nx, int64_t ny, int64_t 
   if (rc) { fail_create(h); return rc; }
   const size_t hplane = (size_t)h->X * h->Y;
   cudaError_t e = cudaSuccess;
-  double* stage = acquire_stage(h);
+  {  // the staging slots are released (in stream order) before the synchronize below
+  Stager stage(h);
   for (auto& s : h->slabs) {
     // V^0 once, then device copies into the other state buffers (same layout: ghosts and all)
-    e = upload_planes(h, s, s.buf[0], v0, stage);
+    e = stage.upload(s, s.buf[0], v0);
     for (int b = 1; b < h->nbuf && e == cudaSuccess; ++b)
       e = cudaMemcpyAsync(s.buf[b], s.buf[0], (size_t)h->plane * s.zl * sizeof(double), cudaMemcpyDeviceToDevice,
                           h->stream);
@@ -922,10 +972,10 @@ int stencil_create(stencil_ctx** out, int kind, int64_t nx, int64_t ny, int64_t 
     }
     // coefficient fields follow the scalars in coeff[] (kind 5: w0..w4, then the alpha field)
     for (int i = 0; i < h->ncoef && e == cudaSuccess; ++i)
-      e = upload_planes(h, s, s.coef + (size_t)i * h->plane * s.zl, coeff[h->nscal + i], stage);
+      e = stage.upload(s, s.coef + (size_t)i * h->plane * s.zl, coeff[h->nscal + i]);
+  }
   }
   if (e != cudaSuccess) rc = cuda_fail(h, e, "upload");
-  release_stage(h, stage);
   if (rc == ST_OK)
     for (int i = 0; i < h->nscal; ++i) h->scal[i] = *coeff[i];
   if (rc == ST_OK) {
@@ -1095,11 +1145,11 @@ int stencil_write(stencil_ctx* h, int level, const double* in, int64_t in_elems)
   if (!g.ok) { set_err("handle used concurrently"); return ST_E_STATE; }
   if ((rc = wait_peers(h))) return rc;
   cudaError_t e = cudaSuccess;
-  double* stage = acquire_stage(h);
+  Stager stage(h);
   for (auto& s : h->slabs) {
     const int dstb = level == 0 ? h->lv0 : h->lv1;
     const size_t bytes = (size_t)h->plane * s.zl * sizeof(double);
-    if (e == cudaSuccess) e = upload_planes(h, s, s.buf[dstb], in, stage);
+    if (e == cudaSuccess) e = stage.upload(s, s.buf[dstb], in);
     if (e == cudaSuccess && level == 0 && !is_wave(h->kind))  // keep level 1's ghosts equal to the new ghosts
       e = cudaMemcpyAsync(s.buf[h->lv1], s.buf[dstb], bytes, cudaMemcpyDeviceToDevice, h->stream);
     if (e == cudaSuccess && is_wave(h->kind) && h->nbuf == 4 && level == 0)
@@ -1108,7 +1158,6 @@ int stencil_write(stencil_ctx* h, int level, const double* in, int64_t in_elems)
           e = cudaMemcpyAsync(s.buf[b], s.buf[dstb], bytes, cudaMemcpyDeviceToDevice, h->stream);
   }
   if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
-  release_stage(h, stage);
   if (e != cudaSuccess) return cuda_fail(h, e, "write");
   return ST_OK;
 }
