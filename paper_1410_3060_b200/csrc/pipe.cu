@@ -111,22 +111,11 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&w)[32]) {
       : "memory");
 }
 // Distributed shared memory (cluster-pair tiles): the partner CTA's copy of a local
-// shared-memory address, a 128-bit load from it, a remote mbarrier arrive, and a barrier over every
-// thread of the cluster.
+// shared-memory address, a remote mbarrier arrive, and a barrier over every thread of the cluster.
 __device__ __forceinline__ uint32_t dsmem_addr(const void* local, uint32_t rank) {
   uint32_t r;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(local)), "r"(rank));
   return r;
-}
-__device__ __forceinline__ double2 ld_dsmem2(uint32_t addr) {
-  double2 v;
-  asm volatile("ld.shared::cluster.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr) : "memory");
-  return v;
-}
-__device__ __forceinline__ double ld_dsmem1(uint32_t addr) {
-  double v;
-  asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(addr) : "memory");
-  return v;
 }
 __device__ __forceinline__ void mbar_arrive_remote(uint32_t remote_bar) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote_bar) : "memory");
@@ -349,7 +338,7 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN,
   constexpr int R = C::R, NC = C::NC, RL = C::RL, NCONS = C::NCONS, FXB = C::FXB, EXB = C::EXB;
   constexpr int L = C::L;
   constexpr bool WAVE = C::WAVE, HAS_C = C::HAS_C;
-  constexpr int OX = C::OX, OY = C::OY;
+  constexpr int OX = C::OX;
   constexpr int CLAG = C::CLAG;  // steps a C-ring plane stays in use after its level-1 step
 
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -445,7 +434,7 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN,
           // 26 neighbouring items (x/y tiles, z-chunks: the trapezoid halo reaches R*BT <= one tile or
           // chunk) and overwrites what they read, so it starts once all of them are done.  Ids are
           // handed out in order and every CTA is resident, so the items waited for are in progress.
-          const int per = ntx * nty, nzc = p.nzc, zc = item % nzc, t = item / nzc, ty = t / ntx, tx = t - ty * ntx;
+          const int nzc = p.nzc, zc = item % nzc, t = item / nzc, ty = t / ntx, tx = t - ty * ntx;
           const unsigned int want = p.dbase + (unsigned int)blk;
           for (int dz = -1; dz <= 1; ++dz)
             for (int dy = -1; dy <= 1; ++dy)
