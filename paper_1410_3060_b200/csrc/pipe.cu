@@ -454,8 +454,9 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN,
         }
         // Jacobi kinds alternate the two state buffers between blocks: mapA describes the other one
         const CUtensorMap* mv = (!WAVE && (blk & 1)) ? &mapA : &mapV;
-        const int xv = (it.gx0 - R + p.xoff) & ~1;  // footprint box
-        const int xc = (it.gx0 + p.xoff) & ~1;      // level-1 extent box
+        // TMA x coordinates: raw column - X0 (the maps start at raw column X0 = xoff rounded down to even)
+        const int xv = ((it.gx0 - R + p.xoff) & ~1) - (p.xoff & ~1);  // footprint box
+        const int xc = ((it.gx0 + p.xoff) & ~1) - (p.xoff & ~1);      // level-1 extent box
         for (int s = it.s_begin; s <= it.s_end; ++s, ++iv) {
           const uint32_t sv = iv % DV, nv = iv / DV;
           mbar_wait(&emptyV[sv], (nv & 1) ^ 1);
@@ -863,11 +864,13 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 // rank-3 (x, y, z) or rank-4 (x, y, z, field) map of fp64 padded arrays in the library's layout
-bool make_map(CUtensorMap* m, const double* base, int rank, long long pitch, long long Y, long long zl,
+// The map starts at raw column kX0 of each row and is X columns wide: the row padding beyond the padded
+// extent is out of bounds (zero-filled by the TMA unit, no DRAM traffic), not loaded.
+bool make_map(CUtensorMap* m, const double* base, int rank, long long pitch, long long X, long long Y, long long zl,
               long long nfields, long long plane, long long fstride, int bx, int by, int bf) {
   auto enc = encode_fn();
   if (!enc) return false;
-  cuuint64_t dims[4] = {(cuuint64_t)pitch, (cuuint64_t)Y, (cuuint64_t)zl, (cuuint64_t)nfields};
+  cuuint64_t dims[4] = {(cuuint64_t)X, (cuuint64_t)Y, (cuuint64_t)zl, (cuuint64_t)nfields};
   cuuint64_t strides[3] = {(cuuint64_t)pitch * 8, (cuuint64_t)plane * 8, (cuuint64_t)fstride * 8};
   cuuint32_t box[4] = {(cuuint32_t)bx, (cuuint32_t)by, 1, (cuuint32_t)bf};
   cuuint32_t es[4] = {1, 1, 1, 1};
@@ -929,17 +932,21 @@ cudaError_t run_pipe(const KParams& p0, int zchunk_req, int num_sms, cudaStream_
   CUtensorMap mapV, mapC, mapA;
   memset(&mapC, 0, sizeof mapC);
   memset(&mapA, 0, sizeof mapA);
-  if (!make_map(&mapV, p.src_raw, 3, p.pitch, p.ny + 2 * C::R, p.zl, 1, p.plane, 0, C::FXB, C::FY, 1))
+  // TMA x coordinate 0 = raw column X0 (even, so the map base stays 16-byte aligned); the row's last
+  // column is the padded extent's (raw xoff + nx + 2R - 1)
+  const int X0 = p.xoff & ~1;
+  const long long MX = p.xoff + p.nx + 2 * C::R - X0, MY = p.ny + 2 * C::R;
+  if (!make_map(&mapV, p.src_raw + X0, 3, p.pitch, MX, MY, p.zl, 1, p.plane, 0, C::FXB, C::FY, 1))
     return cudaErrorInvalidValue;
   if (!C::WAVE && p.nblk > 1 &&  // multi-block launch: the V box of odd blocks comes from the other buffer
-      !make_map(&mapA, p.dst_raw, 3, p.pitch, p.ny + 2 * C::R, p.zl, 1, p.plane, 0, C::FXB, C::FY, 1))
+      !make_map(&mapA, p.dst_raw + X0, 3, p.pitch, MX, MY, p.zl, 1, p.plane, 0, C::FXB, C::FY, 1))
     return cudaErrorInvalidValue;
   if (C::HAS_C) {
-    bool ok = C::WAVE ? make_map(&mapC, p.srcu_raw, 3, p.pitch, p.ny + 2 * C::R, p.zl, 1, p.plane, 0, C::EXB, TY, 1)
-                      : make_map(&mapC, p.coef_raw, 4, p.pitch, p.ny + 2 * C::R, p.zl, C::NC, p.plane, p.cstride,
+    bool ok = C::WAVE ? make_map(&mapC, p.srcu_raw + X0, 3, p.pitch, MX, MY, p.zl, 1, p.plane, 0, C::EXB, TY, 1)
+                      : make_map(&mapC, p.coef_raw + X0, 4, p.pitch, MX, MY, p.zl, C::NC, p.plane, p.cstride,
                                  C::EXB, TY, C::NC);
     if (ok && C::WAVE && C::NC > 0)
-      ok = make_map(&mapA, p.coef_raw, 4, p.pitch, p.ny + 2 * C::R, p.zl, C::NC, p.plane, p.cstride, C::EXB, TY, C::NC);
+      ok = make_map(&mapA, p.coef_raw + X0, 4, p.pitch, MX, MY, p.zl, C::NC, p.plane, p.cstride, C::EXB, TY, C::NC);
     if (!ok) return cudaErrorInvalidValue;
   }
   int occ = 1;
