@@ -328,7 +328,11 @@ def main():
 
     ms, (kern_ms, kern_launches), launches, clk = timed_region()
     # a timed region that saw a hardware or thermal slowdown is measured once more (any rank's verdict)
-    bad = torch.tensor([int(bool(set(clk.summary().get("reasons", [])) & SLOWDOWN_REASONS))], device=dev)
+    # (or whose SM clock sat far below its maximum with no throttle reason: a leftover clock lock)
+    cs0 = clk.summary()
+    stuck = (not cs0.get("reasons") and cs0.get("sm_mhz") and cs0.get("sm_max_mhz")
+             and cs0["sm_mhz"] < 0.75 * cs0["sm_max_mhz"])
+    bad = torch.tensor([int(bool(set(cs0.get("reasons", [])) & SLOWDOWN_REASONS) or bool(stuck))], device=dev)
     if world > 1:
         dist.all_reduce(bad, op=dist.ReduceOp.MAX)
     remeasured = None
