@@ -21,8 +21,8 @@ import synth  # noqa: E402
 from synth import workloads  # noqa: E402
 
 TUNED = os.path.join(ROOT, "paper_1410_3060_b200", "tuned.json")
-MAX_BT = {1: 8, 2: 4, 3: 1, 4: 1, 5: 1}
-N_CFG = {1: 1, 2: 9, 3: 8, 4: 4, 5: 4}  # pipe tile configurations per kind (pipe.cu launch_pipe)
+MAX_BT = {1: 8, 2: 4, 3: 2, 4: 1, 5: 1}
+N_CFG = {1: 1, 2: 10, 3: 9, 4: 4, 5: 5}  # pipe tile configurations per kind (pipe.cu launch_pipe)
 
 
 def time_plan(w, T, bt, cfg, zchunk, reps=3, variant=st.ST_VARIANT_PIPE):
