@@ -413,26 +413,35 @@ def main():
     # read the newest level (D2H), every step.
     e2e = None
     if not args.no_e2e:
-        inp = synth.make_inputs(w.kind, w.nx, w.ny, w.nz)
+        # multi-rank: every rank holds (and uploads) only the planes it stores, and reads back the planes
+        # it owns (st_opts.host_slab) -- no rank ever materialises the global inputs in host memory
+        pl = None
+        box = None
+        if world > 1:
+            pl = st.stencil_plan_slab(w.nz, synth.RADIUS[w.kind], world, rank, info["bt"])
+            dims = synth.padded_dims(w.kind, w.nx, w.ny, w.nz)
+            box = ((pl["store_z0"], pl["store_z1"]), (0, dims[1]), (0, dims[2]))
+        inp = synth.make_inputs(w.kind, w.nx, w.ny, w.nz, box=box)
         pin = lambda a: torch.from_numpy(a).pin_memory().numpy()  # noqa: E731
         V = pin(inp.V)
         U = pin(inp.U) if w.kind in synth.WAVE_KINDS else None
         coeff = list(inp.scalars) + [pin(c) for c in inp.coef]
-        out = pin(np.empty_like(inp.V))
+        out = pin(np.empty_like(inp.V) if pl is None else
+                  np.empty((pl["own_z1"] - pl["own_z0"],) + inp.V.shape[1:], dtype=np.float64))
         del inp
         h2d = V.nbytes + (U.nbytes if U is not None else 0) + sum(c.nbytes for c in coeff if hasattr(c, "nbytes"))
         d2h = out.nbytes
-        if world > 1:  # every rank uploads only the planes it stores and reads back the planes it owns
-            R = synth.RADIUS[w.kind]
-            pl = st.stencil_plan_slab(w.nz, R, world, rank, info["bt"])
-            planes = w.nz + 2 * R
-            h2d = h2d * (pl["store_z1"] - pl["store_z0"]) // planes
-            d2h = d2h * (pl["own_z1"] - pl["own_z0"]) // planes
 
         def make_grid(stream=None):
             return st.Grid(w.kind, w.nx, w.ny, w.nz, v0=V, u0=U, coeff=coeff, variant=args.variant,
-                           bt=args.bt, zchunk=args.zchunk, rank=rank, nranks=world, nccl_id=nccl_id,
-                           halo=halo, stream=stream)
+                           bt=info["bt"] if world > 1 else args.bt, zchunk=args.zchunk, rank=rank, nranks=world,
+                           nccl_id=nccl_id, halo=halo, stream=stream, host_slab=world > 1)
+
+        def read_result(ge, o):
+            if pl is None:
+                ge.read(0, out=o)
+            else:
+                st.stencil_read_planes(ge.h, 0, pl["own_z0"], pl["own_z1"], o)
 
         # Single GPU with room for two grids: a two-deep pipeline -- a host thread creates (uploads)
         # step k+1's grid on its own stream while step k runs and reads back on the other; every
@@ -441,16 +450,18 @@ def main():
         pipelined = world == 1 and free_b > 2.2 * info["device_bytes"]
         ek = max(1, min(2 * args.steps, 8) if pipelined else min(args.steps, 3))
         outs = [out, pin(np.empty_like(out))] if pipelined else [out, out]
+        # the pipeline's two streams live across the warm-up and the timed steps: torch's caching
+        # allocator keeps freed device memory per stream, so new streams would allocate afresh
+        streams = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
 
         def e2e_run(k_steps):
             if not pipelined:
                 for _ in range(k_steps):
                     with make_grid() as ge:
                         ge.run(w.T)
-                        ge.read(0, out=out)
+                        read_result(ge, out)
                 return
             from concurrent.futures import ThreadPoolExecutor
-            streams = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
 
             def create(k):
                 torch.cuda.set_device(dev)
@@ -462,7 +473,7 @@ def main():
                     if k + 1 < k_steps:
                         fut = ex.submit(create, k + 1)
                     ge.run(w.T)
-                    ge.read(0, out=outs[k % 2])
+                    read_result(ge, outs[k % 2])
                     ge.close()
         e2e_run(2 if pipelined else 1)  # warm-up: both pipeline slots' device memory cached
         barrier()
@@ -477,6 +488,8 @@ def main():
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "steps": ek,
                "note": ("stencil_create from pinned host arrays + stencil_run(T) + stencil_read of the newest "
                         "level every step, wall clock" +
+                        ("; each rank holds, uploads and reads back only its own planes (st_opts.host_slab)"
+                         if world > 1 else "") +
                         ("; two-deep pipeline (step k+1's upload on a second stream overlaps step k's "
                          "run and readback)" if pipelined else ""))}
         del outs

@@ -127,6 +127,10 @@ typedef struct {
   int halo;            /* ST_HALO_COPY (0) or ST_HALO_PEER; used when nranks > 1.  ST_HALO_PEER across
                           processes allocates the state buffers with cudaMalloc (CUDA IPC needs whole
                           allocations), ignoring alloc/free for them */
+  int host_slab;       /* 0: host arrays of stencil_create / stencil_write are GLOBAL padded arrays.
+                          1 (nranks > 1, local_slabs = 1, bt >= 1): they hold only this rank's stored
+                          planes [store_z0, store_z1) of stencil_plan_slab(nz, R, nranks, rank, bt) --
+                          a rank never needs the other ranks' inputs in host memory */
 } st_opts;
 
 typedef struct {
@@ -149,7 +153,9 @@ void stencil_opts_default(st_opts *o);
 /*
  * Create a grid from host arrays.  Every pointer is a HOST pointer to a dense padded array of
  * (nz+2R)*(ny+2R)*(nx+2R) doubles in the GLOBAL layout (every rank passes the global arrays and
- * copies its slab; the library copies everything before returning; the caller keeps ownership).
+ * copies its slab; the library copies everything before returning; the caller keeps ownership) --
+ * or, with opts->host_slab = 1, to the (store_z1-store_z0)*(ny+2R)*(nx+2R) doubles of this rank's
+ * stored planes only (same layout, plane store_z0 first).
  *   v0      : Omega^0, ghosts included (fixed boundary values).
  *   u0      : wave kinds (3, 5) only: Omega^{-1}; only its interior is used (ghosts come from v0).
  *             Other kinds: must be NULL.

@@ -42,7 +42,7 @@ class StOpts(ctypes.Structure):
                 ("tile_cfg", ctypes.c_int), ("local_slabs", ctypes.c_int), ("zchunk", ctypes.c_int),
                 ("rank", ctypes.c_int), ("nranks", ctypes.c_int), ("nccl_id", ctypes.c_void_p),
                 ("stream", ctypes.c_void_p), ("alloc", ALLOC_FN), ("free", FREE_FN),
-                ("alloc_user", ctypes.c_void_p), ("halo", ctypes.c_int)]
+                ("alloc_user", ctypes.c_void_p), ("halo", ctypes.c_int), ("host_slab", ctypes.c_int)]
 
 
 class StInfo(ctypes.Structure):
@@ -133,9 +133,9 @@ def stencil_opts_default() -> StOpts:
     return o
 
 
-def _f64(a, n=None, name="array"):
+def _f64(a, n=None, name="array", exact=False):
     a = np.ascontiguousarray(a, dtype=np.float64)
-    if n is not None and a.size < n:
+    if n is not None and (a.size < n or (exact and a.size != n)):
         raise ValueError(f"{name} has {a.size} elements, need {n}")
     return a
 
@@ -145,13 +145,19 @@ def stencil_create(kind, nx, ny, nz, coeff, v0, u0=None, opts: StOpts | None = N
     fields (host numpy arrays), in include/stencil.h's order."""
     R = RADIUS.get(kind, 0)
     n = (nx + 2 * R) * (ny + 2 * R) * (nz + 2 * R)
+    exact = bool(opts is not None and opts.host_slab)
+    if exact:  # this rank's stored planes only (stencil_plan_slab), exactly
+        if opts.bt < 1 or opts.nranks < 2:
+            raise ValueError("host_slab needs nranks > 1 and an explicit bt >= 1 (the stored range)")
+        pl = stencil_plan_slab(nz, R, opts.nranks, opts.rank, opts.bt)
+        n = (nx + 2 * R) * (ny + 2 * R) * (pl["store_z1"] - pl["store_z0"])
     ns = N_SCALARS.get(kind, 0)
     coeff = list(coeff)
     arrs = [np.array([float(c)], dtype=np.float64) for c in coeff[:ns]]
-    arrs += [_f64(c, n, "coefficient field") for c in coeff[ns:]]
+    arrs += [_f64(c, n, "coefficient field", exact) for c in coeff[ns:]]
     ptrs = (ctypes.c_void_p * max(1, len(arrs)))(*[a.ctypes.data for a in arrs])
-    v0 = _f64(v0, n, "v0")
-    u0 = None if u0 is None else _f64(u0, n, "u0")
+    v0 = _f64(v0, n, "v0", exact)
+    u0 = None if u0 is None else _f64(u0, n, "u0", exact)
     h = ctypes.c_void_p()
     _check(lib().stencil_create(ctypes.byref(h), kind, nx, ny, nz, ctypes.cast(ptrs, ctypes.c_void_p),
                                 len(arrs), v0.ctypes.data, None if u0 is None else u0.ctypes.data,
@@ -345,7 +351,7 @@ class Grid:
     def __init__(self, kind, nx, ny, nz, *, seed=None, scalars=None, v0=None, u0=None, coeff=None,
                  variant=ST_VARIANT_AUTO, bt=0, zchunk=0, tile_cfg=0, rank=0, nranks=1, nccl_id=None,
                  local_slabs=1, halo=ST_HALO_COPY, wire_peers=True,
-                 device=None, stream=None, torch_memory=True, tuned=False):
+                 device=None, stream=None, torch_memory=True, tuned=False, host_slab=False):
         import torch
         if tuned and bt == 0:  # plan measured by tools/tune.py for this kind and shape, if any
             plan = tuned_plan(kind, nx, ny, nz)
@@ -359,6 +365,7 @@ class Grid:
         o.variant, o.bt, o.zchunk, o.tile_cfg = variant, bt, zchunk, tile_cfg
         o.rank, o.nranks, o.local_slabs = rank, nranks, local_slabs
         o.halo = halo
+        o.host_slab = int(bool(host_slab))  # v0/u0/coeff (and write()) hold this rank's stored planes only
         self._id = None
         if nranks > 1 and local_slabs == 1 and halo == ST_HALO_COPY:
             self._id = ctypes.create_string_buffer(bytes(nccl_id), 128)

@@ -148,6 +148,9 @@ struct stencil_ctx {
   int device = 0, num_sms = 148;
   int variant = ST_VARIANT_PIPE, bt = 1, zchunk_req = 0, tile_cfg = 0;
   cudaStream_t stream = nullptr;
+  bool host_slab = false;  // host arrays hold only the stored planes (st_opts.host_slab)
+  // global padded plane of host array plane 0
+  int64_t host_z0() const { return host_slab ? slabs.front().store_z0 : 0; }
   st_alloc_fn alloc = nullptr;
   st_free_fn free_fn = nullptr;
   void* alloc_user = nullptr;
@@ -337,6 +340,11 @@ int create_common(stencil_ctx** out, int kind, int64_t nx, int64_t ny, int64_t n
   }
   if (nz < o.nranks) { set_err("nz=%lld < nranks=%d", (long long)nz, o.nranks); return ST_E_INVAL; }
   if (o.halo != ST_HALO_COPY && o.halo != ST_HALO_PEER) { set_err("bad halo mode %d", o.halo); return ST_E_INVAL; }
+  if (o.host_slab && (o.nranks < 2 || o.local_slabs != 1 || o.bt < 1)) {
+    set_err("host_slab needs nranks > 1, local_slabs = 1 and an explicit bt >= 1 (the stored range must be "
+            "known to the caller: stencil_plan_slab)");
+    return ST_E_INVAL;
+  }
   if (o.variant == ST_VARIANT_COOP && o.nranks > 1) {
     set_err("ST_VARIANT_COOP runs a single slab (nranks = 1)");
     return ST_E_INVAL;
@@ -372,6 +380,7 @@ int create_common(stencil_ctx** out, int kind, int64_t nx, int64_t ny, int64_t n
   h->zchunk_req = o.zchunk;
   h->tile_cfg = o.tile_cfg;
   h->halo = o.nranks > 1 ? o.halo : ST_HALO_COPY;
+  h->host_slab = o.host_slab != 0;
   h->ipc = h->halo == ST_HALO_PEER && one_slab;
   if (h->ipc) {  // IPC maps whole allocations: state buffers and flags come straight from cudaMalloc
     h->alloc = nullptr;
@@ -508,7 +517,7 @@ struct Stager {
     aux = nullptr;
   }
   cudaError_t upload(const Slab& s, double* raw, const double* host) {
-    const double* src = host + (size_t)s.store_z0 * h->X * h->Y;
+    const double* src = host + (size_t)(s.store_z0 - h->host_z0()) * h->X * h->Y;
     if (!slot[0])
       return cudaMemcpy2DAsync(raw + h->xoff, h->pitch * sizeof(double), src, h->X * sizeof(double),
                                h->X * sizeof(double), (size_t)h->Y * s.zl, cudaMemcpyHostToDevice, h->stream);
@@ -953,11 +962,11 @@ int stencil_create(stencil_ctx** out, int kind, int64_t nx, int64_t ny, int64_t 
       for (int64_t z = 0; z < s.zl && e == cudaSuccess; ++z) {
         const int64_t gz = s.store_z0 + z;
         const bool zghost = gz < R || gz >= nz + R;
-        const double* src = (zghost ? v0 : u0) + (size_t)gz * hplane;
+        const double* src = (zghost ? v0 : u0) + (size_t)(gz - h->host_z0()) * hplane;
         double* dz = d + z * h->plane;
         e = cudaMemcpy2DAsync(dz, P, src, HX, HX, h->Y, cudaMemcpyHostToDevice, h->stream);
         if (e == cudaSuccess && !zghost) {
-          const double* g = v0 + (size_t)gz * hplane;
+          const double* g = v0 + (size_t)(gz - h->host_z0()) * hplane;
           e = cudaMemcpy2DAsync(dz, P, g, HX, HX, R, cudaMemcpyHostToDevice, h->stream);
           if (e == cudaSuccess)
             e = cudaMemcpy2DAsync(dz + (h->Y - R) * h->pitch, P, g + (h->Y - R) * h->X, HX, HX, R,
@@ -1139,7 +1148,8 @@ int stencil_write(stencil_ctx* h, int level, const double* in, int64_t in_elems)
     set_err("level %d not writable for kind %d", level, h->kind);
     return ST_E_INVAL;
   }
-  const int64_t total = (h->nz + 2 * h->R) * h->X * h->Y;
+  const int64_t total = (h->host_slab ? h->slabs.front().store_z1 - h->slabs.front().store_z0 : h->nz + 2 * h->R) *
+                        h->X * h->Y;
   if (!in || in_elems < total) { set_err("in must hold %lld doubles", (long long)total); return ST_E_INVAL; }
   Guard g(h);
   if (!g.ok) { set_err("handle used concurrently"); return ST_E_STATE; }

@@ -204,3 +204,80 @@ def test_wave_bt2_slabs(halo, P):
     got = run(synth.K25W, n, T, nranks=P, local_slabs=P, bt=2, halo=halo)
     assert got[2]["bt"] == 2 and ref[2]["bt"] == 2
     assert np.array_equal(got[0], ref[0]) and np.array_equal(got[1], ref[1])
+
+
+@pytest.mark.parametrize("kind,n,T,bt", [(synth.K7V, (40, 33, 37), 7, 3), (synth.K25W, (70, 20, 41), 5, 1),
+                                         (synth.K25V, (70, 20, 41), 4, 1)])
+@pytest.mark.parametrize("P", [2, 3])
+def test_host_slab_inputs(kind, n, T, bt, P):
+    """st_opts.host_slab: each rank passes host arrays holding only its stored planes
+    [store_z0, store_z1) (stencil_plan_slab) -- a rank never holds the global inputs -- and reads back
+    its owned planes with stencil_read_planes.  Ranks emulated as handles of this process (ST_HALO_PEER
+    protocol as above); owned planes of all ranks == a single slab created from the global arrays,
+    bitwise; stencil_write with a local array round-trips."""
+    import torch
+    R = synth.RADIUS[kind]
+    inp = synth.make_inputs(kind, *n, seed=7)
+    coeff = list(inp.scalars) + list(inp.coef)
+    u0 = inp.U if kind in WAVES else None
+    with st.Grid(kind, *n, v0=inp.V, u0=u0, coeff=coeff, bt=bt) as g:
+        g.run(T)
+        ref = g.read(0)
+    dims = synth.padded_dims(kind, *n)
+    streams = [torch.cuda.Stream() for _ in range(P)]
+    gs = []
+    try:
+        for r in range(P):
+            pl = st.stencil_plan_slab(n[2], R, P, r, bt)
+            box = ((pl["store_z0"], pl["store_z1"]), (0, dims[1]), (0, dims[2]))
+            loc = synth.make_inputs(kind, *n, seed=7, box=box)
+            gs.append(st.Grid(kind, *n, v0=loc.V, u0=loc.U if kind in WAVES else None,
+                              coeff=list(loc.scalars) + list(loc.coef), bt=bt, rank=r, nranks=P,
+                              halo=st.ST_HALO_PEER, wire_peers=False, stream=streams[r], host_slab=True))
+        descs = [g.peer_export() for g in gs]
+        for r, g in enumerate(gs):
+            g.peer_import(*st.peer_neighbours(descs, r))
+        for g in gs:  # post every rank's words first, then poll
+            try:
+                g.peer_handshake(timeout_ms=0)
+            except st.StencilError:
+                pass
+        for g in gs:
+            g.peer_handshake(timeout_ms=2000)
+        for g in gs:
+            g.run(T)
+        for r, g in enumerate(gs):
+            i = g.info()
+            z0, z1 = i["own_z0"], i["own_z1"]
+            assert np.array_equal(g.read_planes(0, z0, z1), ref[z0:z1])
+        # a local array of the wrong size is rejected by the binding
+        pl = st.stencil_plan_slab(n[2], R, P, 0, bt)
+        with pytest.raises(ValueError):
+            st.Grid(kind, *n, v0=inp.V, u0=u0, coeff=coeff, bt=bt, rank=0, nranks=P, halo=st.ST_HALO_PEER,
+                    wire_peers=False, host_slab=True)
+    finally:
+        for g in gs:
+            g.close()
+
+
+def test_host_slab_needs_explicit_bt_and_ranks():
+    inp = synth.make_inputs(synth.K7V, 8, 8, 8, seed=1)
+    with pytest.raises(ValueError):  # a single rank: nothing to slice
+        st.Grid(synth.K7V, 8, 8, 8, v0=inp.V, coeff=list(inp.coef), bt=2, host_slab=True)
+    pl = st.stencil_plan_slab(8, 1, 2, 0, 2)
+    loc = synth.make_inputs(synth.K7V, 8, 8, 8, seed=1, box=((pl["store_z0"], pl["store_z1"]), (0, 10), (0, 10)))
+    with pytest.raises(ValueError):  # bt = 0: the stored range is not known in advance
+        st.Grid(synth.K7V, 8, 8, 8, v0=loc.V, coeff=list(loc.coef), rank=0, nranks=2, halo=st.ST_HALO_PEER,
+                wire_peers=False, host_slab=True)
+    # the library enforces the same rule for C callers (raw ABI call, no binding-side check)
+    import ctypes
+    from paper_1410_3060_b200 import _binding as B
+    o = st.stencil_opts_default()
+    o.nranks, o.rank, o.halo, o.host_slab = 2, 0, st.ST_HALO_PEER, 1  # bt = 0
+    arrs = [np.ascontiguousarray(c) for c in inp.coef]
+    ptrs = (ctypes.c_void_p * 7)(*[a.ctypes.data for a in arrs])
+    h = ctypes.c_void_p()
+    rc = B.lib().stencil_create(ctypes.byref(h), synth.K7V, 8, 8, 8, ctypes.cast(ptrs, ctypes.c_void_p), 7,
+                                np.ascontiguousarray(inp.V).ctypes.data, None, ctypes.byref(o))
+    assert rc == st.ST_E_INVAL and "host_slab" in st.stencil_last_error()
+
