@@ -219,8 +219,9 @@ int stencil_read_planes(stencil_ctx *h, int level, int64_t z0, int64_t z1, doubl
                         int64_t out_elems);
 
 /* Overwrite a level from a dense padded GLOBAL host array (interior and ghosts of this rank's
- * stored planes).  Used for checkpoint/resume and the end-to-end upload path.  level 1 only for the
- * wave.  Writing level 0 of a Jacobi kind also resets level 1's ghosts to the new ghosts. */
+ * stored planes) -- with opts->host_slab, from an array of this rank's stored planes only.  Used for
+ * checkpoint/resume and the end-to-end upload path.  level 1 only for the wave.  Writing level 0 of a
+ * Jacobi kind also resets level 1's ghosts to the new ghosts.  ST_E_INVAL if in_elems is too small. */
 int stencil_write(stencil_ctx *h, int level, const double *in, int64_t in_elems);
 
 /* Plan and state of a handle. */
