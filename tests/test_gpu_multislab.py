@@ -225,12 +225,13 @@ def test_host_slab_inputs(kind, n, T, bt, P):
         ref = g.read(0)
     dims = synth.padded_dims(kind, *n)
     streams = [torch.cuda.Stream() for _ in range(P)]
-    gs = []
+    gs, locs = [], []
     try:
         for r in range(P):
             pl = st.stencil_plan_slab(n[2], R, P, r, bt)
             box = ((pl["store_z0"], pl["store_z1"]), (0, dims[1]), (0, dims[2]))
             loc = synth.make_inputs(kind, *n, seed=7, box=box)
+            locs.append((pl["store_z0"], loc.V))
             gs.append(st.Grid(kind, *n, v0=loc.V, u0=loc.U if kind in WAVES else None,
                               coeff=list(loc.scalars) + list(loc.coef), bt=bt, rank=r, nranks=P,
                               halo=st.ST_HALO_PEER, wire_peers=False, stream=streams[r], host_slab=True))
@@ -250,6 +251,11 @@ def test_host_slab_inputs(kind, n, T, bt, P):
             i = g.info()
             z0, z1 = i["own_z0"], i["own_z1"]
             assert np.array_equal(g.read_planes(0, z0, z1), ref[z0:z1])
+        for g, (s0, lv) in zip(gs, locs):  # stencil_write from a local array round-trips
+            g.sync()
+            g.write(0, lv)
+            i = g.info()
+            assert np.array_equal(g.read_planes(0, i["own_z0"], i["own_z1"]), lv[i["own_z0"] - s0:i["own_z1"] - s0])
         # a local array of the wrong size is rejected by the binding
         pl = st.stencil_plan_slab(n[2], R, P, 0, bt)
         with pytest.raises(ValueError):
