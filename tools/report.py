@@ -36,7 +36,7 @@ def main():
     out = csv.writer(sys.stdout)
     out.writerow(["workload", "kind", "nx", "ny", "nz", "T", "variant", "bt", "tile", "ms_median", "glups",
                   "roof_bt_glups", "frac_roof_bt", "roof_bt1_glups", "frac_roof_bt1", "roof_fp64_glups",
-                  "bound", "sm_mhz", "clock_reasons"])
+                  "bound", "sm_mhz", "clock_reasons", "power_w", "nj_per_lup"])
     for name in a.workloads.split(","):
         w = by[name]
         g = st.Grid(w.kind, w.nx, w.ny, w.nz, seed=synth.DEFAULT_SEED)
@@ -66,7 +66,8 @@ def main():
         out.writerow([w.name, synth.KIND_NAMES[w.kind], w.nx, w.ny, w.nz, w.T, VARIANTS.get(info["variant"]), bt,
                       f"{info['tile_x']}x{info['tile_y']}", round(ms, 3), round(glups, 2), round(roof, 1),
                       round(glups / roof, 3), round(roof1, 1), round(glups / roof1, 3), round(roof_fp, 1),
-                      "hbm" if roof_hbm <= roof_fp else "fp64", c.get("sm_mhz"), "|".join(c.get("reasons") or [])])
+                      "hbm" if roof_hbm <= roof_fp else "fp64", c.get("sm_mhz"), "|".join(c.get("reasons") or []),
+                      c.get("power_w"), round(c["power_w"] / glups, 3) if c.get("power_w") else None])
         sys.stdout.flush()
 
 
