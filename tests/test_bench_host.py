@@ -1,0 +1,43 @@
+"""Host-side logic of bench.py (no GPU): the fused-block schedule the roofline's byte count assumes, the
+N-GPU workloads, and the compulsory bytes per launch."""
+import bench
+import synth
+from synth import workloads
+
+
+def test_blocks_of_matches_the_runtime_schedule():
+    # runtime.cu: full blocks of bt; a remainder shorter than bt is merged with the last full block and
+    # split evenly (T = 100 at bt = 3 -> 32 blocks of 3, then 2 + 2)
+    assert bench.blocks_of(100, 3) == [3] * 32 + [2, 2]
+    assert bench.blocks_of(100, 4) == [4] * 25
+    assert bench.blocks_of(10, 1) == [1] * 10
+    assert bench.blocks_of(7, 3) == [3, 2, 2]
+    assert bench.blocks_of(5, 8) == [5]
+    for T in range(1, 60):
+        for bt in range(1, 9):
+            b = bench.blocks_of(T, bt)
+            assert sum(b) == T and max(b) <= bt and min(b) >= 1
+
+
+def test_block_bytes_per_cell():
+    # C2 at bt = 3: 16 B of state + 56 B of coefficients per cell per launch = 24 B per update
+    assert bench.block_bytes_per_cell(synth.K7V, 3) == 72
+    assert bench.block_bytes_per_cell(synth.K7V, 1) == 72
+    assert bench.block_bytes_per_cell(synth.K25V, 1) == 120
+    assert bench.block_bytes_per_cell(synth.K25W, 2) == 32  # both levels in (16 B) and out (16 B)
+    assert bench.block_bytes_per_cell(synth.K25W, 1) == 24  # V, U in; U out (in place)
+
+
+def test_pick_workload_weak_and_strong():
+    w = bench.pick_workload("C2", 4, "weak")
+    assert (w.nx, w.ny, w.nz, w.T) == (512, 512, 2048, 100)
+    w = bench.pick_workload("C2", 4, "strong")
+    assert (w.nx, w.ny, w.nz) == (512, 512, 512)
+    w = bench.pick_workload("C5", 8, "weak")  # BASELINE.json's weak variant: 1024 x 1024 x 256N
+    assert (w.nx, w.ny, w.nz, w.T) == (1024, 1024, 2048, 200)
+    assert bench.pick_workload("C2", 1) is workloads.C2 or bench.pick_workload("C2", 1).nz == 512
+
+
+def test_slowdown_reasons_trigger_a_second_measurement():
+    assert {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"} <= bench.SLOWDOWN_REASONS
+    assert "sw_power_cap" not in bench.SLOWDOWN_REASONS  # kept and noted, not re-measured
