@@ -212,3 +212,14 @@ def test_multiblock_launch_bitwise(kind, monkeypatch):
         monkeypatch.delenv("STENCIL_MULTIBLOCK")
         assert np.array_equal(got[0], ref[0]), bt
         assert got[2]["launches"] < ref[2]["launches"]
+
+
+@pytest.mark.parametrize("T,bt", [(7, 3), (10, 3), (12, 4), (5, 1), (9, 2)])
+def test_launch_schedule_matches_bench_accounting(T, bt):
+    """bench.py counts the roofline's algorithmic bytes per fused block with bench.blocks_of(T, bt);
+    the runtime must launch exactly those blocks (one pipe launch per block on a single slab)."""
+    import bench
+    with st.Grid(synth.K7V, 40, 36, 30, seed=2, variant=st.ST_VARIANT_PIPE, bt=bt) as g:
+        l0 = g.info()["launches"]
+        g.run(T)
+        assert g.info()["launches"] - l0 == len(bench.blocks_of(T, bt))
