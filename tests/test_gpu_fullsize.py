@@ -9,7 +9,7 @@ import oracle
 import paper_1410_3060_b200 as st
 import synth
 from synth import workloads
-from gpu_common import WAVE, assert_parity, gpu_run
+from gpu_common import WAVES, assert_parity, gpu_run
 
 pytestmark = pytest.mark.gpu
 
@@ -40,7 +40,8 @@ def test_C1_full_oracle():
     assert_parity(w.kind, g_new, g_old, o_new, o_old, inp.R, 1e-11, inputs=inp)
 
 
-@pytest.mark.parametrize("name", ["C2-7pt-var-512", "C3-25pt-wave-512", "C4-25pt-var-512"])
+@pytest.mark.parametrize("name", ["C2-7pt-var-512", "C3-25pt-wave-512", "C4-25pt-var-512",
+                                  "C3A-25pt-wave-alpha-512"])
 def test_512_sampled_cells(name):
     w = workloads.BY_NAME[name]
     R = synth.RADIUS[w.kind]
@@ -53,15 +54,16 @@ def test_512_sampled_cells(name):
         g.run(T)
         g_new = grid_values(g, cells)
         scale = np.max(np.abs(g.read_planes(0, w.nz // 2, w.nz // 2 + 1)))
-        if w.kind == WAVE:
+        if w.kind in WAVES:
             g_old = grid_values(g, cells, 1)
     # normwise against the field's magnitude (max over a mid plane), BASELINE.json's 1e-11
     assert np.max(np.abs(g_new - o_new)) <= 1e-11 * scale
-    if w.kind == WAVE:
+    if w.kind in WAVES:
         assert np.max(np.abs(g_old - o_old)) <= 1e-11 * scale
 
 
-@pytest.mark.parametrize("name", ["C2-7pt-var-512", "C3-25pt-wave-512", "C4-25pt-var-512"])
+@pytest.mark.parametrize("name", ["C2-7pt-var-512", "C3-25pt-wave-512", "C4-25pt-var-512",
+                                  "C3A-25pt-wave-alpha-512"])
 def test_512_full_T_bitwise_vs_naive(name):
     w = workloads.BY_NAME[name]
     planes = [synth.RADIUS[w.kind], w.nz // 3, w.nz // 2 + 7, w.nz + synth.RADIUS[w.kind] - 1]
@@ -70,7 +72,7 @@ def test_512_full_T_bitwise_vs_naive(name):
         with st.Grid(w.kind, w.nx, w.ny, w.nz, seed=synth.DEFAULT_SEED, variant=variant) as g:
             g.run(w.T)
             res.append([g.read_planes(0, z, z + 1) for z in planes])
-            if w.kind == WAVE:
+            if w.kind in WAVES:
                 res[-1] += [g.read_planes(1, z, z + 1) for z in planes]
     for a, b in zip(*res):
         assert np.array_equal(a, b)
