@@ -223,3 +223,22 @@ def test_launch_schedule_matches_bench_accounting(T, bt):
         l0 = g.info()["launches"]
         g.run(T)
         assert g.info()["launches"] - l0 == len(bench.blocks_of(T, bt))
+
+
+@pytest.mark.parametrize("kind,n", [(synth.K7V, (8000, 3, 3)), (synth.K7V, (3, 5000, 5)),
+                                    (synth.K7V, (4096, 4096, 2)), (synth.K25V, (2500, 9, 6)),
+                                    (synth.K25W, (7, 3000, 9))])
+def test_extreme_aspect_ratios_bitwise(kind, n):
+    """G6 at the extremes: very long rows / columns and a 16.8 M-cell plane (64-bit plane offsets, TMA
+    boxes at the far end of a row, one z-chunk per tile) -- the default plan equals the naive sweeps
+    bitwise, and the oracle on the thin cases."""
+    T = 3
+    ref = gpu_run(kind, *n, T, seed=5, variant=st.ST_VARIANT_NAIVE)
+    got = gpu_run(kind, *n, T, seed=5)
+    assert np.array_equal(got[0], ref[0])
+    if kind in WAVES:
+        assert np.array_equal(got[1], ref[1])
+    if n[0] * n[1] * n[2] <= 200000:
+        inp = synth.make_inputs(kind, *n, seed=5)
+        o_new, o_old = oracle.run(inp, T)
+        assert_parity(kind, got[0], got[1], o_new, o_old, inp.R, 1e-13, inputs=inp)
