@@ -122,3 +122,30 @@ def test_C2_full_size_every_plan_bitwise():
             full.append(g.read(0))
     for i, a in enumerate(full[1:]):
         assert np.array_equal(a, full[0]), i
+
+
+def _host_gb():
+    import os
+    return os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES") / 2**30
+
+
+@pytest.mark.skipif(_host_gb() < 64, reason="needs ~30 GB of host memory for the full-size oracle")
+def test_C2_full_size_every_cell_G1_G2_G5():
+    """BASELINE.json's headline config exactly as bench.py times it (C2, 512^3, T = 100, the default
+    plan): every interior cell against the oracle -- G1 normwise <= 1e-11, G2 per cell <= 1e-11 * S(p)
+    (S = the oracle on |inputs|; C2's coefficients are non-negative), and G5 ghosts bitwise unchanged."""
+    w = workloads.C2
+    inp = synth.make_inputs(w.kind, w.nx, w.ny, w.nz)
+    g_new, _, info = gpu_run(w.kind, w.nx, w.ny, w.nz, w.T)
+    assert info["bt"] == 3  # the bench's plan
+    o_new, _ = oracle.run(inp, w.T)
+    R = inp.R
+    I = (slice(R, -R),) * 3
+    assert np.max(np.abs(g_new[I] - o_new[I])) <= 1e-11 * np.max(np.abs(o_new[I]))  # G1
+    ghost = np.ones(g_new.shape, dtype=bool)
+    ghost[I] = False
+    assert np.array_equal(g_new[ghost], inp.V[ghost])  # G5
+    absinp = synth.Inputs(w.kind, w.nx, w.ny, w.nz, np.abs(inp.V), np.abs(inp.U), inp.coef, inp.scalars)
+    del inp
+    S, _ = oracle.run(absinp, w.T)
+    assert np.all(np.abs(g_new[I] - o_new[I]) <= 1e-11 * S[I])  # G2
