@@ -149,3 +149,28 @@ def test_C2_full_size_every_cell_G1_G2_G5():
     del inp
     S, _ = oracle.run(absinp, w.T)
     assert np.all(np.abs(g_new[I] - o_new[I]) <= 1e-11 * S[I])  # G2
+
+
+@pytest.mark.skipif(_host_gb() < 96, reason="needs ~50 GB of host memory for the full-size oracle")
+@pytest.mark.parametrize("name", ["C3-25pt-wave-512", "C4-25pt-var-512"])
+def test_25pt_full_size_every_cell(name):
+    """C3 and C4 at full size and full T in the default plan: every interior cell against the oracle --
+    G1 (both levels for the wave), G5 ghosts, and G2 per cell for C4 (non-negative coefficients)."""
+    w = workloads.BY_NAME[name]
+    inp = synth.make_inputs(w.kind, w.nx, w.ny, w.nz)
+    g_new, g_old, _ = gpu_run(w.kind, w.nx, w.ny, w.nz, w.T)
+    o_new, o_old = oracle.run(inp, w.T)
+    R = inp.R
+    I = (slice(R, -R),) * 3
+    assert np.max(np.abs(g_new[I] - o_new[I])) <= 1e-11 * np.max(np.abs(o_new[I]))
+    ghost = np.ones(g_new.shape, dtype=bool)
+    ghost[I] = False
+    assert np.array_equal(g_new[ghost], inp.V[ghost])
+    if w.kind in WAVES:
+        assert np.max(np.abs(g_old[I] - o_old[I])) <= 1e-11 * np.max(np.abs(o_old[I]))
+        assert np.array_equal(g_old[ghost], inp.V[ghost])
+    else:
+        absinp = synth.Inputs(w.kind, w.nx, w.ny, w.nz, np.abs(inp.V), np.abs(inp.U), inp.coef, inp.scalars)
+        del inp
+        S, _ = oracle.run(absinp, w.T)
+        assert np.all(np.abs(g_new[I] - o_new[I]) <= 1e-11 * S[I])
