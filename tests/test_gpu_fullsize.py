@@ -152,7 +152,7 @@ def test_C2_full_size_every_cell_G1_G2_G5():
 
 
 @pytest.mark.skipif(_host_gb() < 96, reason="needs ~50 GB of host memory for the full-size oracle")
-@pytest.mark.parametrize("name", ["C3-25pt-wave-512", "C4-25pt-var-512"])
+@pytest.mark.parametrize("name", ["C3-25pt-wave-512", "C4-25pt-var-512", "C3A-25pt-wave-alpha-512"])
 def test_25pt_full_size_every_cell(name):
     """C3 and C4 at full size and full T in the default plan: every interior cell against the oracle --
     G1 (both levels for the wave), G5 ghosts, and G2 per cell for C4 (non-negative coefficients)."""
