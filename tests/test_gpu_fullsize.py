@@ -174,3 +174,23 @@ def test_25pt_full_size_every_cell(name):
         del inp
         S, _ = oracle.run(absinp, w.T)
         assert np.all(np.abs(g_new[I] - o_new[I]) <= 1e-11 * S[I])
+
+
+@pytest.mark.skipif(_host_gb() < 64, reason="needs ~30 GB of host memory for the full-size oracle")
+@pytest.mark.parametrize("name", ["C2-7pt-var-512", "C3-25pt-wave-512", "C4-25pt-var-512"])
+def test_G3_short_T_full_size(name):
+    """G3 at the full config shapes: T in {1, 2, bt-1, bt, bt+1, 2bt+1} (values still O(0.1-1) everywhere,
+    so normwise <= 1e-13 checks every level of the first blocks sharply); one oracle run snapshots
+    every T."""
+    w = workloads.BY_NAME[name]
+    inp = synth.make_inputs(w.kind, w.nx, w.ny, w.nz)
+    with st.Grid(w.kind, w.nx, w.ny, w.nz, seed=synth.DEFAULT_SEED) as g:
+        bt = g.info()["bt"]
+    Ts = sorted({t for t in (1, 2, bt - 1, bt, bt + 1, 2 * bt + 1) if t >= 1})
+    o_new, o_old = inp.V.copy(), inp.U.copy()
+    done = 0
+    for T in Ts:
+        oracle.run_arrays(w.kind, w.nx, w.ny, w.nz, o_new, o_old, inp.coef, inp.scalars, T - done)
+        done = T
+        g_new, g_old, _ = gpu_run(w.kind, w.nx, w.ny, w.nz, T)
+        assert_parity(w.kind, g_new, g_old, o_new, o_old, inp.R, 1e-13)
