@@ -80,6 +80,7 @@ def test_512_full_T_bitwise_vs_naive(name):
 
 def _fits(bytes_needed):
     import torch
+    torch.cuda.empty_cache()  # earlier tests' grids return their memory to torch's cache, not the driver
     free, _ = torch.cuda.mem_get_info()
     return free > bytes_needed * 1.05
 
@@ -194,3 +195,23 @@ def test_G3_short_T_full_size(name):
         done = T
         g_new, g_old, _ = gpu_run(w.kind, w.nx, w.ny, w.nz, T)
         assert_parity(w.kind, g_new, g_old, o_new, o_old, inp.R, 1e-13)
+
+
+@pytest.mark.parametrize("halo", [st.ST_HALO_PEER, st.ST_HALO_COPY])
+def test_C5_full_size_eight_slabs_bitwise(halo):
+    """C5 (1024^3, T = 200) in BASELINE.json's 8-way z-slab decomposition, all 8 slabs on this GPU
+    (loopback; fused peer-store halos or halo copies after every block): the owned planes equal the
+    single-slab run bitwise (G4 across the slab count, at the config's full size and T)."""
+    w = workloads.C5
+    R = 4
+    need = 15 * (w.nx + 2 * R + 16) * (w.ny + 2 * R) * (w.nz + 2 * R + 14 * R) * 8
+    if not _fits(need):
+        pytest.skip("C5 in 8 slabs does not fit this GPU")
+    planes = [R, R + 127, R + 128, 300, 515, 516, 900, w.nz + R - 1]  # slab seams at multiples of 128
+    res = []
+    for kw in (dict(), dict(nranks=8, local_slabs=8, halo=halo)):
+        with st.Grid(w.kind, w.nx, w.ny, w.nz, seed=synth.DEFAULT_SEED, **kw) as g:
+            g.run(w.T)
+            res.append([g.read_planes(0, z, z + 1) for z in planes])
+    for a, b in zip(*res):
+        assert np.array_equal(a, b)
