@@ -492,6 +492,22 @@ def main():
                          if world > 1 else "") +
                         ("; two-deep pipeline (step k+1's upload on a second stream overlaps step k's "
                          "run and readback)" if pipelined else ""))}
+        # the e2e's own bound: this GPU's pinned host->device bandwidth (a 1 GiB copy, best of 3) carrying
+        # the step's inputs -- the step can be no faster than its upload
+        hbuf = V.reshape(-1)[: (1 << 27)] if V.size >= (1 << 27) else V.reshape(-1)
+        hb = torch.from_numpy(hbuf)
+        db = torch.empty(hb.numel(), dtype=torch.float64, device=dev)
+        best = None
+        for _ in range(3):
+            t1 = time.perf_counter()
+            db.copy_(hb, non_blocking=True)
+            torch.cuda.synchronize()
+            dt = time.perf_counter() - t1
+            best = dt if best is None or dt < best else best
+        h2d_gbs = hb.numel() * 8 / best / 1e9
+        bound = (w.nx * w.ny * w.nz * w.T) / (h2d / (h2d_gbs * 1e9)) / 1e9 * world
+        e2e.update({"h2d_gbs": h2d_gbs, "bound_glups": bound, "frac_of_bound": e2e["value"] / bound})
+        del db, hb
         del outs
         del V, U, coeff, out
 
