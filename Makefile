@@ -11,7 +11,7 @@ CSRC      := paper_1410_3060_b200/csrc
 LIB       := paper_1410_3060_b200/libstencil.so
 OBJS      := build/kernels.o build/pipe.o build/runtime.o
 
-all: $(LIB) oracle/liboracle.so synth/libsynth.so build/fp64_peak build/tmem_probe
+all: $(LIB) oracle/liboracle.so synth/libsynth.so build/fp64_peak build/tmem_probe build/libenergy_probe.so
 
 build:
 	mkdir -p build
@@ -33,6 +33,9 @@ build/fp64_peak: tools/fp64_peak.cu | build
 
 build/tmem_probe: tools/tmem_probe.cu | build
 	$(NVCC) $(ARCH) -O3 -o $@ $<
+
+build/libenergy_probe.so: tools/energy_probe.cu | build
+	$(NVCC) $(ARCH) -O3 -Xcompiler -fPIC -shared -o $@ $<
 
 oracle/liboracle.so: oracle/oracle.c
 	gcc -O2 -ffp-contract=off -fno-fast-math -fopenmp -fPIC -shared -std=c11 -o $@ $<
