@@ -36,7 +36,7 @@ __global__ void __launch_bounds__(512, 1) k_smem(double* out, long long iters) {
   for (long long i = 0; i < iters; ++i) {
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
-      const double2 v = buf[(idx + u * 512) & 2047];
+      const double2 v = buf[(idx + u * 256) & 2047];  // 8 distinct addresses per iteration
       acc.x += v.x;
       acc.y += v.y;
     }
