@@ -520,6 +520,10 @@ def main():
         clocks = clk.summary()
         if remeasured:
             clocks["remeasured"] = remeasured
+        # what actually limits the timed region: the roofline above is HBM / FP64; a run that sat at the
+        # board's power limit with sw_power_cap active is power-bound (DESIGN.md §6's power model)
+        roofline["observed_limiter"] = ("board_power_cap" if "sw_power_cap" in (clocks.get("reasons") or [])
+                                        and (clocks.get("power_w") or 0) >= 900 else roofline["bound"])
         if clocks.get("power_w"):  # board energy per lattice update on this GPU (cf. the paper's Table 1)
             clocks["energy_nj_per_lup"] = round(clocks["power_w"] / (value / world), 3)
         line = {
