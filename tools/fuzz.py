@@ -1,0 +1,80 @@
+"""Randomised plan fuzzing on the GPU: random kind, extents, T and plan (variant, bt, tile_cfg, z-chunk,
+z-slabs with copy / peer halos), each compared bitwise with the naive sweeps (G4).  Prints one line per
+mismatch and a summary; exit code 1 if any plan disagrees.
+
+python tools/fuzz.py [--minutes 5] [--seed 1]
+"""
+import argparse
+import os
+import random
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_1410_3060_b200 as st  # noqa: E402
+import synth  # noqa: E402
+
+N_CFG = {synth.K7C: 1, synth.K7V: 10, synth.K25W: 9, synth.K25V: 4, synth.K25WA: 5}
+MAX_BT = {synth.K7C: 8, synth.K7V: 4, synth.K25W: 2, synth.K25V: 1, synth.K25WA: 1}
+
+
+def run(kind, n, T, seed, **kw):
+    with st.Grid(kind, *n, seed=seed, **kw) as g:
+        g.run(T)
+        new = g.read(0)
+        old = g.read(1) if kind in synth.WAVE_KINDS else None
+    return new, old
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--minutes", type=float, default=5.0)
+    ap.add_argument("--seed", type=int, default=1)
+    a = ap.parse_args()
+    torch.cuda.set_device(0)
+    rnd = random.Random(a.seed)
+    t_end = time.time() + 60 * a.minutes
+    cases = bad = 0
+    while time.time() < t_end:
+        kind = rnd.choice(list(N_CFG))
+        R = synth.RADIUS[kind]
+        big = rnd.random() < 0.2
+        n = tuple(rnd.randint(1, 300 if big else 90) for _ in range(3))
+        T = rnd.randint(1, 13)
+        seed = rnd.randint(1, 10**6)
+        v = rnd.choice(["pipe", "pipe", "pipe", "stream", "coop", "slabs"])
+        kw = {}
+        if v == "pipe":
+            kw = dict(variant=st.ST_VARIANT_PIPE, bt=rnd.randint(1, MAX_BT[kind]), tile_cfg=rnd.randrange(N_CFG[kind]),
+                      zchunk=rnd.choice([0, 0, rnd.randint(1, 64)]))
+        elif v == "stream":
+            kw = dict(variant=st.ST_VARIANT_STREAM, bt=rnd.randint(1, 2), zchunk=rnd.choice([0, rnd.randint(1, 64)]))
+        elif v == "coop":
+            kw = dict(variant=st.ST_VARIANT_COOP, tile_cfg=2 if kind in (synth.K7C, synth.K7V) and rnd.random() < 0.3 else 0)
+        else:
+            P = rnd.randint(2, 5)
+            if n[2] < P * R:
+                continue
+            kw = dict(nranks=P, local_slabs=P, halo=rnd.choice([st.ST_HALO_COPY, st.ST_HALO_PEER]),
+                      bt=rnd.randint(1, MAX_BT[kind]))
+        try:
+            got = run(kind, n, T, seed, **kw)
+        except st.StencilError as e:  # plans the library rejects (e.g. slabs thinner than R) are fine
+            print(f"rejected {synth.KIND_NAMES[kind]} {n} T={T} {kw}: {str(e)[:90]}", flush=True)
+            continue
+        ref = run(kind, n, T, seed, variant=st.ST_VARIANT_NAIVE)
+        cases += 1
+        ok = np.array_equal(got[0], ref[0]) and (got[1] is None or np.array_equal(got[1], ref[1]))
+        if not ok:
+            bad += 1
+            print(f"MISMATCH {synth.KIND_NAMES[kind]} {n} T={T} seed={seed} {kw}", flush=True)
+        torch.cuda.empty_cache()
+    print(f"fuzz done: {cases} plans, {bad} mismatches", flush=True)
+    sys.exit(1 if bad else 0)
+
+
+if __name__ == "__main__":
+    main()
