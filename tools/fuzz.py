@@ -23,7 +23,8 @@ MAX_BT = {synth.K7C: 8, synth.K7V: 4, synth.K25W: 2, synth.K25V: 1, synth.K25WA:
 
 def run(kind, n, T, seed, **kw):
     with st.Grid(kind, *n, seed=seed, **kw) as g:
-        g.run(T)
+        for t in (T if isinstance(T, tuple) else (T,)):  # consecutive stencil_run calls
+            g.run(t)
         new = g.read(0)
         old = g.read(1) if kind in synth.WAVE_KINDS else None
     return new, old
@@ -44,6 +45,9 @@ def main():
         big = rnd.random() < 0.2
         n = tuple(rnd.randint(1, 300 if big else 90) for _ in range(3))
         T = rnd.randint(1, 13)
+        if rnd.random() < 0.3:  # the same steps split over 2-3 runs (state and remainder blocks carry over)
+            cuts = sorted(rnd.sample(range(1, T), min(T - 1, rnd.randint(1, 2)))) if T > 1 else []
+            T = tuple(b - a for a, b in zip([0] + cuts, cuts + [T]))
         seed = rnd.randint(1, 10**6)
         v = rnd.choice(["pipe", "pipe", "pipe", "stream", "coop", "slabs"])
         kw = {}
@@ -65,7 +69,7 @@ def main():
         except st.StencilError as e:  # plans the library rejects (e.g. slabs thinner than R) are fine
             print(f"rejected {synth.KIND_NAMES[kind]} {n} T={T} {kw}: {str(e)[:90]}", flush=True)
             continue
-        ref = run(kind, n, T, seed, variant=st.ST_VARIANT_NAIVE)
+        ref = run(kind, n, sum(T) if isinstance(T, tuple) else T, seed, variant=st.ST_VARIANT_NAIVE)
         cases += 1
         ok = np.array_equal(got[0], ref[0]) and (got[1] is None or np.array_equal(got[1], ref[1]))
         if not ok:
