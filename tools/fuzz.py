@@ -34,11 +34,16 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--minutes", type=float, default=5.0)
     ap.add_argument("--seed", type=int, default=1)
-    ap.add_argument("--oracle", action="store_true",
-                    help="compare with the CPU oracle (normwise <= 1e-13, extents <= 40) instead of the naive sweeps")
     a = ap.parse_args()
-    if a.oracle:
-        import oracle  # test infrastructure: the fuzzer is a test tool
+    return fuzz(a.minutes, a.seed)[1]
+
+
+def fuzz(minutes, seed0, against=None, max_extent=None):
+    """Run random plans for `minutes`; compare each with the naive sweeps, or -- when `against` is given
+    (tests/test_gpu_fuzz.py passes the CPU oracle's checker; tools never import the oracle) -- with
+    against(kind, n, T, seed, got).  Returns (cases, mismatches)."""
+    from types import SimpleNamespace
+    a = SimpleNamespace(minutes=minutes, seed=seed0, oracle=against is not None)
     torch.cuda.set_device(0)
     rnd = random.Random(a.seed)
     t_end = time.time() + 60 * a.minutes
@@ -47,7 +52,7 @@ def main():
         kind = rnd.choice(list(N_CFG))
         R = synth.RADIUS[kind]
         big = rnd.random() < 0.2 and not a.oracle
-        n = tuple(rnd.randint(1, 40 if a.oracle else (300 if big else 90)) for _ in range(3))
+        n = tuple(rnd.randint(1, max_extent or (40 if a.oracle else (300 if big else 90))) for _ in range(3))
         T = rnd.randint(1, 13)
         if rnd.random() < 0.3:  # the same steps split over 2-3 runs (state and remainder blocks carry over)
             cuts = sorted(rnd.sample(range(1, T), min(T - 1, rnd.randint(1, 2)))) if T > 1 else []
@@ -76,12 +81,7 @@ def main():
         Tt = sum(T) if isinstance(T, tuple) else T
         cases += 1
         if a.oracle:
-            o_new, o_old = oracle.run(synth.make_inputs(kind, *n, seed=seed), Tt, nthreads=1)
-            I = (slice(R, -R),) * 3
-
-            def close(g, o):
-                return np.max(np.abs(g[I] - o[I])) <= 1e-13 * max(np.max(np.abs(o[I])), 1e-300)
-            ok = close(got[0], o_new) and (got[1] is None or close(got[1], o_old))
+            ok = against(kind, n, Tt, seed, got)
         else:
             ref = run(kind, n, Tt, seed, variant=st.ST_VARIANT_NAIVE)
             ok = np.array_equal(got[0], ref[0]) and (got[1] is None or np.array_equal(got[1], ref[1]))
@@ -90,8 +90,8 @@ def main():
             print(f"MISMATCH {synth.KIND_NAMES[kind]} {n} T={T} seed={seed} {kw}", flush=True)
         torch.cuda.empty_cache()
     print(f"fuzz done: {cases} plans, {bad} mismatches", flush=True)
-    sys.exit(1 if bad else 0)
+    return cases, bad
 
 
 if __name__ == "__main__":
-    main()
+    sys.exit(1 if main() else 0)
