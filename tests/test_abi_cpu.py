@@ -116,3 +116,25 @@ def test_stencil_generate_equals_synth(kind):
     if kind not in synth.WAVE_KINDS:
         with pytest.raises(st.StencilError):
             st.stencil_generate(kind, *n, 77, 1)
+
+
+def test_host_slab_binding_checks():
+    """st_opts.host_slab (a rank's host arrays hold only its stored planes): the binding sizes the arrays
+    with stencil_plan_slab and refuses a missing bt, a single rank, and arrays of the wrong size -- all
+    before any device work (the library repeats the bt / rank rule for C callers)."""
+    import synth
+    kind, n = synth.K7V, (8, 8, 12)
+    o = st.stencil_opts_default()
+    o.nranks, o.rank, o.host_slab = 2, 1, 1
+    pl = st.stencil_plan_slab(n[2], 1, 2, 1, 2)
+    box = ((pl["store_z0"], pl["store_z1"]), (0, 10), (0, 10))
+    loc = synth.make_inputs(kind, *n, seed=1, box=box)
+    full = synth.make_inputs(kind, *n, seed=1)
+    with pytest.raises(ValueError):  # bt = 0: the stored range is not known in advance
+        st.stencil_create(kind, *n, list(loc.coef), loc.V, None, o)
+    o.bt = 2
+    with pytest.raises(ValueError):  # the global arrays are not this rank's planes
+        st.stencil_create(kind, *n, list(full.coef), full.V, None, o)
+    o.nranks = 1
+    with pytest.raises(ValueError):
+        st.stencil_create(kind, *n, list(loc.coef), loc.V, None, o)
