@@ -134,6 +134,14 @@ class ClockSampler:
         return out
 
 
+def observed_limiter(clocks, bound):
+    """'board_power_cap' when the timed region sat at the board's power limit with sw_power_cap active,
+    else the roofline's own bound."""
+    if "sw_power_cap" in (clocks.get("reasons") or []) and (clocks.get("power_w") or 0) >= 900:
+        return "board_power_cap"
+    return bound
+
+
 def load_fp64_peak():
     """Measured FP64 FMA throughput (tools/fp64_peak.cu -> profiles/fp64_peak.json), TFLOP/s."""
     try:
@@ -522,8 +530,7 @@ def main():
             clocks["remeasured"] = remeasured
         # what actually limits the timed region: the roofline above is HBM / FP64; a run that sat at the
         # board's power limit with sw_power_cap active is power-bound (DESIGN.md §6's power model)
-        roofline["observed_limiter"] = ("board_power_cap" if "sw_power_cap" in (clocks.get("reasons") or [])
-                                        and (clocks.get("power_w") or 0) >= 900 else roofline["bound"])
+        roofline["observed_limiter"] = observed_limiter(clocks, roofline["bound"])
         if clocks.get("power_w"):  # board energy per lattice update on this GPU (cf. the paper's Table 1)
             clocks["energy_nj_per_lup"] = round(clocks["power_w"] / (value / world), 3)
         line = {

@@ -41,3 +41,10 @@ def test_pick_workload_weak_and_strong():
 def test_slowdown_reasons_trigger_a_second_measurement():
     assert {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"} <= bench.SLOWDOWN_REASONS
     assert "sw_power_cap" not in bench.SLOWDOWN_REASONS  # kept and noted, not re-measured
+
+
+def test_observed_limiter():
+    assert bench.observed_limiter({"reasons": ["sw_power_cap"], "power_w": 1040.0}, "hbm") == "board_power_cap"
+    assert bench.observed_limiter({"reasons": ["sw_power_cap"], "power_w": 480.0}, "hbm") == "hbm"  # a 1-s average
+    assert bench.observed_limiter({"reasons": [], "power_w": 1000.0}, "hbm") == "hbm"
+    assert bench.observed_limiter({}, "fp64") == "fp64"
