@@ -34,11 +34,13 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--minutes", type=float, default=5.0)
     ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--max-extent", type=int, default=0, help="largest extent per axis (0: 90, a fifth up to 300)")
+    ap.add_argument("--max-cells", type=float, default=3e7, help="skip shapes with more interior cells")
     a = ap.parse_args()
-    return fuzz(a.minutes, a.seed)[1]
+    return fuzz(a.minutes, a.seed, max_extent=a.max_extent or None, max_cells=a.max_cells)[1]
 
 
-def fuzz(minutes, seed0, against=None, max_extent=None):
+def fuzz(minutes, seed0, against=None, max_extent=None, max_cells=3e7):
     """Run random plans for `minutes`; compare each with the naive sweeps, or -- when `against` is given
     (tests/test_gpu_fuzz.py passes the CPU oracle's checker; tools never import the oracle) -- with
     against(kind, n, T, seed, got).  Returns (cases, mismatches)."""
@@ -53,6 +55,8 @@ def fuzz(minutes, seed0, against=None, max_extent=None):
         R = synth.RADIUS[kind]
         big = rnd.random() < 0.2 and not a.oracle
         n = tuple(rnd.randint(1, max_extent or (40 if a.oracle else (300 if big else 90))) for _ in range(3))
+        if n[0] * n[1] * n[2] > max_cells:
+            continue
         T = rnd.randint(1, 13)
         if rnd.random() < 0.3:  # the same steps split over 2-3 runs (state and remainder blocks carry over)
             cuts = sorted(rnd.sample(range(1, T), min(T - 1, rnd.randint(1, 2)))) if T > 1 else []
