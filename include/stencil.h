@@ -82,7 +82,9 @@ enum {
                             mbarriers; persistent CTAs.  The default. */
   ST_VARIANT_COOP = 4    /* small, latency-bound grids (their arrays fit in L2): all T steps of a
                             stencil_run in ONE cooperative launch, a grid-wide barrier between
-                            sweeps.  Single slab only.  Auto-selected below a size threshold. */
+                            sweeps.  Single slab only.  Auto-selected below a size threshold.
+                            tile_cfg 2 (7-point Jacobi kinds): temporal blocking in shared memory,
+                            one grid barrier per round of 5 levels. */
 };
 
 /* Halo exchange between z-slabs. */
