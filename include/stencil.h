@@ -113,7 +113,9 @@ typedef struct {
   int device;          /* CUDA ordinal; -1 = the current device */
   int variant;         /* ST_VARIANT_*; 0 = auto */
   int bt;              /* time-block depth (levels fused per launch); 0 = auto; >= 1 otherwise */
-  int tile_cfg;        /* kernel tile configuration index of the variant (0 = default) */
+  int tile_cfg;        /* kernel tile configuration index of the variant (0 = default; an index the
+                          pipe / stream variants do not define selects the default; ST_VARIANT_COOP
+                          accepts 0, 1 and, for the 7-point Jacobi kinds, 2 -- else ST_E_INVAL) */
   int local_slabs;     /* z-slabs held by this handle: 1 (one slab per process and GPU; neighbours
                           exchange halos with NCCL), or nranks with rank = 0 ("loopback": all slabs
                           on this handle's device, halos exchanged by device copies -- the multi-GPU
@@ -222,8 +224,10 @@ int stencil_read_planes(stencil_ctx *h, int level, int64_t z0, int64_t z1, doubl
 
 /* Overwrite a level from a dense padded GLOBAL host array (interior and ghosts of this rank's
  * stored planes) -- with opts->host_slab, from an array of this rank's stored planes only.  Used for
- * checkpoint/resume and the end-to-end upload path.  level 1 only for the wave.  Writing level 0 of a
- * Jacobi kind also resets level 1's ghosts to the new ghosts.  ST_E_INVAL if in_elems is too small. */
+ * checkpoint/resume and the end-to-end upload path.  level 1 only for the wave.  The fixed boundary
+ * is level 0's ghost shell: writing level 0 also resets the other buffers' ghosts to the new ghosts;
+ * writing level 1 (wave) uses only the interior of `in` (its ghosts stay level 0's, as u0 in
+ * stencil_create).  ST_E_INVAL if in_elems is too small. */
 int stencil_write(stencil_ctx *h, int level, const double *in, int64_t in_elems);
 
 /* Plan and state of a handle. */
@@ -251,6 +255,8 @@ int stencil_nccl_unique_id(void *out, size_t out_bytes);
  * ranks.  Outputs (global padded plane indices): [*own_z0, *own_z1) the planes rank owns (its
  * interior slab, plus the bottom / top R ghost planes on the first / last rank);
  * [*store_z0, *store_z1) the planes it stores (owned + halo of depth R*bt on internal sides).
+ * With st_opts.host_slab the handle must run at exactly this bt: stencil_create returns ST_E_INVAL
+ * when the kind / variant caps bt lower (the stored range would differ from the caller's arrays).
  * bt is clamped to max(1, min(bt, thinnest slab / R)) and returned in *bt_eff, so halo data always
  * comes from the adjacent rank only.  ST_E_INVAL if nz < nranks or (nranks > 1 and a slab is
  * thinner than R planes).

@@ -33,25 +33,27 @@ template <int KIND>
 __global__ void __launch_bounds__(256) naive_kernel(const KParams p) {
   constexpr int R = Traits<KIND>::R, NC = Traits<KIND>::NCOEF;
   const int x = blockIdx.x * 32 + threadIdx.x + R;
-  const int y = blockIdx.y * 8 + threadIdx.y + R;
-  const int z = p.zo0 + blockIdx.z;
-  if (x >= p.nx + R || y >= p.ny + R) return;
-  const long long i = (long long)z * p.plane + (long long)y * p.pitch + x;
-  double m[3][R], pl[3][R];
+  if (x >= p.nx + R) return;
+  // grid-stride over y and z: the launch caps grid.y / grid.z at 65535 (tall grids, thick slabs)
+  for (int z = p.zo0 + (int)blockIdx.z; z < p.zo1; z += (int)gridDim.z)
+    for (int y = (int)blockIdx.y * 8 + (int)threadIdx.y + R; y < p.ny + R; y += (int)gridDim.y * 8) {
+      const long long i = (long long)z * p.plane + (long long)y * p.pitch + x;
+      double m[3][R], pl[3][R];
 #pragma unroll
-  for (int r = 1; r <= R; ++r) {
-    m[0][r - 1] = p.src[i - r];
-    pl[0][r - 1] = p.src[i + r];
-    m[1][r - 1] = p.src[i - r * p.pitch];
-    pl[1][r - 1] = p.src[i + r * p.pitch];
-    m[2][r - 1] = p.src[i - r * p.plane];
-    pl[2][r - 1] = p.src[i + r * p.plane];
-  }
-  double W[NC > 0 ? NC : 1];
+      for (int r = 1; r <= R; ++r) {
+        m[0][r - 1] = p.src[i - r];
+        pl[0][r - 1] = p.src[i + r];
+        m[1][r - 1] = p.src[i - r * p.pitch];
+        pl[1][r - 1] = p.src[i + r * p.pitch];
+        m[2][r - 1] = p.src[i - r * p.plane];
+        pl[2][r - 1] = p.src[i + r * p.plane];
+      }
+      double W[NC > 0 ? NC : 1];
 #pragma unroll
-  for (int k = 0; k < NC; ++k) W[k] = p.coef[k * p.cstride + i];
-  const double u = Traits<KIND>::WAVE ? p.srcu[i] : 0.0;
-  p.dst[i] = apply_point<KIND, R>(p.src[i], u, m, pl, W, p.s);
+      for (int k = 0; k < NC; ++k) W[k] = p.coef[k * p.cstride + i];
+      const double u = Traits<KIND>::WAVE ? p.srcu[i] : 0.0;
+      p.dst[i] = apply_point<KIND, R>(p.src[i], u, m, pl, W, p.s);
+    }
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -463,20 +465,22 @@ __global__ void fill_kernel(double* base, long long pitch, long long plane, int 
                             long long GX, long long GY, long long GZ, int R, uint64_t key,
                             uint64_t key_u, int mode, double c) {
   const long long x = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const long long y = blockIdx.y;
-  const long long z = blockIdx.z;
-  if (x >= GX || z >= zl) return;
-  const long long gz = gz0 + z;
-  const uint64_t idx = (uint64_t)((gz * GY + y) * GX + x);
-  double v;
-  if (mode == 2) {
-    v = synth_scaled(key, idx, c);
-  } else if (mode == 1 && x >= R && x < GX - R && y >= R && y < GY - R && gz >= R && gz < GZ - R) {
-    v = synth_sym(key_u, idx);
-  } else {
-    v = synth_sym(key, idx);
-  }
-  base[z * plane + y * pitch + x] = v;
+  if (x >= GX) return;
+  // grid-stride over y and z (grid.y / grid.z are capped at 65535 by the launch)
+  for (long long z = blockIdx.z; z < zl; z += gridDim.z)
+    for (long long y = blockIdx.y; y < GY; y += gridDim.y) {
+      const long long gz = gz0 + z;
+      const uint64_t idx = (uint64_t)((gz * GY + y) * GX + x);
+      double v;
+      if (mode == 2) {
+        v = synth_scaled(key, idx, c);
+      } else if (mode == 1 && x >= R && x < GX - R && y >= R && y < GY - R && gz >= R && gz < GZ - R) {
+        v = synth_sym(key_u, idx);
+      } else {
+        v = synth_sym(key, idx);
+      }
+      base[z * plane + y * pitch + x] = v;
+    }
 }
 
 cudaError_t launch_fill(double* base, long long pitch, long long plane, int zl, long long gz0,
@@ -484,10 +488,34 @@ cudaError_t launch_fill(double* base, long long pitch, long long plane, int zl, 
                         int mode, double c, cudaStream_t cs) {
   if (zl <= 0) return cudaSuccess;
   dim3 block(128);
-  dim3 grid((unsigned)((GX + 127) / 128), (unsigned)GY, (unsigned)zl);
+  dim3 grid((unsigned)((GX + 127) / 128), (unsigned)std::min<long long>(GY, 65535),
+            (unsigned)std::min(zl, 65535));
   const uint64_t key = synth_key(seed, mode == 1 ? SYNTH_STREAM_V : stream);
   const uint64_t key_u = synth_key(seed, SYNTH_STREAM_U);
   fill_kernel<<<grid, block, 0, cs>>>(base, pitch, plane, zl, gz0, GX, GY, GZ, R, key, key_u, mode, c);
+  return cudaGetLastError();
+}
+
+// Copy the cells of the global ghost shell (width R) of local planes [0, zl) from src to dst (same
+// layout); interior cells are left alone.
+__global__ void ghost_copy_kernel(double* dst, const double* src, long long pitch, long long plane, int zl,
+                                  long long gz0, long long GX, long long GY, long long GZ, int R) {
+  const long long x = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= GX) return;
+  for (long long z = blockIdx.z; z < zl; z += gridDim.z)
+    for (long long y = blockIdx.y; y < GY; y += gridDim.y) {
+      const long long gz = gz0 + z;
+      if (x >= R && x < GX - R && y >= R && y < GY - R && gz >= R && gz < GZ - R) continue;
+      const long long o = z * plane + y * pitch + x;
+      dst[o] = src[o];
+    }
+}
+
+cudaError_t launch_ghost_copy(double* dst, const double* src, long long pitch, long long plane, int zl,
+                              long long gz0, long long GX, long long GY, long long GZ, int R, cudaStream_t cs) {
+  if (zl <= 0) return cudaSuccess;
+  dim3 grid((unsigned)((GX + 127) / 128), (unsigned)std::min<long long>(GY, 65535), (unsigned)std::min(zl, 65535));
+  ghost_copy_kernel<<<grid, 128, 0, cs>>>(dst, src, pitch, plane, zl, gz0, GX, GY, GZ, R);
   return cudaGetLastError();
 }
 
@@ -496,7 +524,7 @@ cudaError_t launch_naive(int kind, const KParams& p, cudaStream_t stream, Launch
   const int planes = p.zo1 - p.zo0;
   if (planes <= 0) return cudaSuccess;
   dim3 block(32, 8);
-  dim3 grid((p.nx + 31) / 32, (p.ny + 7) / 8, planes);
+  dim3 grid((p.nx + 31) / 32, std::min((p.ny + 7) / 8, 65535), std::min(planes, 65535));
   switch (kind) {
     case K7C: naive_kernel<K7C><<<grid, block, 0, stream>>>(p); break;
     case K7V: naive_kernel<K7V><<<grid, block, 0, stream>>>(p); break;

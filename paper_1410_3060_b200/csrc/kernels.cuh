@@ -99,4 +99,9 @@ cudaError_t launch_fill(double* base, long long pitch, long long plane, int zl, 
                         long long GX, long long GY, long long GZ, int R, uint64_t seed, int stream,
                         int mode, double c, cudaStream_t cs);
 
+// Copy the global ghost shell (width R) of local planes [0, zl) of one padded array into another of
+// the same layout (stencil_write keeps every buffer's fixed boundary equal to level 0's).
+cudaError_t launch_ghost_copy(double* dst, const double* src, long long pitch, long long plane, int zl,
+                              long long gz0, long long GX, long long GY, long long GZ, int R, cudaStream_t cs);
+
 }  // namespace st

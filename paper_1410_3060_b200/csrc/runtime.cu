@@ -349,6 +349,12 @@ int create_common(stencil_ctx** out, int kind, int64_t nx, int64_t ny, int64_t n
     set_err("ST_VARIANT_COOP runs a single slab (nranks = 1)");
     return ST_E_INVAL;
   }
+  if (o.variant == ST_VARIANT_COOP &&
+      (o.tile_cfg > 2 || (o.tile_cfg == 2 && kind != ST_7PT_CONST && kind != ST_7PT_VAR))) {
+    set_err("ST_VARIANT_COOP: tile_cfg %d is not defined for kind %d (0, 1; 2 for the 7-point Jacobi kinds)",
+            o.tile_cfg, kind);
+    return ST_E_INVAL;
+  }
   if (o.halo == ST_HALO_PEER && o.variant != ST_VARIANT_AUTO && o.variant != ST_VARIANT_PIPE) {
     set_err("halo mode ST_HALO_PEER needs the pipe variant (got variant %d)", o.variant);
     return ST_E_INVAL;
@@ -399,6 +405,13 @@ int create_common(stencil_ctx** out, int kind, int64_t nx, int64_t ny, int64_t n
   const int bt_cap = h->variant == ST_VARIANT_PIPE ? st::max_pipe_bt(kind)
                    : h->variant == ST_VARIANT_STREAM ? st::max_stream_bt(kind) : 1;
   bt = std::min(bt, std::max(1, bt_cap));
+  if (o.host_slab && bt != o.bt) {
+    // the caller sized its host arrays with stencil_plan_slab(..., o.bt): a different depth would shift
+    // every stored plane by R*(o.bt - bt) (the stored range is [lo - R*bt, hi + R*bt))
+    set_err("host_slab: bt=%d is not available for kind %d with variant %d (at most %d); size the host arrays "
+            "for an available bt", o.bt, kind, h->variant, bt);
+    return ST_E_INVAL;
+  }
   h->slabs.resize(local);
   for (int i = 0; i < local; ++i) {
     int bt_eff = 1;
@@ -1049,15 +1062,22 @@ int stencil_run(stencil_ctx* h, int64_t T) {
     p.dst = h->at(s, h->lv1);
     cudaEvent_t ev_end = nullptr;
     cudaEvent_t ev_begin = timing_begin(h, &ev_end);
-    int swaps = 0;
-    const cudaError_t le = st::launch_coop(h->kind, p, (int)std::min<int64_t>(T, 1 << 30), h->num_sms, h->tile_cfg,
-                                           h->stream, &h->last_launch, &swaps);
+    // one launch per 2^30 steps (the kernel's step counter is an int)
+    for (int64_t left = T; left > 0;) {
+      const int Tl = (int)std::min<int64_t>(left, 1 << 30);
+      p.src = h->at(s, h->lv0);
+      p.srcu = h->at(s, h->lv1);
+      p.dst = h->at(s, h->lv1);
+      int swaps = 0;
+      const cudaError_t le = st::launch_coop(h->kind, p, Tl, h->num_sms, h->tile_cfg, h->stream, &h->last_launch, &swaps);
+      if (le != cudaSuccess) return cuda_fail(h, le, "cooperative launch");
+      h->launches++;
+      if (swaps & 1) std::swap(h->lv0, h->lv1);
+      h->steps += Tl;
+      h->blocks += Tl;
+      left -= Tl;
+    }
     if (ev_begin) cudaEventRecord(ev_end, h->stream);
-    if (le != cudaSuccess) return cuda_fail(h, le, "cooperative launch");
-    h->launches++;
-    if (swaps & 1) std::swap(h->lv0, h->lv1);
-    h->steps += T;
-    h->blocks += T;
     return ST_OK;
   }
   const int bt = h->variant == ST_VARIANT_NAIVE ? 1 : h->bt;
@@ -1162,10 +1182,15 @@ int stencil_write(stencil_ctx* h, int level, const double* in, int64_t in_elems)
     if (e == cudaSuccess) e = stage.upload(s, s.buf[dstb], in);
     if (e == cudaSuccess && level == 0 && !is_wave(h->kind))  // keep level 1's ghosts equal to the new ghosts
       e = cudaMemcpyAsync(s.buf[h->lv1], s.buf[dstb], bytes, cudaMemcpyDeviceToDevice, h->stream);
-    if (e == cudaSuccess && is_wave(h->kind) && h->nbuf == 4 && level == 0)
-      for (int b = 0; b < 4 && e == cudaSuccess; ++b)
-        if (b != h->lv0 && b != h->lv1)  // spare buffers' ghosts
-          e = cudaMemcpyAsync(s.buf[b], s.buf[dstb], bytes, cudaMemcpyDeviceToDevice, h->stream);
+    if (is_wave(h->kind)) {
+      // the fixed boundary is level 0's ghost shell in every buffer (reading Q9, as stencil_create does
+      // with v0): a level-0 write hands its ghosts to level 1 (and the spare buffers), a level-1 write
+      // keeps only its interior
+      for (int b = 0; b < h->nbuf && e == cudaSuccess; ++b)
+        if (b != h->lv0 && (level == 0 || b == h->lv1))
+          e = st::launch_ghost_copy(s.buf[b] + h->xoff, s.buf[h->lv0] + h->xoff, h->pitch, h->plane, (int)s.zl,
+                                    s.store_z0, h->X, h->Y, h->nz + 2 * h->R, h->R, h->stream);
+    }
   }
   if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
   if (e != cudaSuccess) return cuda_fail(h, e, "write");

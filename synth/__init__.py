@@ -70,16 +70,22 @@ def lib():
     return _lib_handle
 
 
-def fill_box(seed: int, stream: int, dims, box=None, scale: float | None = None) -> np.ndarray:
+def fill_box(seed: int, stream: int, dims, box=None, scale: float | None = None,
+             out: np.ndarray | None = None) -> np.ndarray:
     """Draw stream `stream` over `box` = ((z0,z1),(y0,y1),(x0,x1)) of a global padded grid `dims`=(Z,Y,X).
 
-    scale None -> U[-1,1); else U[0, scale).
+    scale None -> U[-1,1); else U[0, scale).  out: a C-contiguous float64 array of the box's shape to
+    fill in place (e.g. pinned host memory); default a new array.
     """
     Z, Y, X = dims
     if box is None:
         box = ((0, Z), (0, Y), (0, X))
     (z0, z1), (y0, y1), (x0, x1) = box
-    out = np.empty((z1 - z0, y1 - y0, x1 - x0), dtype=np.float64)
+    shape = (z1 - z0, y1 - y0, x1 - x0)
+    if out is None:
+        out = np.empty(shape, dtype=np.float64)
+    elif out.shape != shape or out.dtype != np.float64 or not out.flags.c_contiguous:
+        raise ValueError(f"out must be a C-contiguous float64 array of shape {shape}")
     rc = lib().synth_fill_box(seed, stream, 0 if scale is None else 1, 0.0 if scale is None else scale,
                               Z, Y, X, z0, z1, y0, y1, x0, x1, out.ctypes.data)
     if rc != 0:

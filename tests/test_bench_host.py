@@ -48,3 +48,40 @@ def test_observed_limiter():
     assert bench.observed_limiter({"reasons": ["sw_power_cap"], "power_w": 480.0}, "hbm") == "hbm"  # a 1-s average
     assert bench.observed_limiter({"reasons": [], "power_w": 1000.0}, "hbm") == "hbm"
     assert bench.observed_limiter({}, "fp64") == "fp64"
+
+
+def test_default_headline_is_the_metric_config():
+    # BASELINE.json quotes GLUP/s "at 1/2/4/8 B200" on config 5 (C5, 1024^3, T = 200)
+    w = bench.pick_workload(bench.DEFAULT_WORKLOAD, 1)
+    assert w is workloads.C5 and (w.nx, w.ny, w.nz, w.T) == (1024, 1024, 1024, 200)
+    w = bench.pick_workload(bench.DEFAULT_WORKLOAD, 4, "strong")
+    assert (w.nx, w.ny, w.nz) == (1024, 1024, 1024)
+
+
+def test_both_arms_share_the_config_keys():
+    w = bench.pick_workload("C5", 2, "weak")
+    c = bench.workload_config(w, 2, "weak")
+    assert c["workload"] == w.name and c["nz"] == 512 and c["T"] == 200
+    assert c["parallelism"] == "z-slab x2"
+    assert c == bench.workload_config(bench.pick_workload("C5", 2, "weak"), 2, "weak")
+
+
+def test_oracle_sample_is_a_bounded_z_slab():
+    # C5's 1024^3 inputs need 132 GB of host memory: the oracle is timed on whole xy planes of a z-slab
+    assert bench.sample_planes(workloads.C5) == 96
+    assert bench.sample_planes(workloads.C2) == 384
+    assert bench.sample_planes(workloads.C1) == 64  # small grids: the full grid
+
+
+def test_gpus_2_spawns_two_ranks():
+    # `bench.py --gpus 2` without torchrun re-launches itself as 2 ranks (here: gloo, no GPU work)
+    import json
+    import os
+    import subprocess
+    import sys
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, os.path.join(bench.ROOT, "bench.py"), "--gpus", "2", "--probe-launch"],
+                       capture_output=True, text=True, timeout=300, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1 and lines[0]["world"] == 2 and sorted(lines[0]["ranks"]) == [0, 1]
