@@ -9,7 +9,7 @@ ARCH      := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall -Xptxas -v -I$(NCCL_INC)
 CSRC      := paper_1410_3060_b200/csrc
 LIB       := paper_1410_3060_b200/libstencil.so
-OBJS      := build/kernels.o build/pipe.o build/runtime.o
+OBJS      := build/kernels.o build/pipe.o build/pipe25.o build/runtime.o
 
 all: $(LIB) oracle/liboracle.so synth/libsynth.so build/fp64_peak build/tmem_probe build/libenergy_probe.so
 
@@ -19,8 +19,11 @@ build:
 build/kernels.o: $(CSRC)/kernels.cu $(CSRC)/kernels.cuh $(CSRC)/point.cuh synth/synth.h | build
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> build/kernels.ptxas.log || (cat build/kernels.ptxas.log; false)
 
-build/pipe.o: $(CSRC)/pipe.cu $(CSRC)/kernels.cuh $(CSRC)/point.cuh | build
+build/pipe.o: $(CSRC)/pipe.cu $(CSRC)/kernels.cuh $(CSRC)/point.cuh $(CSRC)/sm100.cuh | build
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> build/pipe.ptxas.log || (cat build/pipe.ptxas.log; false)
+
+build/pipe25.o: $(CSRC)/pipe25.cu $(CSRC)/kernels.cuh $(CSRC)/point.cuh $(CSRC)/sm100.cuh | build
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> build/pipe25.ptxas.log || (cat build/pipe25.ptxas.log; false)
 
 build/runtime.o: $(CSRC)/runtime.cu $(CSRC)/kernels.cuh include/stencil.h | build
 	$(NVCC) $(NVFLAGS) -c $< -o $@

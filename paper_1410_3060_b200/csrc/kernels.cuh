@@ -1,6 +1,7 @@
 // kernels.cuh -- launch interface between the runtime (runtime.cu) and the device kernels.
 #pragma once
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace st {
@@ -82,6 +83,17 @@ constexpr long long kMaxDoneItems = 1 << 18;  // per-item completion counters of
 cudaError_t launch_pipe(int kind, int b, const KParams& p, int zchunk_req, int num_sms, int cfg,
                         cudaStream_t stream, LaunchInfo* info);
 int max_pipe_bt(int kind);
+
+// The 25-point variable-coefficient kind with two fused levels (pipe25.cu): same contract as
+// launch_pipe for (K25V, b = 2); cfg selects a tile configuration (0 = default).
+cudaError_t launch_pipe25v2(const KParams& p, int zchunk_req, int num_sms, int cfg, cudaStream_t stream,
+                            LaunchInfo* info);
+
+// Tensor map (cuTensorMapEncodeTiled) of fp64 padded arrays in the library's layout: rank 3 (x, y, z)
+// or 4 (x, y, z, field); box bx x by x 1 (x bf).  The map covers columns [0, X) from `base` (the row
+// padding beyond the padded extent is out of bounds: zero-filled by the TMA unit, never fetched).
+bool make_tensor_map(CUtensorMap* m, const double* base, int rank, long long pitch, long long X, long long Y,
+                     long long zl, long long nfields, long long plane, long long fstride, int bx, int by, int bf);
 
 // T time steps of the whole slab in ONE cooperative launch with a grid-wide barrier between sweeps
 // (ST_VARIANT_COOP, small latency-bound grids).  p.src = Omega^t, p.dst = p.srcu = the other buffer.

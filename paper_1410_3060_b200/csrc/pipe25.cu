@@ -1,0 +1,443 @@
+// pipe25.cu -- the 25-point variable-coefficient stencil (Fig. 1d) with TWO fused
+// time levels per launch (b_t = 2): the wavefront temporal blocking of P:569-602 for the kind whose 13
+// coefficient fields made it capacity-bound on the paper's CPU (1WD needs 93 MiB of cache).
+//
+// Why a kernel of its own: in the generic pipe kernel, level k reads the coefficients of
+// plane z at step z + k*R, so a fused block must keep each coefficient plane on chip for (b_t - 1)*R = 4
+// steps: 5 planes x 13 fields x the level-1 extent >= 320 KB per CTA -- more than shared memory.  Here the
+// update of a level-2 cell is split the way its arithmetic already is (point.cuh, point_25v_xy /
+// point_25v_zterm):
+//   * the x/y half (centre + 8 x-pair + 8 y-pair terms, 9 coefficients) needs level 1's plane z only; it
+//     is computed in the SAME step that level 1 computes plane z, with the coefficient plane still in the
+//     shared-memory ring -- so every coefficient plane crosses HBM once per block and leaves shared memory
+//     after one step;
+//   * the z chain's term r needs level-1 plane z + r, computed r steps later: it is accumulated one term
+//     per step.  What a cell must carry between steps -- its pending x/y partial sums (4 planes), z chains
+//     (3 planes) and the z-coefficients they still need (10 values) -- lives in TENSOR MEMORY (TMEM,
+//     tcgen05.ld/st), as do both z-rings (level-0 and level-1 values of the last 8 planes).  Registers
+//     hold only the current step's operands.
+// The operations are exactly point_25v's (same FMA chains, same final (xy) + z add), so the results are
+// bitwise equal to every other variant (test G4).
+//
+// Per step s of a work item's z-stream (one CTA per SM, persistent; a producer warp + 6 consumer warps):
+//   producer: TMA loads into one ring slot (one full mbarrier): box A = plane s of Omega^t over the
+//     level-1 extent E1 (TX x TY; its centre column enters the z-ring), box B = plane s-R with an R-wide
+//     halo (x/y neighbours of level 1), box C = the 13 coefficient fields of plane s-R over E1 (one 4-D
+//     box); and an L2 prefetch of step s+2's A and C boxes (the ring is 2 slots deep);
+//   level 1 (all consumer warps, 2x2 cells per thread): plane q = s-R of level 1 over E1 (full point_25v),
+//     written to a shared plane;  named barrier;
+//   level 2 (the 4 warps whose rows hold output cells): x/y half of plane q, the z-chain terms of planes
+//     q-1..q-4, and the finished output plane q-4 = s-2R, streamed to HBM.
+// The output tile is (TX - 2R) x (TY - 2R) (overlapped tiles shrinking by R per level, as in pipe.cu).
+#include "kernels.cuh"
+#include "point.cuh"
+#include "sm100.cuh"
+
+#include <algorithm>
+#include <cstring>
+
+namespace st {
+
+template <int TX, int TY, int D>
+struct P25Cfg {
+  static constexpr int R = 4, NC = 13, CX = 2, CY = 2, NCELL = CX * CY;
+  static constexpr int LPR = TX / CX;             // threads per block row
+  static constexpr int NCONS = LPR * (TY / CY);   // consumer threads
+  static constexpr int NW = NCONS / 32;           // consumer warps
+  static constexpr int THREADS = NCONS + 32;      // + the producer warp
+  static constexpr int OX = TX - 2 * R, OY = TY - 2 * R;
+  static constexpr int FX = TX + 2 * R, FY = TY + 2 * R;  // box B (level-1 footprint)
+  static constexpr int AEL = TX * TY, BEL = FX * FY, CFIELD = TX * TY, CEL = NC * CFIELD;
+  static constexpr int BOFF = (AEL + 15) / 16 * 16, COFF = BOFF + (BEL + 15) / 16 * 16;
+  static constexpr int SLOT = COFF + (CEL + 15) / 16 * 16;  // doubles per ring slot (128-byte aligned parts)
+  static constexpr int PEL = TX * TY;                       // one shared level-1 plane
+  static constexpr int WROWS = 32 / LPR * CY;               // E1 rows per consumer warp
+  static constexpr int W2A = R / WROWS, W2B = (TY - R) / WROWS;  // level-2 warps: [W2A, W2B)
+  static constexpr uint32_t TX_BYTES_A = AEL * 8, TX_BYTES_BC = (BEL + CEL) * 8;
+  static constexpr size_t SMEM = 8 * ((size_t)D * SLOT + 2 * (size_t)PEL) + 8 * (2 * D + 8) + 4 * 4 + 128;
+  static_assert(TX % 16 == 0 && TY % CY == 0 && NCONS % 32 == 0 && 32 % LPR == 0, "thread layout");
+  static_assert(R % WROWS == 0 && (TY - R) % WROWS == 0, "level-2 rows must be whole warps");
+  static_assert(OX > 0 && OY > 0 && (OX & 3) == 0, "output tile (whole 32-byte sectors per row)");
+  // TMEM (512 columns x 128 lanes; warp w reaches lanes 32*(w%4)..): a level-2 warp uses columns
+  // [0, 264) of its quadrant (z-rings 128, carried state 136), another warp [448, 512) (its z-ring);
+  // no quadrant holds two warps of the same kind.
+  static_assert(W2B - W2A <= 4 && NW - (W2B - W2A) <= 4 && NW <= 8, "TMEM quadrants");
+  static_assert(SMEM <= 227 * 1024, "shared memory");
+  static_assert(SMEM > 116 * 1024, "one CTA per SM (the CTA allocates all 512 TMEM columns)");
+  static_assert(FX <= 256 && FY <= 256 && TX <= 256, "TMA box dimension limit");
+};
+
+// TMEM column map of a consumer thread (32-bit columns of its lane)
+constexpr uint32_t kColV1 = 64;   // level-1 z-ring: 2 parity regions x 4 planes x 4 cells (level-2 warps)
+constexpr uint32_t kColS1 = 128;  // carried state, 16 doubles per cell (level-2 warps)
+constexpr uint32_t kColS2 = 256;  // carried state, 1 double per cell
+constexpr uint32_t kColOther = 448;  // level-0 z-ring of a warp without level-2 rows
+
+__device__ __forceinline__ double dbl(uint32_t lo, uint32_t hi) { return __hiloint2double((int)hi, (int)lo); }
+__device__ __forceinline__ void put(uint32_t* w, double v) {
+  w[0] = (uint32_t)__double2loint(v);
+  w[1] = (uint32_t)__double2hiint(v);
+}
+
+template <int TX, int TY, int D>
+__global__ void __launch_bounds__(P25Cfg<TX, TY, D>::THREADS, 1)
+    pipe25_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+                  const __grid_constant__ CUtensorMap mapC, const KParams p, int ntx, int nty, int items) {
+  using C = P25Cfg<TX, TY, D>;
+  constexpr int R = C::R, NC = C::NC, NCONS = C::NCONS, FX = C::FX, CX = C::CX, CY = C::CY;
+
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double* ring = reinterpret_cast<double*>(smem_raw);
+  double* sP = ring + (size_t)D * C::SLOT;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sP + 2 * C::PEL);
+  uint64_t* empty = full + D;
+  uint64_t* itemFull = empty + D;
+  uint64_t* itemEmpty = itemFull + 4;
+  volatile int* itemq = reinterpret_cast<volatile int*>(itemEmpty + 4);
+
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    for (int i = 0; i < D; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], C::NW); }
+    for (int i = 0; i < 4; ++i) { mbar_init(&itemFull[i], 1); mbar_init(&itemEmpty[i], C::NW); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __shared__ uint32_t tmem_base;
+  if (tid < 32) {  // consumer warp 0 allocates all 512 columns (one CTA per SM)
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_base))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+
+  if (tid >= NCONS) {
+    // ---------------------------------------------------------------- producer warp
+    if (tid == NCONS) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&mapA) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&mapB) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&mapC) : "memory");
+      uint32_t iv = 0;
+      for (uint32_t n = 0;; ++n) {
+        const uint32_t qs = n & 3;
+        mbar_wait(&itemEmpty[qs], ((n >> 2) & 1) ^ 1);
+        int g = (int)atomicAdd(p.sched, 1u);
+        if (g >= items) g = -1;
+        itemq[qs] = g;
+        mbar_arrive(&itemFull[qs]);  // release: the id is visible to the consumers' acquire
+        if (g < 0) break;
+        if ((p.dbg & 8) && g == 0) continue;
+        const Item it = decode<R, 1, C::OX, C::OY>(g, ntx, nty, p);
+        const int xb = ((it.gx0 - R + p.xoff) & ~1) - (p.xoff & ~1);  // box B (footprint)
+        const int xa = ((it.gx0 + p.xoff) & ~1) - (p.xoff & ~1);      // boxes A, C (level-1 extent)
+        for (int s = it.s_begin; s <= it.s_end; ++s, ++iv) {
+          const uint32_t sl = iv % D;
+          mbar_wait(&empty[sl], ((iv / D) & 1) ^ 1);
+          // level 1 computes plane s - R this step only once its z-neighbours are in the ring
+          const int q = s - R;
+          const bool need1 = q >= 0 && (it.s_begin == 0 || q >= it.s_begin + R);
+          mbar_expect_tx(&full[sl], C::TX_BYTES_A + (need1 ? C::TX_BYTES_BC : 0u));
+          double* slot = ring + (size_t)sl * C::SLOT;
+          tma_load_3d(slot, &mapA, &full[sl], xa, it.gy0, s);
+          if (need1) {
+            tma_load_3d(slot + C::BOFF, &mapB, &full[sl], xb, it.gy0 - R, q);
+            tma_load_4d(slot + C::COFF, &mapC, &full[sl], xa, it.gy0, q, 0);
+          }
+          if (s + 2 <= it.s_end) {  // warm L2 for the loads two steps ahead (beyond the 2-slot ring)
+            tma_prefetch_3d(&mapA, xa, it.gy0, s + 2);
+            if (q + 2 >= 0) tma_prefetch_4d(&mapC, xa, it.gy0, q + 2, 0);
+          }
+        }
+      }
+      // every CTA has drawn its terminating id before the last one gets here: reset for the next launch
+      __threadfence();
+      if (atomicAdd(p.sched + 1, 1u) == gridDim.x - 1) {
+        p.sched[0] = 0;
+        p.sched[1] = 0;
+        __threadfence();
+      }
+    }
+    return;
+  }
+
+  // ---------------------------------------------------------------- consumers
+  const int warp = tid >> 5, lane = tid & 31;
+  const bool lvl2 = warp >= C::W2A && warp < C::W2B;  // warp-uniform
+  const int x0 = (tid % C::LPR) * CX;                  // first E1 column of this thread's 2x2 block
+  const int ly0 = (tid / C::LPR) * CY;                 // first E1 row
+  const uint32_t tq = tmem_base + ((uint32_t)((warp & 3) * 32) << 16);
+  const uint32_t colV0 = lvl2 ? 0u : kColOther;
+  uint32_t iv = 0;
+
+  for (uint32_t n = 0;; ++n) {
+    const uint32_t qs = n & 3;
+    mbar_wait(&itemFull[qs], (n >> 2) & 1);
+    const int g = itemq[qs];
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&itemEmpty[qs]);
+    if (g < 0) break;
+    if ((p.dbg & 8) && g == 0) continue;  // fault injection: work item 0 never computed
+    const Item it = decode<R, 1, C::OX, C::OY>(g, ntx, nty, p);
+    bool act1[CY][CX], outc[CY][CX];
+    long long col[CY];
+#pragma unroll
+    for (int j = 0; j < CY; ++j) {
+      const int ly = ly0 + j, gy = it.gy0 + ly;
+      col[j] = (long long)gy * p.pitch + it.gx0 + x0;
+#pragma unroll
+      for (int i = 0; i < CX; ++i) {
+        const int lx = x0 + i, gx = it.gx0 + lx;
+        act1[j][i] = gx >= R && gx < p.nx + R && gy >= R && gy < p.ny + R;
+        outc[j][i] = act1[j][i] && lx >= R && lx < TX - R && ly >= R && ly < TY - R;
+      }
+    }
+
+    for (int s = it.s_begin; s <= it.s_end; ++s, ++iv) {
+      const uint32_t sl = iv % D;
+      const double* slot = ring + (size_t)sl * C::SLOT;
+      mbar_wait(&full[sl], (iv / D) & 1);
+
+      // ---------------- level 1: plane q = s - R over the level-1 extent (all consumer warps)
+      const int q = s - R;
+      const bool zv1 = !(p.dbg & 1) && q >= p.zi0 && q < p.zi1 && (it.s_begin == 0 || q >= it.s_begin + R);
+      const double* Bb = slot + C::BOFF + R * FX + R;  // Bb[y * FX + x] = E1 cell (x, y) of plane q
+      const double* Cs = slot + C::COFF;               // Cs[f * CFIELD + y * TX + x]: field f at E1 (x, y)
+      double v1[CY][CX];
+      {
+        double ys[CY + 2 * R][CX];
+#pragma unroll
+        for (int r = 0; r < CY + 2 * R; ++r) lds_row<CX, true>(Bb + (ly0 - R + r) * FX + x0, ys[r]);
+#pragma unroll
+        for (int j = 0; j < CY; ++j) {
+          // level-0 z-ring of row j's two cells (TMEM, cell-major): planes s-8 .. s-1, k = 0 oldest
+          uint32_t zr[32];
+          tmem_ld32(tq + colV0 + 32u * j, zr);
+          double vnew[CX];  // plane s (box A): the ring's newest entry
+          lds_row<CX, true>(slot + (ly0 + j) * TX + x0, vnew);
+          double xr[R + CX + R];
+          lds_row<R, true>(Bb + (ly0 + j) * FX + x0 - R, xr);
+          lds_row<R, true>(Bb + (ly0 + j) * FX + x0 + CX, xr + R + CX);
+#pragma unroll
+          for (int i = 0; i < CX; ++i) xr[R + i] = ys[R + j][i];
+          double Wr[NC][CX];
+#pragma unroll
+          for (int f = 0; f < NC; ++f) lds_row<CX, true>(Cs + f * C::CFIELD + (ly0 + j) * TX + x0, Wr[f]);
+          tmem_wait_ld();
+          auto V0 = [&](int k, int i) -> double {  // plane s - 8 + k of cell (j, i); k = 8: plane s
+            return k == 8 ? vnew[i] : dbl(zr[16 * i + 2 * k], zr[16 * i + 2 * k + 1]);
+          };
+          uint32_t zn[32];
+#pragma unroll
+          for (int i = 0; i < CX; ++i) {
+            double m[3][R], pl[3][R], W[NC];
+#pragma unroll
+            for (int r = 1; r <= R; ++r) {
+              m[0][r - 1] = xr[R + i - r];
+              pl[0][r - 1] = xr[R + i + r];
+              m[1][r - 1] = ys[R + j - r][i];
+              pl[1][r - 1] = ys[R + j + r][i];
+              m[2][r - 1] = V0(R - r, i);
+              pl[2][r - 1] = V0(R + r, i);
+            }
+#pragma unroll
+            for (int f = 0; f < NC; ++f) W[f] = Wr[f][i];
+            const double c = V0(R, i);
+            const double v = point_25v(c, m, pl, W);
+            // ghosts, cells outside the grid and planes not computed at level 1 keep their input value
+            v1[j][i] = (zv1 && act1[j][i]) ? v : c;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) put(zn + 16 * i + 2 * k, V0(k + 1, i));  // the ring moves on a plane
+          }
+          tmem_st32(tq + colV0 + 32u * j, zn);
+        }
+      }
+      double* P = sP + (size_t)(iv & 1u) * C::PEL;  // alternate with the CTA's step counter (pipe.cu)
+#pragma unroll
+      for (int j = 0; j < CY; ++j) sts_row<CX, true>(P + (ly0 + j) * TX + x0, v1[j]);
+      if (!(p.dbg & 2)) named_sync(1, NCONS);
+
+      // ---------------- level 2: x/y half of plane q, z-chain terms of planes q-1..q-4, output plane q-4
+      if (lvl2) {
+        const uint32_t colR = kColV1 + (uint32_t)(q & 1) * 32;  // level-1 z-ring of q's parity, cell-major:
+        uint32_t s2[8], s2n[8];                                  // V1(q-2), V1(q-4), V1(q-6), V1(q-8)
+        tmem_ld8(tq + kColS2, s2);  // Z(q-2) of the 4 cells
+        double ys[CY + 2 * R][CX];
+#pragma unroll
+        for (int r = 0; r < CY + 2 * R; ++r) {
+          const int row = min(max(ly0 - R + r, 0), TY - 1);  // rows outside E1 only feed discarded cells
+          lds_row<CX, true>(P + row * TX + x0, ys[r]);
+        }
+        const int c4 = q - R;  // the plane level 2 finishes this step
+        const bool store = c4 >= it.zc0 && c4 < it.zc1 && !((p.dbg & 4) && c4 == it.zc1 - 1);
+#pragma unroll
+        for (int j = 0; j < CY; ++j) {
+          double Pq[CX];
+          {  // x/y half (point_25v_xy): W0, x and y coefficients of plane q
+            double xr[R + CX + R];
+            lds_row<R, true>(P + (ly0 + j) * TX + x0 - R, xr);
+            lds_row<R, true>(P + (ly0 + j) * TX + x0 + CX, xr + R + CX);
+#pragma unroll
+            for (int i = 0; i < CX; ++i) xr[R + i] = ys[R + j][i];
+            double Wr[NC][CX];
+#pragma unroll
+            for (int f = 0; f < NC; ++f)
+              if (f % 3 != 0 || f == 0) lds_row<CX, true>(Cs + f * C::CFIELD + (ly0 + j) * TX + x0, Wr[f]);
+#pragma unroll
+            for (int i = 0; i < CX; ++i) {
+              double m[3][R], pl[3][R], W[NC];
+#pragma unroll
+              for (int r = 1; r <= R; ++r) {
+                m[0][r - 1] = xr[R + i - r];
+                pl[0][r - 1] = xr[R + i + r];
+                m[1][r - 1] = ys[R + j - r][i];
+                pl[1][r - 1] = ys[R + j + r][i];
+                m[2][r - 1] = pl[2][r - 1] = 0.0;  // not read by the x/y half
+              }
+#pragma unroll
+              for (int f = 0; f < NC; ++f) W[f] = (f % 3 != 0 || f == 0) ? Wr[f][i] : 0.0;
+              Pq[i] = point_25v_xy(v1[j][i], m, pl, W);
+            }
+          }
+          double Wz[4][CX];  // z coefficients of plane q, carried for its chain
+#pragma unroll
+          for (int r = 1; r <= 4; ++r) lds_row<CX, true>(Cs + 3 * r * C::CFIELD + (ly0 + j) * TX + x0, Wz[r - 1]);
+          double vout[CX];
+#pragma unroll
+          for (int i = 0; i < CX; ++i) {
+            const int cell = j * CX + i;
+            uint32_t st[32], rv[8];
+            tmem_ld32(tq + kColS1 + (uint32_t)cell * 32, st);
+            tmem_ld8(tq + colR + (uint32_t)cell * 8, rv);
+            tmem_wait_ld();
+            const double v = v1[j][i];
+            double vr[4];  // V1(q-2), V1(q-4), V1(q-6), V1(q-8)
+#pragma unroll
+            for (int k = 0; k < 4; ++k) vr[k] = dbl(rv[2 * k], rv[2 * k + 1]);
+            // carried state S1 (16 doubles): P(q-4..q-1) [0..3], Z(q-4) [4], Z(q-3) [5], the z coefficients
+            // still pending: plane q-4 {r4} [6], q-3 {r3, r4} [7, 8], q-2 {r2, r3, r4} [9..11],
+            // q-1 {r1..r4} [12..15];  S2: Z(q-2)
+            double S[16];
+#pragma unroll
+            for (int k = 0; k < 16; ++k) S[k] = dbl(st[2 * k], st[2 * k + 1]);
+            const double z2 = dbl(s2[2 * cell], s2[2 * cell + 1]);
+            const double z4 = point_25v_zterm(4, S[4], S[6], vr[3], v);   // plane q-4: last term
+            const double z3 = point_25v_zterm(3, S[5], S[7], vr[2], v);   // plane q-3
+            const double z2n = point_25v_zterm(2, z2, S[9], vr[1], v);    // plane q-2
+            const double z1 = point_25v_zterm(1, 0.0, S[12], vr[0], v);   // plane q-1: first term
+            vout[i] = __dadd_rn(S[0], z4);  // point_25v: (x/y half) + z chain
+            const double N[16] = {S[1], S[2], S[3], Pq[i], z3, z2n, S[8], S[10], S[11], S[13], S[14], S[15],
+                                  Wz[0][i], Wz[1][i], Wz[2][i], Wz[3][i]};
+#pragma unroll
+            for (int k = 0; k < 16; ++k) put(st + 2 * k, N[k]);
+            tmem_st32(tq + kColS1 + (uint32_t)cell * 32, st);
+            put(s2n + 2 * cell, z1);
+            // the ring of q's parity moves on: V1(q), V1(q-2), V1(q-4), V1(q-6)
+            put(rv, v);
+#pragma unroll
+            for (int k = 1; k < 4; ++k) put(rv + 2 * k, vr[k - 1]);
+            tmem_st8(tq + colR + (uint32_t)cell * 8, rv);
+          }
+          if (store) stg_row<CX, true>(p.dst + (long long)c4 * p.plane + col[j], vout, outc[j]);
+        }
+        tmem_st8(tq + kColS2, s2n);
+      }
+      tmem_wait_st();  // this step's TMEM stores land before the next step's loads
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[sl]);
+    }
+
+    // Fused halo exchange (ST_HALO_PEER; pipe.cu): the item's output planes that are a z-neighbour's halo
+    // go straight into the neighbour's buffer once the item is done (each thread forwards its own stores).
+    if (lvl2) {
+#pragma unroll 1
+      for (int qd = 0; qd < 2; ++qd) {
+        if (!p.rdst[qd]) continue;
+        const int c0 = max(it.zc0, p.rz0[qd]), c1 = min(it.zc1, p.rz1[qd]);
+#pragma unroll 1
+        for (int c = c0; c < c1; ++c) {
+          if ((p.dbg & 4) && c == it.zc1 - 1) continue;
+#pragma unroll
+          for (int j = 0; j < CY; ++j) {
+            const long long o = (long long)c * p.plane + col[j];
+            if (outc[j][0] && outc[j][1]) {
+              *reinterpret_cast<double2*>(p.rdst[qd] + o) = __ldcg(reinterpret_cast<const double2*>(p.dst + o));
+            } else {
+#pragma unroll
+              for (int i = 0; i < CX; ++i)
+                if (outc[j][i]) p.rdst[qd][o + i] = __ldcg(p.dst + o + i);
+            }
+          }
+        }
+      }
+    }
+  }
+  if (p.rfence) __threadfence_system();  // peer stores of another process's memory before the stream signal
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  named_sync(1, NCONS);
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  if (tid < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base) : "memory");
+}
+
+namespace {
+
+template <int TX, int TY, int D>
+cudaError_t run_pipe25(const KParams& p0, int zchunk_req, int num_sms, cudaStream_t stream, LaunchInfo* info) {
+  using C = P25Cfg<TX, TY, D>;
+  auto kern = pipe25_kernel<TX, TY, D>;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  KParams p = p0;
+  if (p.nblk > 1) return cudaErrorInvalidValue;  // single-block launches only
+  p.nblk = 1;
+  const int planes = p.zo1 - p.zo0;
+  if (planes <= 0) return cudaSuccess;
+  if (p.xoff != 16 - C::R) return cudaErrorInvalidValue;  // decode() assumes interior column R at raw 16
+  const int dx = p.walign ? 0 : ((p.xoff) & 1);
+  const int ntx = (p.nx + dx + C::OX - 1) / C::OX, nty = (p.ny + C::OY - 1) / C::OY;
+  const long long tiles = (long long)ntx * nty;
+  int zchunk = zchunk_req;
+  if (zchunk <= 0) {
+    const long long slots = num_sms;
+    const int min_chunk = 24 * 2 * C::R;  // keeps the 4R fill/drain planes of a chunk small
+    if (tiles * ((planes + min_chunk - 1) / min_chunk) >= 2 * slots) {
+      const long long chunks = std::max<long long>(1, (4 * slots + tiles - 1) / tiles);
+      zchunk = std::max((int)((planes + chunks - 1) / chunks), std::min(planes, min_chunk));
+    } else {
+      zchunk = (int)std::max<long long>(2, (planes * tiles + slots - 1) / slots);
+    }
+  }
+  p.zchunk = zchunk;
+  const int nzc = (planes + zchunk - 1) / zchunk;
+  p.nzc = nzc;
+  const long long items = tiles * nzc;
+  CUtensorMap mapA, mapB, mapC;
+  const int X0 = p.xoff & ~1;
+  const long long MX = p.xoff + p.nx + 2 * C::R - X0, MY = p.ny + 2 * C::R;
+  if (!make_tensor_map(&mapA, p.src_raw + X0, 3, p.pitch, MX, MY, p.zl, 1, p.plane, 0, TX, TY, 1) ||
+      !make_tensor_map(&mapB, p.src_raw + X0, 3, p.pitch, MX, MY, p.zl, 1, p.plane, 0, C::FX, C::FY, 1) ||
+      !make_tensor_map(&mapC, p.coef_raw + X0, 4, p.pitch, MX, MY, p.zl, C::NC, p.plane, p.cstride, TX, TY, C::NC))
+    return cudaErrorInvalidValue;
+  const int grid = (int)std::min<long long>(items, num_sms);
+  kern<<<grid, C::THREADS, C::SMEM, stream>>>(mapA, mapB, mapC, p, ntx, nty, (int)items);
+  if (info) {
+    info->tile_x = C::OX; info->tile_y = C::OY; info->zchunk = zchunk; info->threads = C::THREADS;
+    info->smem = (int)C::SMEM; info->ctas = grid;
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+// Tile configurations <TX, TY, D>: level-1 extent TX x TY (output (TX-8) x (TY-8)), ring depth D.
+cudaError_t launch_pipe25v2(const KParams& p, int zchunk_req, int num_sms, int cfg, cudaStream_t stream,
+                            LaunchInfo* info) {
+  switch (cfg) {
+    default: return run_pipe25<32, 24, 2>(p, zchunk_req, num_sms, stream, info);
+  }
+}
+
+}  // namespace st

@@ -47,19 +47,32 @@ __device__ __forceinline__ double point_7v(double c, const double (&m)[3][1], co
 }
 
 // Fig. 1d: W0*O + sum_{r=1..4} [W_{3r-2}(x pair) + W_{3r-1}(y pair) + W_{3r}(z pair)],
-// as three independent FMA chains (one per axis; the centre term starts the x chain) added at the end:
-// dependent-latency depth 6 instead of 13.
+// as three independent FMA chains (one per axis; the centre term starts the x chain) added at the end,
+// (x + y) + z: dependent-latency depth 6 instead of 13.  The two halves are separate functions because
+// the two-level kernel (pipe25.cu) evaluates them at different steps of its z-stream: the x/y half when
+// plane z is complete, the z chain one term per plane as planes z+1..z+4 arrive -- same operations.
+__device__ __forceinline__ double point_25v_xy(double c, const double (&m)[3][4], const double (&p)[3][4],
+                                               const double (&W)[13]) {
+  double a = __fma_rn(W[1], __dadd_rn(m[0][0], p[0][0]), __dmul_rn(W[0], c));
+  double b = __dmul_rn(W[2], __dadd_rn(m[1][0], p[1][0]));
+#pragma unroll
+  for (int r = 1; r < 4; ++r) {
+    a = __fma_rn(W[1 + 3 * r], __dadd_rn(m[0][r], p[0][r]), a);
+    b = __fma_rn(W[2 + 3 * r], __dadd_rn(m[1][r], p[1][r]), b);
+  }
+  return __dadd_rn(a, b);
+}
+// term r (1..4) of the z chain: W_{3r} * (V[z-r] + V[z+r]) (r = 1 starts the chain) added to z
+__device__ __forceinline__ double point_25v_zterm(int r, double z, double w, double vm, double vp) {
+  return r == 1 ? __dmul_rn(w, __dadd_rn(vm, vp)) : __fma_rn(w, __dadd_rn(vm, vp), z);
+}
 __device__ __forceinline__ double point_25v(double c, const double (&m)[3][4], const double (&p)[3][4],
                                             const double (&W)[13]) {
-  double acc[3];
-  acc[0] = __fma_rn(W[1], __dadd_rn(m[0][0], p[0][0]), __dmul_rn(W[0], c));
-  acc[1] = __dmul_rn(W[2], __dadd_rn(m[1][0], p[1][0]));
-  acc[2] = __dmul_rn(W[3], __dadd_rn(m[2][0], p[2][0]));
+  const double xy = point_25v_xy(c, m, p, W);
+  double z = 0.0;
 #pragma unroll
-  for (int r = 1; r < 4; ++r)
-#pragma unroll
-    for (int a = 0; a < 3; ++a) acc[a] = __fma_rn(W[1 + 3 * r + a], __dadd_rn(m[a][r], p[a][r]), acc[a]);
-  return __dadd_rn(__dadd_rn(acc[0], acc[1]), acc[2]);
+  for (int r = 1; r <= 4; ++r) z = point_25v_zterm(r, z, W[3 * r], m[2][r - 1], p[2][r - 1]);
+  return __dadd_rn(xy, z);
 }
 
 // Fig. 1e: 2*O^t - O^{t-1} + alpha*[w0*O^t + sum_r w_r*(x+y+z pairs_r)].

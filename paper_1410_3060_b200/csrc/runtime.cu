@@ -855,7 +855,8 @@ uint64_t handshake_magic(int rank) { return 0x5EED000000000000ull + (uint64_t)ra
 // 193, C4 49 vs 52.5 GLUP/s): the kernels run at the 1 kW power cap, where the idle tails of per-block
 // launches cost no throughput and filling them lowers the SM clock (profiles/r01_summary.md).
 bool multiblock_ok(const stencil_ctx* h) {
-  return env_int("STENCIL_MULTIBLOCK") == 1 && h->variant == ST_VARIANT_PIPE && h->nranks == 1 && !is_wave(h->kind);
+  return env_int("STENCIL_MULTIBLOCK") == 1 && h->variant == ST_VARIANT_PIPE && h->nranks == 1 && !is_wave(h->kind) &&
+         !(h->kind == ST_25PT_VAR && h->bt >= 2);  // the two-level 25-point kernel (pipe25.cu): one block per launch
 }
 
 int run_blocks_fused(stencil_ctx* h, int nblk, int b) {
