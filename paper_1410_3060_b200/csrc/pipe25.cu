@@ -5,8 +5,8 @@
 // Why a kernel of its own: in the generic pipe kernel, level k reads the coefficients of
 // plane z at step z + k*R, so a fused block must keep each coefficient plane on chip for (b_t - 1)*R = 4
 // steps: 5 planes x 13 fields x the level-1 extent >= 320 KB per CTA -- more than shared memory.  Here the
-// update of a level-2 cell is split the way its arithmetic already is (point.cuh, point_25v_xy /
-// point_25v_zterm):
+// update of a level-2 cell is split the way its arithmetic already is (point.cuh: point_25v_x / _y /
+// _zterm):
 //   * the x/y half (centre + 8 x-pair + 8 y-pair terms, 9 coefficients) needs level 1's plane z only; it
 //     is computed in the SAME step that level 1 computes plane z, with the coefficient plane still in the
 //     shared-memory ring -- so every coefficient plane crosses HBM once per block and leaves shared memory
@@ -14,21 +14,32 @@
 //   * the z chain's term r needs level-1 plane z + r, computed r steps later: it is accumulated one term
 //     per step.  What a cell must carry between steps -- its pending x/y partial sums (4 planes), z chains
 //     (3 planes) and the z-coefficients they still need (10 values) -- lives in TENSOR MEMORY (TMEM,
-//     tcgen05.ld/st), as do both z-rings (level-0 and level-1 values of the last 8 planes).  Registers
-//     hold only the current step's operands.
-// The operations are exactly point_25v's (same FMA chains, same final (xy) + z add), so the results are
-// bitwise equal to every other variant (test G4).
+//     tcgen05.ld/st), as do both z-rings (level-0 and level-1 values of the last planes).  Registers hold
+//     only the current step's operands.
+// The operations are exactly point_25v's (same FMA chains, same final (x + y) + z adds), so the results
+// are bitwise equal to every other variant (test G4).
 //
-// Per step s of a work item's z-stream (one CTA per SM, persistent; a producer warp + 6 consumer warps):
+// Per step s of a work item's z-stream (one CTA per SM, persistent; a producer warp + NW consumer warps):
 //   producer: TMA loads into one ring slot (one full mbarrier): box A = plane s of Omega^t over the
-//     level-1 extent E1 (TX x TY; its centre column enters the z-ring), box B = plane s-R with an R-wide
-//     halo (x/y neighbours of level 1), box C = the 13 coefficient fields of plane s-R over E1 (one 4-D
-//     box); and an L2 prefetch of step s+2's A and C boxes (the ring is 2 slots deep);
+//     level-1 extent E1 (TX x TY; its centre column is the z-ring's newest entry), box B = plane s-R with
+//     an R-wide halo (x/y neighbours of level 1; its centre is the ring's middle entry), box C = the 13
+//     coefficient fields of plane s-R over E1 (one 4-D box); and an L2 prefetch of step s+2's A and C
+//     boxes (the ring is 2 slots deep);
 //   level 1 (all consumer warps, 2x2 cells per thread): plane q = s-R of level 1 over E1 (full point_25v),
 //     written to a shared plane;  named barrier;
-//   level 2 (the 4 warps whose rows hold output cells): x/y half of plane q, the z-chain terms of planes
+//   level 2 (the warps whose rows hold output cells): x/y half of plane q, the z-chain terms of planes
 //     q-1..q-4, and the finished output plane q-4 = s-2R, streamed to HBM.
 // The output tile is (TX - 2R) x (TY - 2R) (overlapped tiles shrinking by R per level, as in pipe.cu).
+//
+// CLU > 1 (the GPU analog of the paper's thread groups sharing one cache block,
+// P:735-764): a thread-block cluster of CLU CTAs stacked in y shares one TX x (CLU*TY) tile.  Each CTA
+// computes level 1 on its own TY rows only; the R level-1 rows a CTA's level 2 needs from a neighbour are
+// pushed to it through distributed shared memory (cp.async.bulk.shared::cluster, completion on the
+// receiver's mbarrier), so the trapezoid shrinks only at the cluster's outer rows: level-1 work and
+// coefficient-box traffic per output cell drop by (CLU*TY - 2R)/(CLU*(TY - 2R)).  The rows cross SMs
+// while the next step runs: the warp next to a cluster neighbour ("boundary warp") finishes the y chain of
+// its cells one step late, from the rows received meanwhile (x chain and the y-coefficients wait in
+// shared memory for that step) -- no warp ever waits on the neighbour's current step.
 #include "kernels.cuh"
 #include "point.cuh"
 #include "sm100.cuh"
@@ -38,67 +49,131 @@
 
 namespace st {
 
-template <int TX, int TY, int D>
+template <int TX, int TY, int D, int CLU>
 struct P25Cfg {
   static constexpr int R = 4, NC = 13, CX = 2, CY = 2, NCELL = CX * CY;
   static constexpr int LPR = TX / CX;             // threads per block row
   static constexpr int NCONS = LPR * (TY / CY);   // consumer threads
   static constexpr int NW = NCONS / 32;           // consumer warps
   static constexpr int THREADS = NCONS + 32;      // + the producer warp
-  static constexpr int OX = TX - 2 * R, OY = TY - 2 * R;
+  static constexpr int OX = TX - 2 * R;           // output columns of a tile
+  static constexpr int OYP = CLU * TY - 2 * R;    // output rows of a (cluster) tile
   static constexpr int FX = TX + 2 * R, FY = TY + 2 * R;  // box B (level-1 footprint)
   static constexpr int AEL = TX * TY, BEL = FX * FY, CFIELD = TX * TY, CEL = NC * CFIELD;
   static constexpr int BOFF = (AEL + 15) / 16 * 16, COFF = BOFF + (BEL + 15) / 16 * 16;
   static constexpr int SLOT = COFF + (CEL + 15) / 16 * 16;  // doubles per ring slot (128-byte aligned parts)
   static constexpr int PEL = TX * TY;                       // one shared level-1 plane
+  static constexpr int NPB = 3;                             // level-1 planes kept (boundary warps read q-1)
+  static constexpr int RXEL = R * TX;                       // one pushed boundary strip (R rows)
+  static constexpr int NRX = CLU > 1 ? 4 : 0;               // receive slots per side
+  static constexpr int STASH = CLU > 1 ? 2 * 32 * NCELL * 5 : 0;  // boundary warps' carried x chain + Wy
   static constexpr int WROWS = 32 / LPR * CY;               // E1 rows per consumer warp
-  static constexpr int W2A = R / WROWS, W2B = (TY - R) / WROWS;  // level-2 warps: [W2A, W2B)
-  static constexpr uint32_t TX_BYTES_A = AEL * 8, TX_BYTES_BC = (BEL + CEL) * 8;
-  static constexpr size_t SMEM = 8 * ((size_t)D * SLOT + 2 * (size_t)PEL) + 8 * (2 * D + 8) + 4 * 4 + 128;
+  static constexpr uint32_t TX_BYTES_A = AEL * 8, TX_BYTES_BC = (BEL + CEL) * 8, RX_BYTES = RXEL * 8;
+  static constexpr size_t SMEM = 8 * ((size_t)D * SLOT + (size_t)NPB * PEL + 2 * (size_t)NRX * RXEL + STASH) +
+                                 8 * (2 * D + 8 + 2 * NRX + 8) + 4 * 8 + 128;
   static_assert(TX % 16 == 0 && TY % CY == 0 && NCONS % 32 == 0 && 32 % LPR == 0, "thread layout");
-  static_assert(R % WROWS == 0 && (TY - R) % WROWS == 0, "level-2 rows must be whole warps");
-  static_assert(OX > 0 && OY > 0 && (OX & 3) == 0, "output tile (whole 32-byte sectors per row)");
-  // TMEM (512 columns x 128 lanes; warp w reaches lanes 32*(w%4)..): a level-2 warp uses columns
-  // [0, 264) of its quadrant (z-rings 128, carried state 136), another warp [448, 512) (its z-ring);
-  // no quadrant holds two warps of the same kind.
-  static_assert(W2B - W2A <= 4 && NW - (W2B - W2A) <= 4 && NW <= 8, "TMEM quadrants");
+  static_assert(TY % WROWS == 0 && WROWS == R, "one warp = R rows (the pushed strip)");
+  static_assert(OX > 0 && TY > 2 * R && (OX & 3) == 0, "output tile (whole 32-byte sectors per row)");
+  static_assert(CLU == 1 || CLU == 2 || CLU == 4, "clusters of 1, 2 or 4 CTAs along y");
+  // TMEM (512 columns x 128 lanes; warp w reaches lanes 32*(w%4)..): warp w uses columns
+  // [256*(w/4), +256): at most two warps per lane quadrant.
+  static_assert(NW <= 8, "TMEM quadrants");
   static_assert(SMEM <= 227 * 1024, "shared memory");
   static_assert(SMEM > 116 * 1024, "one CTA per SM (the CTA allocates all 512 TMEM columns)");
   static_assert(FX <= 256 && FY <= 256 && TX <= 256, "TMA box dimension limit");
 };
 
-// TMEM column map of a consumer thread (32-bit columns of its lane)
-constexpr uint32_t kColV1 = 64;   // level-1 z-ring: 2 parity regions x 4 planes x 4 cells (level-2 warps)
-constexpr uint32_t kColS1 = 128;  // carried state, 16 doubles per cell (level-2 warps)
-constexpr uint32_t kColS2 = 256;  // carried state, 1 double per cell
-constexpr uint32_t kColOther = 448;  // level-0 z-ring of a warp without level-2 rows
+// TMEM column map of a consumer thread (32-bit columns of its lane, relative to its warp's 256)
+constexpr uint32_t kColV1 = 0;    // level-1 z-ring: 2 parity regions x 4 cells x 4 planes   [0, 64)
+constexpr uint32_t kColS1 = 64;   // carried state, 16 doubles per cell                       [64, 192)
+constexpr uint32_t kColV0 = 192;  // level-0 z-ring: 2 rows x 2 cells x 7 planes, row j at 192 + 28j
+constexpr uint32_t kColS2 = 248;  // carried state, 1 double per cell                         [248, 256)
 
 __device__ __forceinline__ double dbl(uint32_t lo, uint32_t hi) { return __hiloint2double((int)hi, (int)lo); }
 __device__ __forceinline__ void put(uint32_t* w, double v) {
   w[0] = (uint32_t)__double2loint(v);
   w[1] = (uint32_t)__double2hiint(v);
 }
+// one row's level-0 ring (28 columns) as aligned x16 / x8 / x4 pieces
+template <int J>
+__device__ __forceinline__ void v0ring_ld(uint32_t t, uint32_t (&w)[28]) {
+  uint32_t a[16], b[8], c[4];
+  if constexpr (J == 0) {
+    tmem_ld16(t + kColV0, a); tmem_ld8(t + kColV0 + 16, b); tmem_ld4(t + kColV0 + 24, c);
+  } else {
+    tmem_ld4(t + kColV0 + 28, c); tmem_ld16(t + kColV0 + 32, a); tmem_ld8(t + kColV0 + 48, b);
+  }
+  tmem_wait_ld();
+  if constexpr (J == 0) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) w[i] = a[i];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) w[16 + i] = b[i];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) w[24 + i] = c[i];
+  } else {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) w[i] = c[i];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) w[4 + i] = a[i];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) w[20 + i] = b[i];
+  }
+}
+template <int J>
+__device__ __forceinline__ void v0ring_st(uint32_t t, const uint32_t (&w)[28]) {
+  uint32_t a[16], b[8], c[4];
+  if constexpr (J == 0) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) a[i] = w[i];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) b[i] = w[16 + i];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) c[i] = w[24 + i];
+    tmem_st16(t + kColV0, a); tmem_st8(t + kColV0 + 16, b); tmem_st4(t + kColV0 + 24, c);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) c[i] = w[i];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) a[i] = w[4 + i];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) b[i] = w[20 + i];
+    tmem_st4(t + kColV0 + 28, c); tmem_st16(t + kColV0 + 32, a); tmem_st8(t + kColV0 + 48, b);
+  }
+}
 
-template <int TX, int TY, int D>
-__global__ void __launch_bounds__(P25Cfg<TX, TY, D>::THREADS, 1)
+template <int TX, int TY, int D, int CLU>
+__global__ void __launch_bounds__(P25Cfg<TX, TY, D, CLU>::THREADS, 1)
     pipe25_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                   const __grid_constant__ CUtensorMap mapC, const KParams p, int ntx, int nty, int items) {
-  using C = P25Cfg<TX, TY, D>;
-  constexpr int R = C::R, NC = C::NC, NCONS = C::NCONS, FX = C::FX, CX = C::CX, CY = C::CY;
+  using C = P25Cfg<TX, TY, D, CLU>;
+  constexpr int R = C::R, NC = C::NC, NCONS = C::NCONS, FX = C::FX, CX = C::CX, CY = C::CY, NW = C::NW;
 
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double* ring = reinterpret_cast<double*>(smem_raw);
   double* sP = ring + (size_t)D * C::SLOT;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sP + 2 * C::PEL);
+  double* rxTop = sP + (size_t)C::NPB * C::PEL;      // rows -R..-1 (the CTA above, rank - 1), per slot
+  double* rxBot = rxTop + (size_t)C::NRX * C::RXEL;  // rows TY..TY+R-1 (the CTA below, rank + 1)
+  double* stash = rxBot + (size_t)C::NRX * C::RXEL;  // [boundary warp top/bottom][lane][cell][5]
+  uint64_t* full = reinterpret_cast<uint64_t*>(stash + C::STASH);
   uint64_t* empty = full + D;
   uint64_t* itemFull = empty + D;
   uint64_t* itemEmpty = itemFull + 4;
-  volatile int* itemq = reinterpret_cast<volatile int*>(itemEmpty + 4);
+  uint64_t* rxbTop = itemEmpty + 4;
+  uint64_t* rxbBot = rxbTop + C::NRX;
+  uint64_t* cfull = rxbBot + C::NRX;  // cluster work-item queue (rank 0 -> ranks 1..CLU-1)
+  uint64_t* cempty = cfull + 4;
+  volatile int* itemq = reinterpret_cast<volatile int*>(cempty + 4);
+  volatile int* cid = itemq + 4;
 
+  uint32_t crank = 0;
+  if constexpr (CLU > 1) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
   const int tid = threadIdx.x;
   if (tid == 0) {
-    for (int i = 0; i < D; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], C::NW); }
-    for (int i = 0; i < 4; ++i) { mbar_init(&itemFull[i], 1); mbar_init(&itemEmpty[i], C::NW); }
+    for (int i = 0; i < D; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], NW); }
+    for (int i = 0; i < 4; ++i) { mbar_init(&itemFull[i], 1); mbar_init(&itemEmpty[i], NW); }
+    for (int i = 0; i < C::NRX; ++i) { mbar_init(&rxbTop[i], 1); mbar_init(&rxbBot[i], 1); }
+    for (int i = 0; i < 4; ++i) { mbar_init(&cfull[i], 1); mbar_init(&cempty[i], CLU > 1 ? CLU - 1 : 1); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __shared__ uint32_t tmem_base;
@@ -110,6 +185,7 @@ __global__ void __launch_bounds__(P25Cfg<TX, TY, D>::THREADS, 1)
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  if constexpr (CLU > 1) cluster_sync_all();  // every CTA's barriers exist before any remote arrive / copy
 
   if (tid >= NCONS) {
     // ---------------------------------------------------------------- producer warp
@@ -121,13 +197,34 @@ __global__ void __launch_bounds__(P25Cfg<TX, TY, D>::THREADS, 1)
       for (uint32_t n = 0;; ++n) {
         const uint32_t qs = n & 3;
         mbar_wait(&itemEmpty[qs], ((n >> 2) & 1) ^ 1);
-        int g = (int)atomicAdd(p.sched, 1u);
-        if (g >= items) g = -1;
+        int g;
+        if constexpr (CLU > 1) {
+          // every CTA of a cluster takes the same items: rank 0 draws from the global counter and passes
+          // the id to the others through a 4-entry queue in their shared memory
+          if (crank == 0) {
+            mbar_wait(&cempty[qs], ((n >> 2) & 1) ^ 1);
+            g = (int)atomicAdd(p.sched, 1u);
+            if (g >= items) g = -1;
+            for (uint32_t k = 1; k < (uint32_t)CLU; ++k) {
+              asm volatile("st.shared::cluster.s32 [%0], %1;" ::"r"(dsmem_addr((const void*)&cid[qs], k)), "r"(g)
+                           : "memory");
+              mbar_arrive_remote(dsmem_addr(&cfull[qs], k));
+            }
+          } else {
+            mbar_wait_cluster(&cfull[qs], (n >> 2) & 1);
+            g = cid[qs];
+            mbar_arrive_remote(dsmem_addr(&cempty[qs], 0u));
+          }
+        } else {
+          g = (int)atomicAdd(p.sched, 1u);
+          if (g >= items) g = -1;
+        }
         itemq[qs] = g;
         mbar_arrive(&itemFull[qs]);  // release: the id is visible to the consumers' acquire
         if (g < 0) break;
         if ((p.dbg & 8) && g == 0) continue;
-        const Item it = decode<R, 1, C::OX, C::OY>(g, ntx, nty, p);
+        Item it = decode<R, 1, C::OX, C::OYP>(g, ntx, nty, p);
+        it.gy0 += (int)crank * TY;
         const int xb = ((it.gx0 - R + p.xoff) & ~1) - (p.xoff & ~1);  // box B (footprint)
         const int xa = ((it.gx0 + p.xoff) & ~1) - (p.xoff & ~1);      // boxes A, C (level-1 extent)
         for (int s = it.s_begin; s <= it.s_end; ++s, ++iv) {
@@ -151,22 +248,29 @@ __global__ void __launch_bounds__(P25Cfg<TX, TY, D>::THREADS, 1)
       }
       // every CTA has drawn its terminating id before the last one gets here: reset for the next launch
       __threadfence();
-      if (atomicAdd(p.sched + 1, 1u) == gridDim.x - 1) {
+      if ((CLU == 1 || crank == 0) && atomicAdd(p.sched + 1, 1u) == gridDim.x / CLU - 1) {
         p.sched[0] = 0;
         p.sched[1] = 0;
         __threadfence();
       }
     }
+    if constexpr (CLU > 1) cluster_sync_all();  // no CTA leaves while a neighbour may still push into it
     return;
   }
 
   // ---------------------------------------------------------------- consumers
   const int warp = tid >> 5, lane = tid & 31;
-  const bool lvl2 = warp >= C::W2A && warp < C::W2B;  // warp-uniform
-  const int x0 = (tid % C::LPR) * CX;                  // first E1 column of this thread's 2x2 block
-  const int ly0 = (tid / C::LPR) * CY;                 // first E1 row
-  const uint32_t tq = tmem_base + ((uint32_t)((warp & 3) * 32) << 16);
-  const uint32_t colV0 = lvl2 ? 0u : kColOther;
+  const int x0 = (tid % C::LPR) * CX;   // first E1 column of this thread's 2x2 block
+  const int ly0 = (tid / C::LPR) * CY;  // first E1 row
+  // level-2 rows of this CTA (the trapezoid shrinks by R only at the cluster's outer rows)
+  const int ylo = crank == 0 ? R : 0, yhi = crank == (uint32_t)CLU - 1 ? TY - R : TY;
+  const int wr0 = warp * C::WROWS;  // the warp's first row (warp-uniform)
+  const bool lvl2 = wr0 + C::WROWS > ylo && wr0 < yhi;
+  const bool topB = CLU > 1 && warp == 0 && crank > 0;                        // needs rows of rank - 1
+  const bool botB = CLU > 1 && warp == NW - 1 && crank < (uint32_t)CLU - 1;  // needs rows of rank + 1
+  const bool bnd = topB || botB;
+  const uint32_t tq = tmem_base + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)((warp >> 2) * 256);
+  double* myst = stash + (size_t)((topB ? 0 : 1) * 32 + lane) * C::NCELL * 5;  // boundary warps only
   uint32_t iv = 0;
 
   for (uint32_t n = 0;; ++n) {
@@ -177,7 +281,8 @@ __global__ void __launch_bounds__(P25Cfg<TX, TY, D>::THREADS, 1)
     if (lane == 0) mbar_arrive(&itemEmpty[qs]);
     if (g < 0) break;
     if ((p.dbg & 8) && g == 0) continue;  // fault injection: work item 0 never computed
-    const Item it = decode<R, 1, C::OX, C::OY>(g, ntx, nty, p);
+    Item it = decode<R, 1, C::OX, C::OYP>(g, ntx, nty, p);
+    it.gy0 += (int)crank * TY;
     bool act1[CY][CX], outc[CY][CX];
     long long col[CY];
 #pragma unroll
@@ -188,7 +293,7 @@ __global__ void __launch_bounds__(P25Cfg<TX, TY, D>::THREADS, 1)
       for (int i = 0; i < CX; ++i) {
         const int lx = x0 + i, gx = it.gx0 + lx;
         act1[j][i] = gx >= R && gx < p.nx + R && gy >= R && gy < p.ny + R;
-        outc[j][i] = act1[j][i] && lx >= R && lx < TX - R && ly >= R && ly < TY - R;
+        outc[j][i] = act1[j][i] && lx >= R && lx < TX - R && ly >= ylo && ly < yhi;
       }
     }
 
@@ -209,10 +314,11 @@ __global__ void __launch_bounds__(P25Cfg<TX, TY, D>::THREADS, 1)
         for (int r = 0; r < CY + 2 * R; ++r) lds_row<CX, true>(Bb + (ly0 - R + r) * FX + x0, ys[r]);
 #pragma unroll
         for (int j = 0; j < CY; ++j) {
-          // level-0 z-ring of row j's two cells (TMEM, cell-major): planes s-8 .. s-1, k = 0 oldest
-          uint32_t zr[32];
-          tmem_ld32(tq + colV0 + 32u * j, zr);
-          double vnew[CX];  // plane s (box A): the ring's newest entry
+          // level-0 z-ring of row j's two cells (TMEM): planes s-8+k, k in {0..3, 5..7} (7 entries);
+          // k = 4 is plane q itself (the centre of box B), k = 8 plane s (box A)
+          uint32_t zr[28];
+          if (j == 0) v0ring_ld<0>(tq, zr); else v0ring_ld<1>(tq, zr);
+          double vnew[CX];
           lds_row<CX, true>(slot + (ly0 + j) * TX + x0, vnew);
           double xr[R + CX + R];
           lds_row<R, true>(Bb + (ly0 + j) * FX + x0 - R, xr);
@@ -222,11 +328,13 @@ __global__ void __launch_bounds__(P25Cfg<TX, TY, D>::THREADS, 1)
           double Wr[NC][CX];
 #pragma unroll
           for (int f = 0; f < NC; ++f) lds_row<CX, true>(Cs + f * C::CFIELD + (ly0 + j) * TX + x0, Wr[f]);
-          tmem_wait_ld();
-          auto V0 = [&](int k, int i) -> double {  // plane s - 8 + k of cell (j, i); k = 8: plane s
-            return k == 8 ? vnew[i] : dbl(zr[16 * i + 2 * k], zr[16 * i + 2 * k + 1]);
+          auto V0 = [&](int k, int i) -> double {  // plane s - 8 + k of cell (j, i)
+            if (k == 8) return vnew[i];
+            if (k == R) return ys[R + j][i];
+            const int e = k < R ? k : k - 1;
+            return dbl(zr[14 * i + 2 * e], zr[14 * i + 2 * e + 1]);
           };
-          uint32_t zn[32];
+          uint32_t zn[28];
 #pragma unroll
           for (int i = 0; i < CX; ++i) {
             double m[3][R], pl[3][R], W[NC];
@@ -245,39 +353,98 @@ __global__ void __launch_bounds__(P25Cfg<TX, TY, D>::THREADS, 1)
             const double v = point_25v(c, m, pl, W);
             // ghosts, cells outside the grid and planes not computed at level 1 keep their input value
             v1[j][i] = (zv1 && act1[j][i]) ? v : c;
+            // the ring moves on a plane: next step's entries are this step's k = 1..3, 4 (box B), 6, 7, 8
 #pragma unroll
-            for (int k = 0; k < 8; ++k) put(zn + 16 * i + 2 * k, V0(k + 1, i));  // the ring moves on a plane
+            for (int e = 0; e < 7; ++e) put(zn + 14 * i + 2 * e, V0(e < R ? e + 1 : e + 2, i));
           }
-          tmem_st32(tq + colV0 + 32u * j, zn);
+          if (j == 0) v0ring_st<0>(tq, zn); else v0ring_st<1>(tq, zn);
         }
       }
-      double* P = sP + (size_t)(iv & 1u) * C::PEL;  // alternate with the CTA's step counter (pipe.cu)
+      double* P = sP + (size_t)(iv % C::NPB) * C::PEL;  // rotates with the CTA's step counter (pipe.cu)
 #pragma unroll
       for (int j = 0; j < CY; ++j) sts_row<CX, true>(P + (ly0 + j) * TX + x0, v1[j]);
+      if constexpr (CLU > 1) {
+        // the previous step's push has read its rows before this barrier releases their rewrite (NPB
+        // steps after they were written)
+        if (bnd && lane == 0) bulk_wait_read<0>();
+      }
       if (!(p.dbg & 2)) named_sync(1, NCONS);
+
+      if constexpr (CLU > 1) {
+        // push this CTA's outer R level-1 rows of plane q to the cluster neighbours, which finish their
+        // boundary rows' y chains with them next step; arm this step's receive slot
+        if (bnd && lane == 0) {
+          const uint32_t k = iv % C::NRX;
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          if (topB) {
+            mbar_expect_tx(&rxbTop[k], C::RX_BYTES);
+            bulk_copy_to_peer(dsmem_addr(rxBot + (size_t)k * C::RXEL, crank - 1), P, C::RX_BYTES,
+                              dsmem_addr(&rxbBot[k], crank - 1));
+          } else {
+            mbar_expect_tx(&rxbBot[k], C::RX_BYTES);
+            bulk_copy_to_peer(dsmem_addr(rxTop + (size_t)k * C::RXEL, crank + 1), P + (TY - R) * TX, C::RX_BYTES,
+                              dsmem_addr(&rxbTop[k], crank + 1));
+          }
+        }
+      }
 
       // ---------------- level 2: x/y half of plane q, z-chain terms of planes q-1..q-4, output plane q-4
       if (lvl2) {
-        const uint32_t colR = kColV1 + (uint32_t)(q & 1) * 32;  // level-1 z-ring of q's parity, cell-major:
+        const uint32_t colR = kColV1 + (uint32_t)(q & 1) * 32;  // level-1 z-ring of q's parity, per cell:
         uint32_t s2[8], s2n[8];                                  // V1(q-2), V1(q-4), V1(q-6), V1(q-8)
         tmem_ld8(tq + kColS2, s2);  // Z(q-2) of the 4 cells
         double ys[CY + 2 * R][CX];
+        double Pprev[CY][CX];  // boundary warps: P(q-1), completed this step
+        if (!bnd) {
 #pragma unroll
-        for (int r = 0; r < CY + 2 * R; ++r) {
-          const int row = min(max(ly0 - R + r, 0), TY - 1);  // rows outside E1 only feed discarded cells
-          lds_row<CX, true>(P + row * TX + x0, ys[r]);
+          for (int r = 0; r < CY + 2 * R; ++r) {
+            const int row = min(max(ly0 - R + r, 0), TY - 1);  // rows outside E1 only feed discarded cells
+            lds_row<CX, true>(P + row * TX + x0, ys[r]);
+          }
+        } else if constexpr (CLU > 1) {
+          // the y chain of plane q-1, one step late: level-1 plane q-1 and the neighbour's rows of it,
+          // received during the last step
+          const double* Pp = sP + (size_t)((iv + C::NPB - 1) % C::NPB) * C::PEL;
+          const uint32_t k = (iv + C::NRX - 1) % C::NRX;
+          if (iv > 0) mbar_wait(topB ? &rxbTop[k] : &rxbBot[k], ((iv - 1) / C::NRX) & 1);
+          const double* rx = (topB ? rxTop : rxBot) + (size_t)k * C::RXEL;
+#pragma unroll
+          for (int r = 0; r < CY + 2 * R; ++r) {
+            const int row = ly0 - R + r;
+            if (row < 0) lds_row<CX, true>(rx + (row + R) * TX + x0, ys[r]);
+            else if (row >= TY) lds_row<CX, true>(rx + (row - TY) * TX + x0, ys[r]);
+            else lds_row<CX, true>(Pp + row * TX + x0, ys[r]);
+          }
+#pragma unroll
+          for (int j = 0; j < CY; ++j)
+#pragma unroll
+            for (int i = 0; i < CX; ++i) {
+              const double* sv = myst + (j * CX + i) * 5;  // x chain and Wy_1..4 of plane q-1
+              double m[3][R], pl[3][R], W[NC];
+#pragma unroll
+              for (int r = 1; r <= R; ++r) {
+                m[1][r - 1] = ys[R + j - r][i];
+                pl[1][r - 1] = ys[R + j + r][i];
+                m[0][r - 1] = pl[0][r - 1] = m[2][r - 1] = pl[2][r - 1] = 0.0;
+              }
+#pragma unroll
+              for (int f = 0; f < NC; ++f) W[f] = 0.0;
+#pragma unroll
+              for (int r = 1; r <= R; ++r) W[3 * r - 1] = sv[r];
+              Pprev[j][i] = __dadd_rn(sv[0], point_25v_y(m, pl, W));
+            }
         }
         const int c4 = q - R;  // the plane level 2 finishes this step
         const bool store = c4 >= it.zc0 && c4 < it.zc1 && !((p.dbg & 4) && c4 == it.zc1 - 1);
 #pragma unroll
         for (int j = 0; j < CY; ++j) {
-          double Pq[CX];
-          {  // x/y half (point_25v_xy): W0, x and y coefficients of plane q
+          double Pq[CX];  // x/y half of plane q (boundary warps: its x chain goes to the stash)
+          {
             double xr[R + CX + R];
             lds_row<R, true>(P + (ly0 + j) * TX + x0 - R, xr);
             lds_row<R, true>(P + (ly0 + j) * TX + x0 + CX, xr + R + CX);
 #pragma unroll
-            for (int i = 0; i < CX; ++i) xr[R + i] = ys[R + j][i];
+            for (int i = 0; i < CX; ++i) xr[R + i] = v1[j][i];
             double Wr[NC][CX];
 #pragma unroll
             for (int f = 0; f < NC; ++f)
@@ -289,13 +456,21 @@ __global__ void __launch_bounds__(P25Cfg<TX, TY, D>::THREADS, 1)
               for (int r = 1; r <= R; ++r) {
                 m[0][r - 1] = xr[R + i - r];
                 pl[0][r - 1] = xr[R + i + r];
-                m[1][r - 1] = ys[R + j - r][i];
-                pl[1][r - 1] = ys[R + j + r][i];
+                m[1][r - 1] = bnd ? 0.0 : ys[R + j - r][i];
+                pl[1][r - 1] = bnd ? 0.0 : ys[R + j + r][i];
                 m[2][r - 1] = pl[2][r - 1] = 0.0;  // not read by the x/y half
               }
 #pragma unroll
               for (int f = 0; f < NC; ++f) W[f] = (f % 3 != 0 || f == 0) ? Wr[f][i] : 0.0;
-              Pq[i] = point_25v_xy(v1[j][i], m, pl, W);
+              if (!bnd) {
+                Pq[i] = point_25v_xy(v1[j][i], m, pl, W);
+              } else {  // carried to the next step with plane q's y coefficients
+                double* sv = myst + (j * CX + i) * 5;
+                sv[0] = point_25v_x(v1[j][i], m, pl, W);
+#pragma unroll
+                for (int r = 1; r <= R; ++r) sv[r] = W[3 * r - 1];
+                Pq[i] = 0.0;
+              }
             }
           }
           double Wz[4][CX];  // z coefficients of plane q, carried for its chain
@@ -325,7 +500,9 @@ __global__ void __launch_bounds__(P25Cfg<TX, TY, D>::THREADS, 1)
             const double z2n = point_25v_zterm(2, z2, S[9], vr[1], v);    // plane q-2
             const double z1 = point_25v_zterm(1, 0.0, S[12], vr[0], v);   // plane q-1: first term
             vout[i] = __dadd_rn(S[0], z4);  // point_25v: (x/y half) + z chain
-            const double N[16] = {S[1], S[2], S[3], Pq[i], z3, z2n, S[8], S[10], S[11], S[13], S[14], S[15],
+            // boundary warps complete P(q-1) only now (its slot held a placeholder)
+            const double Pq1 = bnd ? Pprev[j][i] : S[3];
+            const double N[16] = {S[1], S[2], Pq1, Pq[i], z3, z2n, S[8], S[10], S[11], S[13], S[14], S[15],
                                   Wz[0][i], Wz[1][i], Wz[2][i], Wz[3][i]};
 #pragma unroll
             for (int k = 0; k < 16; ++k) put(st + 2 * k, N[k]);
@@ -372,18 +549,22 @@ __global__ void __launch_bounds__(P25Cfg<TX, TY, D>::THREADS, 1)
     }
   }
   if (p.rfence) __threadfence_system();  // peer stores of another process's memory before the stream signal
+  if constexpr (CLU > 1) {
+    if (bnd && lane == 0) bulk_wait_read<0>();
+  }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   named_sync(1, NCONS);
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   if (tid < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base) : "memory");
+  if constexpr (CLU > 1) cluster_sync_all();  // the neighbours may still push into this CTA
 }
 
 namespace {
 
-template <int TX, int TY, int D>
+template <int TX, int TY, int D, int CLU>
 cudaError_t run_pipe25(const KParams& p0, int zchunk_req, int num_sms, cudaStream_t stream, LaunchInfo* info) {
-  using C = P25Cfg<TX, TY, D>;
-  auto kern = pipe25_kernel<TX, TY, D>;
+  using C = P25Cfg<TX, TY, D, CLU>;
+  auto kern = pipe25_kernel<TX, TY, D, CLU>;
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
@@ -396,12 +577,31 @@ cudaError_t run_pipe25(const KParams& p0, int zchunk_req, int num_sms, cudaStrea
   const int planes = p.zo1 - p.zo0;
   if (planes <= 0) return cudaSuccess;
   if (p.xoff != 16 - C::R) return cudaErrorInvalidValue;  // decode() assumes interior column R at raw 16
-  const int dx = p.walign ? 0 : ((p.xoff) & 1);
-  const int ntx = (p.nx + dx + C::OX - 1) / C::OX, nty = (p.ny + C::OY - 1) / C::OY;
+  const int dx = p.walign ? 0 : (p.xoff & 1);  // decode<R, 1, ...>'s shift
+  const int ntx = (p.nx + dx + C::OX - 1) / C::OX, nty = (p.ny + C::OYP - 1) / C::OYP;
   const long long tiles = (long long)ntx * nty;
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  cfg.blockDim = dim3(C::THREADS);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = stream;
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CLU;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  // concurrent clusters: a cluster's CTAs share one GPC, whose SM count need not be a multiple of CLU
+  int clusters = num_sms / CLU;
+  if (CLU > 1) {
+    cfg.gridDim = dim3(CLU * clusters);
+    int nc = 0;
+    if (cudaOccupancyMaxActiveClusters(&nc, kern, &cfg) == cudaSuccess && nc > 0) clusters = nc;
+    else cudaGetLastError();
+  }
   int zchunk = zchunk_req;
   if (zchunk <= 0) {
-    const long long slots = num_sms;
+    const long long slots = clusters;
     const int min_chunk = 24 * 2 * C::R;  // keeps the 4R fill/drain planes of a chunk small
     if (tiles * ((planes + min_chunk - 1) / min_chunk) >= 2 * slots) {
       const long long chunks = std::max<long long>(1, (4 * slots + tiles - 1) / tiles);
@@ -421,10 +621,16 @@ cudaError_t run_pipe25(const KParams& p0, int zchunk_req, int num_sms, cudaStrea
       !make_tensor_map(&mapB, p.src_raw + X0, 3, p.pitch, MX, MY, p.zl, 1, p.plane, 0, C::FX, C::FY, 1) ||
       !make_tensor_map(&mapC, p.coef_raw + X0, 4, p.pitch, MX, MY, p.zl, C::NC, p.plane, p.cstride, TX, TY, C::NC))
     return cudaErrorInvalidValue;
-  const int grid = (int)std::min<long long>(items, num_sms);
-  kern<<<grid, C::THREADS, C::SMEM, stream>>>(mapA, mapB, mapC, p, ntx, nty, (int)items);
+  const int grid = (int)std::min<long long>(items, clusters) * CLU;
+  if constexpr (CLU == 1) {
+    kern<<<grid, C::THREADS, C::SMEM, stream>>>(mapA, mapB, mapC, p, ntx, nty, (int)items);
+  } else {
+    cfg.gridDim = dim3(grid);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, mapA, mapB, mapC, p, ntx, nty, (int)items);
+    if (e != cudaSuccess) return e;
+  }
   if (info) {
-    info->tile_x = C::OX; info->tile_y = C::OY; info->zchunk = zchunk; info->threads = C::THREADS;
+    info->tile_x = C::OX; info->tile_y = C::OYP; info->zchunk = zchunk; info->threads = C::THREADS;
     info->smem = (int)C::SMEM; info->ctas = grid;
   }
   return cudaGetLastError();
@@ -432,11 +638,14 @@ cudaError_t run_pipe25(const KParams& p0, int zchunk_req, int num_sms, cudaStrea
 
 }  // namespace
 
-// Tile configurations <TX, TY, D>: level-1 extent TX x TY (output (TX-8) x (TY-8)), ring depth D.
+// Tile configurations <TX, TY, D, CLU>: level-1 extent TX x TY per CTA, ring depth D, CLU CTAs per
+// cluster stacked in y (output tile (TX - 8) x (CLU*TY - 8)).
 cudaError_t launch_pipe25v2(const KParams& p, int zchunk_req, int num_sms, int cfg, cudaStream_t stream,
                             LaunchInfo* info) {
   switch (cfg) {
-    default: return run_pipe25<32, 24, 2>(p, zchunk_req, num_sms, stream, info);
+    case 1: return run_pipe25<32, 24, 2, 1>(p, zchunk_req, num_sms, stream, info);   // single CTA: 24 x 16
+    case 2: return run_pipe25<32, 20, 2, 4>(p, zchunk_req, num_sms, stream, info);   // cluster of 4: 24 x 72
+    default: return run_pipe25<32, 20, 2, 2>(p, zchunk_req, num_sms, stream, info);  // cluster pair: 24 x 32
   }
 }
 

@@ -51,16 +51,23 @@ __device__ __forceinline__ double point_7v(double c, const double (&m)[3][1], co
 // (x + y) + z: dependent-latency depth 6 instead of 13.  The two halves are separate functions because
 // the two-level kernel (pipe25.cu) evaluates them at different steps of its z-stream: the x/y half when
 // plane z is complete, the z chain one term per plane as planes z+1..z+4 arrive -- same operations.
-__device__ __forceinline__ double point_25v_xy(double c, const double (&m)[3][4], const double (&p)[3][4],
-                                               const double (&W)[13]) {
+// x chain (the centre term starts it) and y chain of Fig. 1d; point_25v_xy = x + y
+__device__ __forceinline__ double point_25v_x(double c, const double (&m)[3][4], const double (&p)[3][4],
+                                              const double (&W)[13]) {
   double a = __fma_rn(W[1], __dadd_rn(m[0][0], p[0][0]), __dmul_rn(W[0], c));
+#pragma unroll
+  for (int r = 1; r < 4; ++r) a = __fma_rn(W[1 + 3 * r], __dadd_rn(m[0][r], p[0][r]), a);
+  return a;
+}
+__device__ __forceinline__ double point_25v_y(const double (&m)[3][4], const double (&p)[3][4], const double (&W)[13]) {
   double b = __dmul_rn(W[2], __dadd_rn(m[1][0], p[1][0]));
 #pragma unroll
-  for (int r = 1; r < 4; ++r) {
-    a = __fma_rn(W[1 + 3 * r], __dadd_rn(m[0][r], p[0][r]), a);
-    b = __fma_rn(W[2 + 3 * r], __dadd_rn(m[1][r], p[1][r]), b);
-  }
-  return __dadd_rn(a, b);
+  for (int r = 1; r < 4; ++r) b = __fma_rn(W[2 + 3 * r], __dadd_rn(m[1][r], p[1][r]), b);
+  return b;
+}
+__device__ __forceinline__ double point_25v_xy(double c, const double (&m)[3][4], const double (&p)[3][4],
+                                               const double (&W)[13]) {
+  return __dadd_rn(point_25v_x(c, m, p, W), point_25v_y(m, p, W));
 }
 // term r (1..4) of the z chain: W_{3r} * (V[z-r] + V[z+r]) (r = 1 starts the chain) added to z
 __device__ __forceinline__ double point_25v_zterm(int r, double z, double w, double vm, double vp) {

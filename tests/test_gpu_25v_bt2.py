@@ -13,17 +13,23 @@ pytestmark = pytest.mark.gpu
 K = synth.K25V
 
 # output tile 24 x 16: shapes with ragged tails in x and y, and z-chunks from 1 plane to the whole slab
-SHAPES = [(130, 37, 41), (24, 16, 9), (25, 17, 13), (71, 50, 30), (1, 1, 1), (3, 2, 5), (50, 3, 8), (2, 40, 17)]
+SHAPES = [(130, 37, 41), (24, 16, 9), (25, 17, 13), (71, 50, 30), (1, 1, 1), (3, 2, 5), (50, 3, 8), (2, 40, 17),
+          (48, 150, 12)]
+
+
+# tile_cfg: 0 = cluster pair (24 x 32 output tiles), 1 = single CTA (24 x 16), 2 = cluster of 4 (24 x 72)
+CFGS = (0, 1, 2)
 
 
 @pytest.mark.parametrize("shape", SHAPES)
 def test_bt2_bitwise_equal_naive(shape):
     for T in (1, 2, 3, 6):
         ref = gpu_run(K, *shape, T, seed=21, variant=st.ST_VARIANT_NAIVE)
-        for zc in (0, 1, 3, 1000):
-            got = gpu_run(K, *shape, T, seed=21, variant=st.ST_VARIANT_PIPE, bt=2, zchunk=zc)
-            assert got[2]["bt"] == 2
-            assert np.array_equal(got[0], ref[0]), (shape, T, zc)
+        for cfg in CFGS:
+            for zc in (0, 1, 3, 1000):
+                got = gpu_run(K, *shape, T, seed=21, variant=st.ST_VARIANT_PIPE, bt=2, zchunk=zc, tile_cfg=cfg)
+                assert got[2]["bt"] == 2
+                assert np.array_equal(got[0], ref[0]), (shape, T, cfg, zc)
 
 
 def test_bt2_oracle_short_T():
@@ -34,9 +40,10 @@ def test_bt2_oracle_short_T():
     for T in (1, 2, 3, 4, 5):
         oracle.run_arrays(K, nx, ny, nz, o_new, o_old, inp.coef, inp.scalars, T - done)
         done = T
-        g_new, _, info = gpu_run(K, nx, ny, nz, T, seed=8, bt=2)
-        assert info["bt"] == 2
-        assert_parity(K, g_new, None, o_new, None, inp.R, 1e-13, inputs=inp)
+        for cfg in CFGS:
+            g_new, _, info = gpu_run(K, nx, ny, nz, T, seed=8, bt=2, tile_cfg=cfg)
+            assert info["bt"] == 2
+            assert_parity(K, g_new, None, o_new, None, inp.R, 1e-13, inputs=inp)
 
 
 def test_bt2_consecutive_runs_and_odd_T():
