@@ -68,7 +68,7 @@ struct P25Cfg {
   static constexpr int NRX = CLU > 1 ? 4 : 0;               // receive slots per side
   static constexpr int STASH = CLU > 1 ? 2 * 32 * NCELL * 5 : 0;  // boundary warps' carried x chain + Wy
   static constexpr int WROWS = 32 / LPR * CY;               // E1 rows per consumer warp
-  static constexpr uint32_t TX_BYTES_A = AEL * 8, TX_BYTES_BC = (BEL + CEL) * 8, RX_BYTES = RXEL * 8;
+  static constexpr uint32_t TX_BYTES_A = AEL * 8, TX_BYTES_B = BEL * 8, TX_BYTES_C = CEL * 8, RX_BYTES = RXEL * 8;
   static constexpr size_t SMEM = 8 * ((size_t)D * SLOT + (size_t)NPB * PEL + 2 * (size_t)NRX * RXEL + STASH) +
                                  8 * (2 * D + 8 + 2 * NRX + 8) + 4 * 8 + 128;
   static_assert(TX % 16 == 0 && TY % CY == 0 && NCONS % 32 == 0 && 32 % LPR == 0, "thread layout");
@@ -230,16 +230,16 @@ __global__ void __launch_bounds__(P25Cfg<TX, TY, D, CLU>::THREADS, 1)
         for (int s = it.s_begin; s <= it.s_end; ++s, ++iv) {
           const uint32_t sl = iv % D;
           mbar_wait(&empty[sl], ((iv / D) & 1) ^ 1);
-          // level 1 computes plane s - R this step only once its z-neighbours are in the ring
+          // level 1 computes plane q = s - R this step only once its z-neighbours are in the ring (then it
+          // needs the coefficients); box B's centre enters the z-ring for every plane of the stream
           const int q = s - R;
-          const bool need1 = q >= 0 && (it.s_begin == 0 || q >= it.s_begin + R);
-          mbar_expect_tx(&full[sl], C::TX_BYTES_A + (need1 ? C::TX_BYTES_BC : 0u));
+          const bool needB = q >= it.s_begin;
+          const bool need1 = needB && (it.s_begin == 0 || q >= it.s_begin + R);
+          mbar_expect_tx(&full[sl], C::TX_BYTES_A + (needB ? C::TX_BYTES_B : 0u) + (need1 ? C::TX_BYTES_C : 0u));
           double* slot = ring + (size_t)sl * C::SLOT;
           tma_load_3d(slot, &mapA, &full[sl], xa, it.gy0, s);
-          if (need1) {
-            tma_load_3d(slot + C::BOFF, &mapB, &full[sl], xb, it.gy0 - R, q);
-            tma_load_4d(slot + C::COFF, &mapC, &full[sl], xa, it.gy0, q, 0);
-          }
+          if (needB) tma_load_3d(slot + C::BOFF, &mapB, &full[sl], xb, it.gy0 - R, q);
+          if (need1) tma_load_4d(slot + C::COFF, &mapC, &full[sl], xa, it.gy0, q, 0);
           if (s + 2 <= it.s_end) {  // warm L2 for the loads two steps ahead (beyond the 2-slot ring)
             tma_prefetch_3d(&mapA, xa, it.gy0, s + 2);
             if (q + 2 >= 0) tma_prefetch_4d(&mapC, xa, it.gy0, q + 2, 0);
@@ -364,9 +364,9 @@ __global__ void __launch_bounds__(P25Cfg<TX, TY, D, CLU>::THREADS, 1)
 #pragma unroll
       for (int j = 0; j < CY; ++j) sts_row<CX, true>(P + (ly0 + j) * TX + x0, v1[j]);
       if constexpr (CLU > 1) {
-        // the previous step's push has read its rows before this barrier releases their rewrite (NPB
-        // steps after they were written)
-        if (bnd && lane == 0) bulk_wait_read<0>();
+        // the push of two steps ago has read its rows before this barrier releases their rewrite (the
+        // plane is rewritten NPB = 3 steps after it was pushed)
+        if (bnd && lane == 0) bulk_wait_read<1>();
       }
       if (!(p.dbg & 2)) named_sync(1, NCONS);
 
@@ -406,7 +406,8 @@ __global__ void __launch_bounds__(P25Cfg<TX, TY, D, CLU>::THREADS, 1)
           // received during the last step
           const double* Pp = sP + (size_t)((iv + C::NPB - 1) % C::NPB) * C::PEL;
           const uint32_t k = (iv + C::NRX - 1) % C::NRX;
-          if (iv > 0) mbar_wait(topB ? &rxbTop[k] : &rxbBot[k], ((iv - 1) / C::NRX) & 1);
+          // acquire at cluster scope: the rows were written by the neighbour's bulk copy
+          if (iv > 0) mbar_wait_cluster(topB ? &rxbTop[k] : &rxbBot[k], ((iv - 1) / C::NRX) & 1);
           const double* rx = (topB ? rxTop : rxBot) + (size_t)k * C::RXEL;
 #pragma unroll
           for (int r = 0; r < CY + 2 * R; ++r) {

@@ -38,3 +38,84 @@ def roofline_glups(kind: int, bandwidth_gbs: float, bt: int = 1, fp64_tflops: fl
     """min(bandwidth / code balance, FP64 peak / flops per update) in GLUP/s (BASELINE.json north star)."""
     mem = bandwidth_gbs / code_balance(kind, bt, write_allocate)
     return min(mem, fp64_tflops * 1e3 / FLOPS_PER_LUP[kind])
+
+
+# ---------------------------------------------------------------------------------------------------------
+# On-chip footprint of one CTA's z-stream (SURVEY NEXT-4): the GPU counterpart of the paper's wavefront
+# cache-block size, Eq. 4.1 / 4.2 (P:881-921).  The paper's cache block of a thread group is
+#     N_xb * [N_D * D_w * (D_w/2 - R + N_F + 1) + 2R (D_w + W_w)]
+# bytes: the domain-sized streams (N_D) over the diamond area plus the wavefront's state rows.  On B200 a
+# CTA plays the thread group: its "cache block" is what its rings keep on chip -- the state planes
+# (the Omega^t footprint of the level-1 extent grown by R) and the N_D coefficient fields over the
+# level-1 extent, each times its ring depth -- held in shared memory (227 KB per CTA), tensor memory
+# (512 columns x 128 lanes x 4 B) and registers.  These functions mirror the kernels' layouts exactly
+# (pipe.cu PipeCfg, pipe25.cu P25Cfg); tests/test_model.py pins them to the configuration tables in the
+# sources, and the GPU tests to the shared memory the launches really request.
+SMEM_LIMIT = 227 * 1024   # opt-in dynamic shared memory per CTA (sm_100a)
+TMEM_COLUMNS = 512        # 32-bit columns per lane, 128 lanes
+RADIUS = {K7C: 1, K7V: 1, K25W: 4, K25V: 4, K25WA: 4}
+
+
+def _ceil16(n):
+    return (n + 15) // 16 * 16
+
+
+def pipe_footprint(kind, bt, TX, TY, CX, CY, DV, DC, WIN, CLU=1):
+    """Footprint of pipe.cu's pipe_kernel<kind, bt, TX, TY, CX, CY, DV, DC, WIN, MINB, UNR, CLU>: shared
+    memory bytes (the kernel's PipeCfg::SMEM), TMEM columns, threads, output tile, and the level work per
+    output update (overlapped-tile redundancy, sum over levels of the level-k extent / (bt * output))."""
+    R, NC, wave = RADIUS[kind], COEF_FIELDS[kind], kind in WAVE_KINDS
+    NS, LPR = TY // CY, TX // CX
+    NCONS = LPR * NS
+    FX, FY = TX + 2 * R, TY + 2 * R
+    OX = TX - 2 * R * (bt - 1)
+    OYP = CLU * TY - 2 * R * (bt - 1)
+    SHV = R & 1
+    FXB = (FX + SHV + 1) // 2 * 2
+    EXB = TX + (2 if R == 1 else 0)
+    VELEMS, CFIELD = FXB * FY, EXB * TY
+    FOFF = 1 if wave else 0
+    NCF = FOFF + NC
+    CF0 = _ceil16(CFIELD) if FOFF else 0
+    CELEMS = CF0 + CFIELD * NC
+    VSLOT, CSLOT = _ceil16(VELEMS), _ceil16(CELEMS)
+    NPL = bt - 1
+    XROW = TX * R
+    doubles = DV * VSLOT + (DC * CSLOT if NCF > 0 else 0) + NPL * 2 * TX * TY + (NPL * 8 * XROW if CLU == 2 else 0)
+    smem = 8 * doubles + 8 * (2 * (DV + DC) + 8 + (12 if CLU == 2 else 0)) + (8 if CLU == 2 else 4) * 4 + 128
+    tmem = 0
+    if WIN < 0:  # TMEM coefficient window: NSL slots of CY * 32 columns per warp, WPQ warps per quadrant
+        NSL = (bt - 1) * R + 1
+        WPQ = (NCONS // 32 + 3) // 4
+        tmem = WPQ * NSL * CY * 32
+    # level-k extent (TX - 2R(k-1)) x (CLU*TY - 2R(k-1)): a cluster pair shrinks only at its outer rows
+    work = sum((TX - 2 * R * (k - 1)) * (CLU * TY - 2 * R * (k - 1)) for k in range(1, bt + 1))
+    return {"smem": smem, "tmem_cols": tmem, "threads": NCONS + 32, "out_tile": (OX, OYP),
+            "level_work": work / (bt * OX * OYP), "fits": smem <= SMEM_LIMIT and tmem <= TMEM_COLUMNS,
+            "ring_bytes": {"state": 8 * DV * VSLOT, "coef": 8 * DC * CSLOT if NCF > 0 else 0,
+                           "level_planes": 8 * NPL * 2 * TX * TY}}
+
+
+def pipe25_footprint(TX, TY, D, CLU):
+    """Footprint of pipe25.cu's two-level 25-point kernel pipe25_kernel<TX, TY, D, CLU> (P25Cfg)."""
+    R, NC = 4, 13
+    NCONS = (TX // 2) * (TY // 2)
+    AEL, BEL = TX * TY, (TX + 2 * R) * (TY + 2 * R)
+    SLOT = _ceil16(AEL) + _ceil16(BEL) + _ceil16(NC * TX * TY)
+    NRX = 4 if CLU > 1 else 0
+    STASH = 2 * 32 * 4 * 5 if CLU > 1 else 0
+    smem = 8 * (D * SLOT + 3 * TX * TY + 2 * NRX * R * TX + STASH) + 8 * (2 * D + 8 + 2 * NRX + 8) + 4 * 8 + 128
+    OX, OYP = TX - 2 * R, CLU * TY - 2 * R
+    work = (TX * CLU * TY + OX * OYP) / (2 * OX * OYP)  # level 1 over every CTA's rows, level 2 = output
+    return {"smem": smem, "tmem_cols": 512, "threads": NCONS + 32, "out_tile": (OX, OYP), "level_work": work,
+            "fits": smem <= SMEM_LIMIT, "coef_box_bytes_per_output": 8 * NC * TX * TY * CLU / (OX * OYP),
+            "ring_bytes": {"slot": 8 * SLOT, "slots": D}}
+
+
+def l2_retention_steps(out_tile, bt, kind, ctas=148, l2_bytes=126 * 2 ** 20):
+    """z-steps for which the L2 holds what all CTAs streamed from DRAM: the drift two neighbouring tiles'
+    z-streams may have and still find each other's overlapping boxes in L2 (the coefficient and state
+    halos overlapped tiles share).  Fresh DRAM bytes per CTA and step = one plane of its output tile at the
+    block's compulsory bytes per cell."""
+    per_step = ctas * out_tile[0] * out_tile[1] * code_balance(kind, bt) * bt
+    return l2_bytes / per_step
