@@ -148,6 +148,7 @@ typedef struct {
   int64_t steps_done;             /* time steps applied since creation (Omega^steps_done is level 0) */
   int64_t launches;               /* kernel launches enqueued since creation / last stats reset */
   int halo;                       /* ST_HALO_* in effect */
+  int smem_bytes, threads;        /* dynamic shared memory and threads per CTA of the bt-deep launches */
 } st_info;
 
 /* Fill *o with defaults: device -1, auto variant/bt/tiles, single rank (local_slabs 1), NULL stream,

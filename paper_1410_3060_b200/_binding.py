@@ -50,7 +50,7 @@ class StInfo(ctypes.Structure):
                                              "tile_x", "tile_y", "zchunk")] + \
                [(n, ctypes.c_int64) for n in ("nx", "ny", "nz", "own_z0", "own_z1", "pitch", "plane",
                                                "local_planes", "device_bytes", "steps_done", "launches")] + \
-               [("halo", ctypes.c_int)]
+               [("halo", ctypes.c_int), ("smem_bytes", ctypes.c_int), ("threads", ctypes.c_int)]
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}

@@ -643,10 +643,12 @@ cudaError_t run_pipe25(const KParams& p0, int zchunk_req, int num_sms, cudaStrea
 // cluster stacked in y (output tile (TX - 8) x (CLU*TY - 8)).
 cudaError_t launch_pipe25v2(const KParams& p, int zchunk_req, int num_sms, int cfg, cudaStream_t stream,
                             LaunchInfo* info) {
+  // Measured on B200 (C4, sustained, profiles/r02_summary.md): the single-CTA tile is the fastest; the
+  // cluster tiles move 15 % fewer L2->SM bytes but stall on their boundary warps (ncu: barrier stalls).
   switch (cfg) {
-    case 1: return run_pipe25<32, 24, 2, 1>(p, zchunk_req, num_sms, stream, info);   // single CTA: 24 x 16
+    case 1: return run_pipe25<32, 20, 2, 2>(p, zchunk_req, num_sms, stream, info);   // cluster pair: 24 x 32
     case 2: return run_pipe25<32, 20, 2, 4>(p, zchunk_req, num_sms, stream, info);   // cluster of 4: 24 x 72
-    default: return run_pipe25<32, 20, 2, 2>(p, zchunk_req, num_sms, stream, info);  // cluster pair: 24 x 32
+    default: return run_pipe25<32, 24, 2, 1>(p, zchunk_req, num_sms, stream, info);  // single CTA: 24 x 16
   }
 }
 

@@ -282,6 +282,7 @@ int default_bt(int kind) {
   switch (kind) {
     case ST_7PT_CONST: return 4;  // tools/sweep.py on B200
     case ST_7PT_VAR: return 3;  // TMEM coefficient window (session 2): 188 vs 154 GLUP/s at bt = 2
+    case ST_25PT_VAR: return 2;  // pipe25.cu (round 2): C4 57.8 vs 52.8 GLUP/s at bt = 1, same box
     default: return 1;
   }
 }
@@ -1212,6 +1213,8 @@ int stencil_info(const stencil_ctx* h, st_info* o) {
   o->local_planes = zl;
   o->device_bytes = h->device_bytes; o->steps_done = h->steps; o->launches = h->launches;
   o->halo = h->halo;
+  o->smem_bytes = h->last_launch.smem;
+  o->threads = h->last_launch.threads;
   return ST_OK;
 }
 

@@ -17,7 +17,7 @@ SHAPES = [(130, 37, 41), (24, 16, 9), (25, 17, 13), (71, 50, 30), (1, 1, 1), (3,
           (48, 150, 12)]
 
 
-# tile_cfg: 0 = cluster pair (24 x 32 output tiles), 1 = single CTA (24 x 16), 2 = cluster of 4 (24 x 72)
+# tile_cfg: 0 = single CTA (24 x 16 output tiles), 1 = cluster pair (24 x 32), 2 = cluster of 4 (24 x 72)
 CFGS = (0, 1, 2)
 
 

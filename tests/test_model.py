@@ -38,3 +38,74 @@ def test_fp64_bound_takes_over():
     assert m.roofline_glups(m.K25W, 6546.9, 2, fp64_tflops=37.0) < 37.0e3 / 30
     with pytest.raises(ValueError):
         m.code_balance(m.K7C, 0)
+
+
+# ------------------------------------------------------------------ footprint model
+import os
+import re
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+KINDS = {"K7C": m.K7C, "K7V": m.K7V, "K25W": m.K25W, "K25V": m.K25V, "K25WA": m.K25WA}
+
+
+def _plans():
+    src = open(os.path.join(ROOT, "paper_1410_3060_b200", "csrc", "pipe.cu")).read()
+    body = src[src.index("cudaError_t launch_pipe("):]
+    plans = []
+    for mac, kind, args in re.findall(r"\b(CFG[UC]?)\((K\w+),\s*([-\d,\s]+)\);", body):
+        bt, TX, TY, CX, CY, DV, DC, WIN, MINB = (int(x) for x in args.split(","))
+        plans.append(dict(kind=KINDS[kind], bt=bt, TX=TX, TY=TY, CX=CX, CY=CY, DV=DV, DC=DC, WIN=WIN,
+                          CLU=2 if mac == "CFGC" else 1))
+    return plans
+
+
+def _plans25():
+    src = open(os.path.join(ROOT, "paper_1410_3060_b200", "csrc", "pipe25.cu")).read()
+    body = src[src.index("cudaError_t launch_pipe25v2("):]
+    return [tuple(int(x) for x in a.split(",")) for a in re.findall(r"run_pipe25<([\d,\s]+)>", body)]
+
+
+def test_every_configured_plan_fits_on_chip():
+    plans = _plans()
+    assert len(plans) >= 40  # the whole table was parsed
+    for p in plans:
+        f = m.pipe_footprint(p["kind"], p["bt"], p["TX"], p["TY"], p["CX"], p["CY"], p["DV"], p["DC"], p["WIN"],
+                             p["CLU"])
+        assert f["fits"], (p, f)
+        if p["WIN"] < 0:  # TMEM-window plans also keep a second CTA off the SM (pipe.cu static_assert)
+            assert f["smem"] > 116 * 1024 and f["tmem_cols"] <= 512, (p, f)
+    p25 = _plans25()
+    assert len(p25) == 3
+    for TX, TY, D, CLU in p25:
+        f = m.pipe25_footprint(TX, TY, D, CLU)
+        assert f["fits"] and f["out_tile"][0] == TX - 8, f
+
+
+def test_footprint_rules_out_what_the_design_says():
+    # DESIGN.md §5/§8: in the generic pipe kernel a 25-point variable bt = 2 plan needs (R + 2) coefficient
+    # slots of 13 fields over the level-1 extent -- over the shared memory for any tile with an output
+    f = m.pipe_footprint(m.K25V, 2, 32, 24, 2, 2, 6, 6, 0)
+    assert not f["fits"] and f["ring_bytes"]["coef"] > 320 * 1024
+    # ... while the two-level kernel that carries the z chains in TMEM needs one slot per step
+    assert m.pipe25_footprint(32, 24, 2, 1)["fits"]
+    # a 7v bt = 4 TMEM window of 3 warps per lane quadrant would need 576 of the 512 columns
+    f = m.pipe_footprint(m.K7V, 4, 32, 36, 2, 2, 4, 2, -1)
+    assert f["tmem_cols"] > 512 and not f["fits"]
+
+
+def test_level_work_matches_the_trapezoid():
+    # C2 default bt = 3: level-1 extent 32 x 28, output 28 x 24 -> (32*28 + 30*26 + 28*24) / (3 * 28 * 24)
+    f = m.pipe_footprint(m.K7V, 3, 32, 28, 2, 2, 4, 3, -1)
+    assert f["out_tile"] == (28, 24)
+    assert f["level_work"] == pytest.approx((32 * 28 + 30 * 26 + 28 * 24) / (3 * 28 * 24))
+    # the cluster pair shares the y halo: less redundant work than two single tiles
+    assert m.pipe25_footprint(32, 20, 2, 2)["level_work"] < m.pipe25_footprint(32, 24, 2, 1)["level_work"]
+    # the 25v bt = 2 single tile 32 x 24 -> 24 x 16: (768 + 384) / (2 * 384) = 1.5
+    assert m.pipe25_footprint(32, 24, 2, 1)["level_work"] == pytest.approx(1.5)
+
+
+def test_l2_retention():
+    # C4 at bt = 2 with 24 x 16 output tiles: 148 CTAs stream 148 * 384 cells * 120 B of fresh DRAM bytes
+    # per z-step, so the 126 MiB L2 holds ~19 steps of them
+    assert m.l2_retention_steps((24, 16), 2, m.K25V) == pytest.approx(126 * 2 ** 20 / (148 * 384 * 120))
+    assert m.l2_retention_steps((24, 32), 2, m.K25V) == pytest.approx(m.l2_retention_steps((24, 16), 2, m.K25V) / 2)
