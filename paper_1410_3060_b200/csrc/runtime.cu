@@ -25,6 +25,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <mutex>
 #include <cstdlib>
 #include <cstdarg>
@@ -190,6 +191,7 @@ struct stencil_ctx {
   bool peer_ready = false;       // neighbours wired (loopback: at create; processes: after import)
   bool ipc = false;              // peers are other processes (CUDA IPC)
   uint64_t* flags = nullptr;     // this rank's halo-arrival counters: [0] from below, [1] from above
+  cudaStream_t poll_stream = nullptr;  // host-side polls of `flags` (peer_wait)
   struct Peer {
     bool on = false;
     bool opened = false;  // pointers come from cudaIpcOpenMemHandle (closed at release)
@@ -261,6 +263,8 @@ void release(stencil_ctx* h) {
   if (h->comm && nccl()) nccl()->CommDestroy(h->comm);
   h->comm = nullptr;
   if (h->comm_stream) cudaStreamSynchronize(h->comm_stream), cudaStreamDestroy(h->comm_stream);
+  if (h->poll_stream) cudaStreamDestroy(h->poll_stream);
+  h->poll_stream = nullptr;
   if (h->ev_edge) cudaEventDestroy(h->ev_edge);
   if (h->ev_halo) cudaEventDestroy(h->ev_halo);
   h->comm_stream = nullptr;
@@ -733,6 +737,8 @@ int launch_range(stencil_ctx* h, Slab& s, int b, int d0, int d1, int64_t z0, int
   return ST_OK;
 }
 
+int peer_wait(stencil_ctx* h, int64_t target);
+
 // One block of b levels on every slab, then the halo exchange of the new level(s).
 // Multi-slab schedule ("halo-first"): the edge kernels compute the R*b boundary planes of
 // each slab that has a neighbour, the exchange of those planes starts on comm_stream, and the interior
@@ -774,13 +780,8 @@ int run_block(stencil_ctx* h, int b) {
     if (h->ipc) {
       // wait until both neighbours have stored block blocks-1's halos into this rank's buffers (and
       // thereby finished reading the buffers this block's remote stores overwrite)
-      if (!m.wait || !m.write) { set_err("stream memory operations unavailable"); h->poisoned = true; return ST_E_CUDA; }
-      for (int q = 0; q < 2; ++q)
-        if (h->peer[q].on) {
-          CUresult r = m.wait((CUstream)h->stream, (CUdeviceptr)(h->flags + q), (cuuint64_t)h->blocks,
-                              CU_STREAM_WAIT_VALUE_GEQ);
-          if (r != CUDA_SUCCESS) { set_err("cuStreamWaitValue64 failed (%d)", (int)r); h->poisoned = true; return ST_E_CUDA; }
-        }
+      if (!m.write) { set_err("stream memory operations unavailable"); h->poisoned = true; return ST_E_CUDA; }
+      if ((rc = peer_wait(h, h->blocks))) return rc;
     }
     for (auto& s : h->slabs)
       if ((rc = launch_range(h, s, b, d0, d1, s.lo, s.hi, true))) return rc;
@@ -850,6 +851,49 @@ __global__ void peer_poke_kernel(uint64_t* below_flags, uint64_t* above_flags, u
 
 uint64_t handshake_magic(int rank) { return 0x5EED000000000000ull + (uint64_t)rank; }
 
+// ST_HALO_PEER across processes: wait until both neighbours' block counters (written into this rank's flag
+// words by their streams after their kernels, cuStreamWriteValue64) reach `target`.  By default the HOST
+// waits -- it polls the flag words with small device-to-host copies on a private stream, with a timeout --
+// so no GPU stream ever blocks on another process (a neighbour that died or stalled becomes an ST_E_STATE
+// error here instead of a hung stream; the profiling recipe warns against device-side cross-process waits
+// on a shared GPU).  STENCIL_PEER_DEVICE_WAIT=1 enqueues cuStreamWaitValue64 on the handle's stream instead
+// (asynchronous; the pre-round-2 behaviour).  Blocks last milliseconds, the poll microseconds.
+int peer_wait(stencil_ctx* h, int64_t target) {
+  if (env_int("STENCIL_PEER_DEVICE_WAIT")) {
+    const MemOps& m = memops();
+    if (!m.wait) { set_err("stream memory operations unavailable"); h->poisoned = true; return ST_E_CUDA; }
+    for (int q = 0; q < 2; ++q)
+      if (h->peer[q].on) {
+        CUresult r = m.wait((CUstream)h->stream, (CUdeviceptr)(h->flags + q), (cuuint64_t)target,
+                            CU_STREAM_WAIT_VALUE_GEQ);
+        if (r != CUDA_SUCCESS) { set_err("cuStreamWaitValue64 failed (%d)", (int)r); h->poisoned = true; return ST_E_CUDA; }
+      }
+    return ST_OK;
+  }
+  if (!h->poll_stream) {
+    cudaError_t e = cudaStreamCreateWithFlags(&h->poll_stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) return cuda_fail(h, e, "peer poll stream");
+  }
+  const int timeout_ms = env_int("STENCIL_PEER_TIMEOUT_MS") > 0 ? env_int("STENCIL_PEER_TIMEOUT_MS") : 120000;
+  uint64_t got[2] = {0, 0};
+  const auto t0 = std::chrono::steady_clock::now();
+  for (int spins = 0;; ++spins) {
+    cudaError_t e = cudaMemcpyAsync(got, h->flags, sizeof got, cudaMemcpyDeviceToHost, h->poll_stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(h->poll_stream);
+    if (e != cudaSuccess) return cuda_fail(h, e, "peer flag poll");
+    if ((!h->peer[0].on || (int64_t)got[0] >= target) && (!h->peer[1].on || (int64_t)got[1] >= target)) return ST_OK;
+    const auto ms = std::chrono::duration_cast<std::chrono::milliseconds>(std::chrono::steady_clock::now() - t0).count();
+    if (ms > timeout_ms) {
+      set_err("ST_HALO_PEER: the neighbours' halos of block %lld did not arrive within %d ms (flags %llu %llu); "
+              "a neighbour rank stopped or failed", (long long)target, timeout_ms, (unsigned long long)got[0],
+              (unsigned long long)got[1]);
+      h->poisoned = true;
+      return ST_E_STATE;
+    }
+    if (spins > 16) usleep(spins > 1000 ? 1000 : 20);
+  }
+}
+
 // Several full blocks of a single-slab Jacobi grid in ONE pipe-kernel launch (dependency-driven
 // scheduling across blocks, pipe.cu): the tail of block i can overlap the start of block i+1.
 // Opt-in (STENCIL_MULTIBLOCK=1): measured 1-7 % slower than one launch per block on B200 (C2 ~189 vs
@@ -896,15 +940,7 @@ int run_blocks_fused(stencil_ctx* h, int nblk, int b) {
 // so far (no remote store into this rank's memory is still in flight afterwards).
 int wait_peers(stencil_ctx* h) {
   if (!h->ipc || !h->peer_ready) return ST_OK;
-  const MemOps& m = memops();
-  if (!m.wait) { set_err("stream memory operations unavailable"); h->poisoned = true; return ST_E_CUDA; }
-  for (int q = 0; q < 2; ++q)
-    if (h->peer[q].on) {
-      CUresult r = m.wait((CUstream)h->stream, (CUdeviceptr)(h->flags + q), (cuuint64_t)h->blocks,
-                          CU_STREAM_WAIT_VALUE_GEQ);
-      if (r != CUDA_SUCCESS) { set_err("cuStreamWaitValue64 failed (%d)", (int)r); h->poisoned = true; return ST_E_CUDA; }
-    }
-  return ST_OK;
+  return peer_wait(h, h->blocks);
 }
 
 int check_handle(stencil_ctx* h) {

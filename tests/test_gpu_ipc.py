@@ -3,10 +3,15 @@ creates its slab with halo=ST_HALO_PEER, the descriptors are all-gathered over t
 stencil_peer_import opens the neighbour's state buffers and flag block with cudaIpcOpenMemHandle, and
 stencil_peer_handshake sends rank-tagged words through both transfer paths the fused exchange uses (a
 kernel's stores into the neighbour's memory, a stream-ordered cuStreamWriteValue64) and polls for the
-neighbour's words from the host.  Nothing waits on the GPU for the other process (no stencil_run here:
-its per-block stream waits would need a GPU per rank, see the profiling recipe)."""
+neighbour's words from the host.  Then stencil_run(T) across 2 and 3 processes: every block's kernel stores
+the neighbours' halo planes into their memory through the IPC mappings, announces the block with a
+stream-ordered flag write, and each rank's HOST waits for its neighbours' flags before enqueuing the next
+block (runtime.cu peer_wait) -- no GPU stream or kernel ever waits on another process (the profiling
+recipe: ranks that wait on one another on the device must not share a GPU).  A host-side watchdog kills
+the ranks if the run does not finish."""
 import os
 import socket
+import time
 
 import numpy as np
 import pytest
@@ -60,3 +65,52 @@ def test_ipc_wiring_and_handshake_two_processes(tmp_path, world, mode):
     mp.spawn(_worker, args=(world, port, str(tmp_path), mode), nprocs=world, join=True)
     res = [open(tmp_path / f"r{r}.txt").read() for r in range(world)]
     assert all(r.startswith("ok halo=1") for r in res), res
+
+
+def _run_worker(rank, world, port, out_dir, kind, n, Ts):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    os.environ["STENCIL_PEER_TIMEOUT_MS"] = "60000"
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_1410_3060_b200 as st
+        torch.cuda.set_device(0)
+        with st.Grid(kind, *n, seed=13, rank=rank, nranks=world, halo=st.ST_HALO_PEER) as g:
+            for T in Ts:  # consecutive runs: the block counters and halos carry over
+                g.run(T)
+            g.sync()
+            info = g.info()
+            own = g.read_planes(0, info["own_z0"], info["own_z1"])
+            dist.barrier()  # every rank has read before any handle (and its IPC-mapped memory) goes away
+        np.save(os.path.join(out_dir, f"r{rank}.npy"), own)
+        with open(os.path.join(out_dir, f"r{rank}.txt"), "w") as f:
+            f.write(f"ok {info['own_z0']} {info['own_z1']} bt={info['bt']} halo={info['halo']}")
+    except Exception as e:
+        with open(os.path.join(out_dir, f"r{rank}.txt"), "w") as f:
+            f.write(f"error {e}")
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("kind,n,Ts", [(2, (40, 33, 37), (7, 5)), (4, (70, 29, 41), (5, 4))])
+def test_peer_halo_stencil_run_across_processes(tmp_path, world, kind, n, Ts):
+    import paper_1410_3060_b200 as st
+    port = _free_port()
+    ctx = mp.spawn(_run_worker, args=(world, port, str(tmp_path), kind, n, Ts), nprocs=world, join=False)
+    deadline = time.time() + 240
+    while not ctx.join(timeout=5):
+        if time.time() > deadline:  # watchdog: a hung rank fails the test instead of wedging the box
+            for p in ctx.processes:
+                p.kill()
+            pytest.fail("cross-process ST_HALO_PEER run did not finish in 240 s")
+    res = [open(tmp_path / f"r{r}.txt").read() for r in range(world)]
+    assert all(r.startswith("ok") and "halo=1" in r for r in res), res
+    with st.Grid(kind, *n, seed=13) as g:
+        for T in Ts:
+            g.run(T)
+        ref = g.read(0)
+    for r, line in enumerate(res):
+        z0, z1 = (int(x) for x in line.split()[1:3])
+        got = np.load(tmp_path / f"r{r}.npy")
+        assert np.array_equal(got, ref[z0:z1]), (r, z0, z1)

@@ -47,10 +47,12 @@ def test_loopback_slabs_bitwise_equal_single(kind, n, T, P):
 
 
 @pytest.mark.parametrize("kind,n,T", CASES)
-def test_loopback_slabs_oracle_parity(kind, n, T):
+@pytest.mark.parametrize("halo", [st.ST_HALO_COPY, st.ST_HALO_PEER])
+def test_loopback_slabs_oracle_parity(kind, n, T, halo):
     inp = synth.make_inputs(kind, *n, seed=31)
     o_new, o_old = oracle.run(inp, T)
-    g_new, g_old, info = run(kind, n, T, nranks=4, local_slabs=4)
+    g_new, g_old, info = run(kind, n, T, nranks=4, local_slabs=4, halo=halo)
+    assert info["halo"] == halo
     assert_parity(kind, g_new, g_old, o_new, o_old, inp.R, 1e-12, inputs=inp)
 
 
