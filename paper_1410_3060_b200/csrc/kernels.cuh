@@ -54,6 +54,8 @@ struct KParams {
   int tband;   // pipe kernel, single-block launches: tile order within a z-chunk (STENCIL_TILE_BAND;
                // 0 = row-major, w > 0 = bands of w tile columns walked row by row, so y-neighbours are w
                // ids apart instead of ntx)
+  int tblk_w, tblk_h;  // tile order in blocks of tblk_w x tblk_h tiles (0 = row-major; set by launchers)
+  int lockstep;        // pipe25: static round-robin items, CTAs start each round together (launcher)
   int walign;  // pipe kernel: tiles write sector-aligned output segments (STENCIL_WALIGN=1; default 0:
                // measured slower under the power cap for OX % 4 != 0, profiles/r01_summary.md)
 };

@@ -31,6 +31,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -220,6 +221,12 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN,
             g = cid[qs];
             mbar_arrive_remote(dsmem_addr(&cempty[qs], 0u));
           }
+        } else if (p.lockstep) {
+          // static rounds (single-block launches): CTA c takes item n * G + c; the tile order (decode,
+          // tblk_*) makes a round a compact patch, and the rounds start together (below), so the y-halo
+          // boxes overlapping tiles share hit L2 (pipe25.cu)
+          g = (int)(n * gridDim.x + blockIdx.x);
+          if (g >= items) g = -1;
         } else {
           g = (int)atomicAdd(p.sched, 1u);
           if (g >= items * p.nblk) g = -1;
@@ -228,7 +235,23 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN,
         mbar_arrive(&itemFull[qs]);  // release: the id is visible to the consumers' acquire
         if (g < 0) break;
         const int blk = g / items, item = g - blk * items;
-        if ((p.dbg & 8) && item == 0) continue;
+        if (CLU == 1 && p.lockstep) {
+          // round n: wait until every CTA with an item in round n - 1 has issued all its loads (all CTAs
+          // are resident, one per SM, so this grid-wide wait cannot deadlock)
+          if (n > 0) {
+            const unsigned int want = (unsigned int)min((long long)n * gridDim.x, (long long)items);
+            unsigned int v;
+            for (;;) {
+              asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p.sched) : "memory");
+              if (v >= want) break;
+              __nanosleep(128);
+            }
+          }
+        }
+        if ((p.dbg & 8) && item == 0) {
+          if (CLU == 1 && p.lockstep) { __threadfence(); atomicAdd(p.sched, 1u); }
+          continue;
+        }
         Item it = decode<R, BT - 1, OX, C::OYP>(item, ntx, nty, p);
         it.gy0 += (int)crank * TY;
         if (blk > 0) {
@@ -280,6 +303,10 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN,
               tma_load_4d(sC + (size_t)sc * C::CSLOT, &mapC, fc, xc, it.gy0, s - R, 0);
             }
           }
+        }
+        if (CLU == 1 && p.lockstep) {  // round n issued
+          __threadfence();
+          atomicAdd(p.sched, 1u);
         }
       }
       // every CTA has drawn its terminating id before the last one gets here: reset for the next launch
@@ -756,6 +783,18 @@ cudaError_t run_pipe(const KParams& p0, int zchunk_req, int num_sms, cudaStream_
   int occ = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, C::THREADS, C::SMEM);
   int grid = (int)std::min<long long>(items * std::max(1, p.nblk), (long long)std::max(1, occ) * num_sms);
+  // single-block launches of single-CTA tiles: lockstep rounds over compact patches of tiles, so the
+  // overlapping halo boxes of y-neighbours are streamed at the same time and hit L2 (STENCIL_SCHED=0:
+  // dynamic work counter, row-major tiles)
+  static const int sched_env = getenv("STENCIL_SCHED") ? atoi(getenv("STENCIL_SCHED")) : 1;
+  if (CLU == 1 && sched_env && p.nblk <= 1 && p.tband == 0 && occ <= 1) {
+    p.lockstep = 1;
+    static const int bw_env = getenv("STENCIL_TILE_BLOCK") ? atoi(getenv("STENCIL_TILE_BLOCK")) : 0;
+    int bw = bw_env > 0 ? bw_env : (int)(std::sqrt((double)grid * TY / TX) + 0.5);
+    bw = std::max(1, std::min(bw, ntx));
+    p.tblk_w = bw;
+    p.tblk_h = std::max(1, (grid + bw - 1) / bw);
+  }
   if (p.nblk > 1 && (C::WAVE || CLU != 1 || items > kMaxDoneItems || !p.done)) return cudaErrorInvalidValue;
   if constexpr (CLU == 1) {
     kern<<<grid, C::THREADS, C::SMEM, stream>>>(mapV, mapC, mapA, p, ntx, nty, (int)items);

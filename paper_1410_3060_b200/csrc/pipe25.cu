@@ -45,6 +45,8 @@
 #include "sm100.cuh"
 
 #include <algorithm>
+#include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 namespace st {
@@ -215,6 +217,12 @@ __global__ void __launch_bounds__(P25Cfg<TX, TY, D, CLU>::THREADS, 1)
             g = cid[qs];
             mbar_arrive_remote(dsmem_addr(&cempty[qs], 0u));
           }
+        } else if (p.lockstep) {
+          // static rounds: CTA c takes item n * G + c; the tile order (decode, tblk_*) makes a round a
+          // compact patch of tiles, and the rounds start together (below), so overlapping tiles stream the
+          // same planes at the same time and their shared halo boxes hit L2
+          g = (int)(n * gridDim.x + blockIdx.x);
+          if (g >= items) g = -1;
         } else {
           g = (int)atomicAdd(p.sched, 1u);
           if (g >= items) g = -1;
@@ -222,12 +230,12 @@ __global__ void __launch_bounds__(P25Cfg<TX, TY, D, CLU>::THREADS, 1)
         itemq[qs] = g;
         mbar_arrive(&itemFull[qs]);  // release: the id is visible to the consumers' acquire
         if (g < 0) break;
-        if ((p.dbg & 8) && g == 0) continue;
+        const bool skip = (p.dbg & 8) && g == 0;  // fault injection: item 0 never loaded (nor computed)
         Item it = decode<R, 1, C::OX, C::OYP>(g, ntx, nty, p);
         it.gy0 += (int)crank * TY;
         const int xb = ((it.gx0 - R + p.xoff) & ~1) - (p.xoff & ~1);  // box B (footprint)
         const int xa = ((it.gx0 + p.xoff) & ~1) - (p.xoff & ~1);      // boxes A, C (level-1 extent)
-        for (int s = it.s_begin; s <= it.s_end; ++s, ++iv) {
+        for (int s = it.s_begin; s <= it.s_end && !skip; ++s, ++iv) {
           const uint32_t sl = iv % D;
           mbar_wait(&empty[sl], ((iv / D) & 1) ^ 1);
           // level 1 computes plane q = s - R this step only once its z-neighbours are in the ring (then it
@@ -243,6 +251,19 @@ __global__ void __launch_bounds__(P25Cfg<TX, TY, D, CLU>::THREADS, 1)
           if (s + 2 <= it.s_end) {  // warm L2 for the loads two steps ahead (beyond the 2-slot ring)
             tma_prefetch_3d(&mapA, xa, it.gy0, s + 2);
             if (q + 2 >= 0) tma_prefetch_4d(&mapC, xa, it.gy0, q + 2, 0);
+          }
+        }
+        if (CLU == 1 && p.lockstep) {
+          // round n issued: wait until every CTA with an item in round n has issued its loads too (all CTAs
+          // are resident, one per SM, so this grid-wide wait cannot deadlock)
+          const unsigned int want = (unsigned int)min((long long)(n + 1) * gridDim.x, (long long)items);
+          __threadfence();
+          atomicAdd(p.sched, 1u);
+          unsigned int v;
+          for (;;) {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p.sched) : "memory");
+            if (v >= want) break;
+            __nanosleep(128);
           }
         }
       }
@@ -623,6 +644,17 @@ cudaError_t run_pipe25(const KParams& p0, int zchunk_req, int num_sms, cudaStrea
       !make_tensor_map(&mapC, p.coef_raw + X0, 4, p.pitch, MX, MY, p.zl, C::NC, p.plane, p.cstride, TX, TY, C::NC))
     return cudaErrorInvalidValue;
   const int grid = (int)std::min<long long>(items, clusters) * CLU;
+  // single-CTA tiles: lockstep rounds over compact patches of tiles (STENCIL_SCHED=0: dynamic, row-major)
+  static const int sched_env = getenv("STENCIL_SCHED") ? atoi(getenv("STENCIL_SCHED")) : 1;
+  if (CLU == 1 && sched_env && p.nblk <= 1 && p.tband == 0) {
+    p.lockstep = 1;
+    // patch shape: a missed block edge costs R*2 halo rows x TX (bottom) or R*2 columns x TY (right)
+    static const int bw_env = getenv("STENCIL_TILE_BLOCK") ? atoi(getenv("STENCIL_TILE_BLOCK")) : 0;
+    int bw = bw_env > 0 ? bw_env : (int)(std::sqrt((double)grid * TY / TX) + 0.5);
+    bw = std::max(1, std::min(bw, ntx));
+    p.tblk_w = bw;
+    p.tblk_h = std::max(1, (grid + bw - 1) / bw);
+  }
   if constexpr (CLU == 1) {
     kern<<<grid, C::THREADS, C::SMEM, stream>>>(mapA, mapB, mapC, p, ntx, nty, (int)items);
   } else {

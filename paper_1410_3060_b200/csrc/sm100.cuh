@@ -143,6 +143,14 @@ __device__ __forceinline__ Item decode(int item, int ntx, int nty, const KParams
     const int w = p.tband, band = t / (w * nty), r = t - band * w * nty, wb = min(w, ntx - band * w);
     ty = r / wb;
     tx = band * w + (r - ty * wb);
+  } else if (p.tblk_w > 0 && p.nblk <= 1) {
+    // blocks of tblk_w x tblk_h tiles (row-major blocks, row-major inside; edge blocks narrower): a run
+    // of ~tblk_w*tblk_h consecutive items is a compact patch, so overlapping tiles run concurrently
+    const int BW = p.tblk_w, BH = p.tblk_h;
+    const int by = t / (ntx * BH), rem = t - by * ntx * BH, h = min(BH, nty - by * BH);
+    const int bx = rem / (BW * h), rem2 = rem - bx * BW * h, w = min(BW, ntx - bx * BW);
+    ty = by * BH + rem2 / w;
+    tx = bx * BW + (rem2 - (rem2 / w) * w);
   } else {
     ty = t / ntx;
     tx = t - ty * ntx;
