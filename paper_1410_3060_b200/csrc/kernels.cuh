@@ -55,7 +55,8 @@ struct KParams {
                // 0 = row-major, w > 0 = bands of w tile columns walked row by row, so y-neighbours are w
                // ids apart instead of ntx)
   int tblk_w, tblk_h;  // tile order in blocks of tblk_w x tblk_h tiles (0 = row-major; set by launchers)
-  int lockstep;        // pipe25: static round-robin items, CTAs start each round together (launcher)
+  int lockstep;        // pipe kernels: static round-robin items, CTAs start each round together (launcher)
+  int pfd;             // pipe25: TMA L2-prefetch distance in steps (launcher; STENCIL_PF)
   int walign;  // pipe kernel: tiles write sector-aligned output segments (STENCIL_WALIGN=1; default 0:
                // measured slower under the power cap for OX % 4 != 0, profiles/r01_summary.md)
 };

@@ -248,9 +248,9 @@ __global__ void __launch_bounds__(P25Cfg<TX, TY, D, CLU>::THREADS, 1)
           tma_load_3d(slot, &mapA, &full[sl], xa, it.gy0, s);
           if (needB) tma_load_3d(slot + C::BOFF, &mapB, &full[sl], xb, it.gy0 - R, q);
           if (need1) tma_load_4d(slot + C::COFF, &mapC, &full[sl], xa, it.gy0, q, 0);
-          if (s + 2 <= it.s_end) {  // warm L2 for the loads two steps ahead (beyond the 2-slot ring)
-            tma_prefetch_3d(&mapA, xa, it.gy0, s + 2);
-            if (q + 2 >= 0) tma_prefetch_4d(&mapC, xa, it.gy0, q + 2, 0);
+          if (p.pfd > 0 && s + p.pfd <= it.s_end) {  // warm L2 for the loads pfd steps ahead (beyond the ring)
+            tma_prefetch_3d(&mapA, xa, it.gy0, s + p.pfd);
+            if (q + p.pfd >= 0) tma_prefetch_4d(&mapC, xa, it.gy0, q + p.pfd, 0);
           }
         }
         if (CLU == 1 && p.lockstep) {
@@ -644,6 +644,8 @@ cudaError_t run_pipe25(const KParams& p0, int zchunk_req, int num_sms, cudaStrea
       !make_tensor_map(&mapC, p.coef_raw + X0, 4, p.pitch, MX, MY, p.zl, C::NC, p.plane, p.cstride, TX, TY, C::NC))
     return cudaErrorInvalidValue;
   const int grid = (int)std::min<long long>(items, clusters) * CLU;
+  static const int pfd_env = getenv("STENCIL_PF") ? atoi(getenv("STENCIL_PF")) : 2;
+  p.pfd = pfd_env;  // L2 prefetch distance in steps (0 = none)
   // single-CTA tiles: lockstep rounds over compact patches of tiles (STENCIL_SCHED=0: dynamic, row-major)
   static const int sched_env = getenv("STENCIL_SCHED") ? atoi(getenv("STENCIL_SCHED")) : 1;
   if (CLU == 1 && sched_env && p.nblk <= 1 && p.tband == 0) {

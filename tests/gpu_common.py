@@ -51,3 +51,32 @@ def assert_parity(kind, g_new, g_old, o_new, o_old, R, tol, inputs=None):
         assert np.array_equal(g_new[m], inputs.V[m])
         if kind in WAVES:
             assert np.array_equal(g_old[m], inputs.V[m])
+
+
+def record(config, **values):
+    """Append parity / oracle-timing facts of a full-size test to $STENCIL_REPORT_DIR/parity.json (read by
+    tools/report.py for the SURVEY d.6 rows; nothing is recorded when the variable is unset)."""
+    import json
+    import os
+    d = os.environ.get("STENCIL_REPORT_DIR")
+    if not d:
+        return
+    os.makedirs(d, exist_ok=True)
+    path = os.path.join(d, "parity.json")
+    try:
+        cur = json.load(open(path))
+    except (OSError, ValueError):
+        cur = {}
+    cur.setdefault(config, {}).update({k: (float(v) if hasattr(v, "__float__") and not isinstance(v, (int, str))
+                                           else v) for k, v in values.items()})
+    json.dump(cur, open(path, "w"), indent=1, sort_keys=True)
+
+
+def timed_oracle(inp, T):
+    """oracle.run with its wall time and thread count (d.6 oracle_threads / oracle_s)."""
+    import os
+    import time
+    n = len(os.sched_getaffinity(0))
+    t0 = time.perf_counter()
+    out = oracle.run(inp, T, n)
+    return out, time.perf_counter() - t0, n

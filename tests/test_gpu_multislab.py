@@ -134,9 +134,9 @@ def test_peer_halo_needs_pipe_variant():
 def test_peer_ranks_as_handles_in_one_process(kind, n, T, P):
     """The one-slab-per-rank ST_HALO_PEER protocol (descriptor export/import, remote stores into the
     neighbour's buffers, stream-ordered flag write / wait per block) with P ranks emulated as P handles
-    of this process on their own streams (descriptors from the same process are used without IPC).
-    The streams only wait on flags with cuStreamWaitValue64 -- no kernel spins -- and every rank's work
-    is enqueued before any stream can block.  Owned planes of all ranks == one slab, bitwise."""
+    of this process on their own streams and host threads (descriptors from the same process are used
+    without IPC).  Each rank's host waits for its neighbours' block flags before enqueuing a block -- no
+    kernel or stream waits on another rank.  Owned planes of all ranks == one slab, bitwise."""
     import torch
     ref = run(kind, n, T)
     streams = [torch.cuda.Stream() for _ in range(P)]
@@ -158,9 +158,25 @@ def test_peer_ranks_as_handles_in_one_process(kind, n, T, P):
                 pass
         for g in gs:
             g.peer_handshake(timeout_ms=2000)
-        for t in (T if isinstance(T, tuple) else (T,)):
-            for g in gs:
-                g.run(t)
+        # every rank's host waits for its neighbours' block flags before enqueuing its next block
+        # (runtime.cu peer_wait), so each rank runs from its own host thread, as separate processes do
+        import threading
+        errs = []
+
+        def drive(g):
+            try:
+                torch.cuda.set_device(0)
+                for t in (T if isinstance(T, tuple) else (T,)):
+                    g.run(t)
+                g.sync()
+            except Exception as e:  # noqa: BLE001 -- reported below
+                errs.append(e)
+        th = [threading.Thread(target=drive, args=(g,)) for g in gs]
+        for x in th:
+            x.start()
+        for x in th:
+            x.join(timeout=120)
+        assert not errs and not any(x.is_alive() for x in th), errs
         new = np.zeros(gs[0].padded_shape)
         old = np.zeros(gs[0].padded_shape)
         for g in gs:
