@@ -644,7 +644,7 @@ cudaError_t run_pipe25(const KParams& p0, int zchunk_req, int num_sms, cudaStrea
       !make_tensor_map(&mapC, p.coef_raw + X0, 4, p.pitch, MX, MY, p.zl, C::NC, p.plane, p.cstride, TX, TY, C::NC))
     return cudaErrorInvalidValue;
   const int grid = (int)std::min<long long>(items, clusters) * CLU;
-  static const int pfd_env = getenv("STENCIL_PF") ? atoi(getenv("STENCIL_PF")) : 2;
+  static const int pfd_env = getenv("STENCIL_PF") ? atoi(getenv("STENCIL_PF")) : 0;
   p.pfd = pfd_env;  // L2 prefetch distance in steps (0 = none)
   // single-CTA tiles: lockstep rounds over compact patches of tiles (STENCIL_SCHED=0: dynamic, row-major)
   static const int sched_env = getenv("STENCIL_SCHED") ? atoi(getenv("STENCIL_SCHED")) : 1;

@@ -24,6 +24,31 @@ def run(kind, n, T, **kw):
     return new, old, info
 
 
+def run_ranks(gs, T):
+    """Run ST_HALO_PEER ranks emulated as handles of this process: every rank's host waits for its
+    neighbours' block flags before enqueuing its next block (runtime.cu peer_wait), so each rank runs
+    T (an int, or a tuple of consecutive runs) from its own host thread, as separate processes do."""
+    import threading
+
+    import torch
+    errs = []
+
+    def drive(g):
+        try:
+            torch.cuda.set_device(0)
+            for t in (T if isinstance(T, tuple) else (T,)):
+                g.run(t)
+            g.sync()
+        except Exception as e:  # noqa: BLE001 -- reported below
+            errs.append(e)
+    th = [threading.Thread(target=drive, args=(g,)) for g in gs]
+    for x in th:
+        x.start()
+    for x in th:
+        x.join(timeout=120)
+    assert not errs and not any(x.is_alive() for x in th), errs
+
+
 CASES = [
     (synth.K7C, (40, 33, 37), 11),
     (synth.K7V, (40, 33, 37), 9),
@@ -158,25 +183,7 @@ def test_peer_ranks_as_handles_in_one_process(kind, n, T, P):
                 pass
         for g in gs:
             g.peer_handshake(timeout_ms=2000)
-        # every rank's host waits for its neighbours' block flags before enqueuing its next block
-        # (runtime.cu peer_wait), so each rank runs from its own host thread, as separate processes do
-        import threading
-        errs = []
-
-        def drive(g):
-            try:
-                torch.cuda.set_device(0)
-                for t in (T if isinstance(T, tuple) else (T,)):
-                    g.run(t)
-                g.sync()
-            except Exception as e:  # noqa: BLE001 -- reported below
-                errs.append(e)
-        th = [threading.Thread(target=drive, args=(g,)) for g in gs]
-        for x in th:
-            x.start()
-        for x in th:
-            x.join(timeout=120)
-        assert not errs and not any(x.is_alive() for x in th), errs
+        run_ranks(gs, T)
         new = np.zeros(gs[0].padded_shape)
         old = np.zeros(gs[0].padded_shape)
         for g in gs:
@@ -263,8 +270,7 @@ def test_host_slab_inputs(kind, n, T, bt, P):
                 pass
         for g in gs:
             g.peer_handshake(timeout_ms=2000)
-        for g in gs:
-            g.run(T)
+        run_ranks(gs, T)
         for r, g in enumerate(gs):
             i = g.info()
             z0, z1 = i["own_z0"], i["own_z1"]
