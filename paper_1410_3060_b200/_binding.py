@@ -351,9 +351,12 @@ class Grid:
     def __init__(self, kind, nx, ny, nz, *, seed=None, scalars=None, v0=None, u0=None, coeff=None,
                  variant=ST_VARIANT_AUTO, bt=0, zchunk=0, tile_cfg=0, rank=0, nranks=1, nccl_id=None,
                  local_slabs=1, halo=ST_HALO_COPY, wire_peers=True,
-                 device=None, stream=None, torch_memory=True, tuned=False, host_slab=False):
+                 device=None, stream=None, torch_memory=True, tuned=True, host_slab=False):
         import torch
-        if tuned and bt == 0:  # plan measured by tools/tune.py for this kind and shape, if any
+        # the plan tools/tune.py measured fastest for exactly this kind and shape (paper_1410_3060_b200/
+        # tuned.json), when the caller leaves the plan to the library (single slab, everything on auto)
+        if (tuned and variant == ST_VARIANT_AUTO and bt == 0 and tile_cfg == 0 and zchunk == 0 and nranks == 1
+                and local_slabs == 1):
             plan = tuned_plan(kind, nx, ny, nz)
             if plan:
                 bt, tile_cfg, zchunk = plan["bt"], plan["tile_cfg"], plan["zchunk"]

@@ -91,7 +91,8 @@ def pipe_footprint(kind, bt, TX, TY, CX, CY, DV, DC, WIN, CLU=1):
     # level-k extent (TX - 2R(k-1)) x (CLU*TY - 2R(k-1)): a cluster pair shrinks only at its outer rows
     work = sum((TX - 2 * R * (k - 1)) * (CLU * TY - 2 * R * (k - 1)) for k in range(1, bt + 1))
     return {"smem": smem, "tmem_cols": tmem, "threads": NCONS + 32, "out_tile": (OX, OYP),
-            "level_work": work / (bt * OX * OYP), "fits": smem <= SMEM_LIMIT and tmem <= TMEM_COLUMNS,
+            "level_work": work / (bt * OX * OYP), "level1_ratio": TX * CLU * TY / (OX * OYP),
+            "fits": smem <= SMEM_LIMIT and tmem <= TMEM_COLUMNS,
             "ring_bytes": {"state": 8 * DV * VSLOT, "coef": 8 * DC * CSLOT if NCF > 0 else 0,
                            "level_planes": 8 * NPL * 2 * TX * TY}}
 
@@ -108,6 +109,7 @@ def pipe25_footprint(TX, TY, D, CLU):
     OX, OYP = TX - 2 * R, CLU * TY - 2 * R
     work = (TX * CLU * TY + OX * OYP) / (2 * OX * OYP)  # level 1 over every CTA's rows, level 2 = output
     return {"smem": smem, "tmem_cols": 512, "threads": NCONS + 32, "out_tile": (OX, OYP), "level_work": work,
+            "level1_ratio": TX * CLU * TY / (OX * OYP),
             "fits": smem <= SMEM_LIMIT, "coef_box_bytes_per_output": 8 * NC * TX * TY * CLU / (OX * OYP),
             "ring_bytes": {"slot": 8 * SLOT, "slots": D}}
 
@@ -119,3 +121,57 @@ def l2_retention_steps(out_tile, bt, kind, ctas=148, l2_bytes=126 * 2 ** 20):
     block's compulsory bytes per cell."""
     per_step = ctas * out_tile[0] * out_tile[1] * code_balance(kind, bt) * bt
     return l2_bytes / per_step
+
+
+# ---------------------------------------------------------------------------------------------------------
+# The plan tables of the kernels (parsed from the sources, so the model and the tuner can never drift from
+# what launch_pipe / launch_pipe25v2 really instantiate) and a modeled cost per lattice update used to
+# prune the tuner's candidates (tools/tune.py).
+_CSRC = __import__("os").path.join(__import__("os").path.dirname(__import__("os").path.abspath(__file__)), "csrc")
+_KINDS = {"K7C": K7C, "K7V": K7V, "K25W": K25W, "K25V": K25V, "K25WA": K25WA}
+
+
+def pipe_plans():
+    """[(kind, bt, tile_cfg, footprint args)] of pipe.cu's launch_pipe table, tile_cfg numbered as the
+    launcher does (explicit `cfg == k` entries, the last entry of each (kind, bt) is cfg 0)."""
+    import re
+    src = open(__import__("os").path.join(_CSRC, "pipe.cu")).read()
+    body = src[src.index("cudaError_t launch_pipe("):src.index("#undef CFG")]
+    out = []
+    for line in body.splitlines():
+        m = re.search(r"(?:if \(cfg == (\d+)\) )?(CFG[UC]?)\((K\w+),\s*([-\d,\s]+)\);", line)
+        if not m:
+            continue
+        cfg = int(m.group(1)) if m.group(1) else 0
+        bt, TX, TY, CX, CY, DV, DC, WIN, _minb = (int(x) for x in m.group(4).split(","))
+        out.append((_KINDS[m.group(3)], bt, cfg, dict(TX=TX, TY=TY, CX=CX, CY=CY, DV=DV, DC=DC, WIN=WIN,
+                                                       CLU=2 if m.group(2) == "CFGC" else 1)))
+    return out
+
+
+def pipe25_plans():
+    """[(tile_cfg, TX, TY, D, CLU)] of pipe25.cu's launch_pipe25v2 table (the default entry is cfg 0)."""
+    import re
+    src = open(__import__("os").path.join(_CSRC, "pipe25.cu")).read()
+    body = src[src.index("cudaError_t launch_pipe25v2("):]
+    out = []
+    for m in re.finditer(r"(case (\d+)|default): return run_pipe25<([\d,\s]+)>", body):
+        cfg = int(m.group(2)) if m.group(2) else 0
+        out.append((cfg,) + tuple(int(x) for x in m.group(3).split(",")))
+    return out
+
+
+def modeled_nj_per_lup(kind, bt, footprint, pj_dram=91.0, pj_l2=23.0, pj_smem=5.9, nj_level=0.6):
+    """Modeled dynamic energy per lattice update of a plan (the board's 1 kW cap makes energy per update
+    the rate limit): compulsory DRAM bytes, L2->SM bytes of the overlapped boxes (each
+    level-1 cell's coefficients and state cross L2 once per block), shared-memory write + read of those
+    bytes, and per-level SM work (redundant trapezoid cells included).  Constants: the round-1 energy probe
+    (profiles/r01_energy_probe.json); nj_level fitted to the C2/C4 power measurements.  A ranking tool,
+    not a prediction to the percent."""
+    R, NC = RADIUS[kind], COEF_FIELDS[kind]
+    W = footprint["level_work"]  # level-k cells per output update, averaged over the bt levels
+    # each level-1 cell brings its coefficients and state on chip once per block
+    per_cell = 8 * (NC + (1 if kind in WAVE_KINDS else 0) + 1)
+    l2_bytes = per_cell * footprint["level1_ratio"] / bt
+    dram = code_balance(kind, bt)
+    return (pj_dram * dram + pj_l2 * l2_bytes + 2 * pj_smem * l2_bytes) / 1e3 + nj_level * W
