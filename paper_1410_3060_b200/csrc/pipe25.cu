@@ -70,6 +70,11 @@ struct P25Cfg {
   static constexpr int NRX = CLU > 1 ? 4 : 0;               // receive slots per side
   static constexpr int STASH = CLU > 1 ? 2 * 32 * NCELL * 5 : 0;  // boundary warps' carried x chain + Wy
   static constexpr int WROWS = 32 / LPR * CY;               // E1 rows per consumer warp
+  // single CTA: level 2 runs on just the output cells, (TX-2R)/2 x (TY-2R)/2 threads of 2x2 blocks in
+  // warps 1.. (a warp-aligned level-1 mapping would also compute the R-wide halo columns at level 2)
+  static constexpr bool REMAP = CLU == 1;
+  static constexpr int L2T = (TX - 2 * R) / 2 * ((TY - 2 * R) / 2);  // level-2 threads when REMAP
+  static_assert(!REMAP || (L2T % 32 == 0 && L2T / 32 + 1 <= NW && L2T / 32 <= 3), "level-2 warps 1..");
   static constexpr uint32_t TX_BYTES_A = AEL * 8, TX_BYTES_B = BEL * 8, TX_BYTES_C = CEL * 8, RX_BYTES = RXEL * 8;
   static constexpr size_t SMEM = 8 * ((size_t)D * SLOT + (size_t)NPB * PEL + 2 * (size_t)NRX * RXEL + STASH) +
                                  8 * (2 * D + 8 + 2 * NRX + 8) + 4 * 8 + 128;
@@ -286,7 +291,11 @@ __global__ void __launch_bounds__(P25Cfg<TX, TY, D, CLU>::THREADS, 1)
   // level-2 rows of this CTA (the trapezoid shrinks by R only at the cluster's outer rows)
   const int ylo = crank == 0 ? R : 0, yhi = crank == (uint32_t)CLU - 1 ? TY - R : TY;
   const int wr0 = warp * C::WROWS;  // the warp's first row (warp-uniform)
-  const bool lvl2 = wr0 + C::WROWS > ylo && wr0 < yhi;
+  const bool lvl2 = C::REMAP ? (warp >= 1 && warp <= C::L2T / 32) : (wr0 + C::WROWS > ylo && wr0 < yhi);
+  // this thread's level-2 cell block (REMAP: blocks of the output region only)
+  const int t2 = tid - 32;
+  const int l2x = C::REMAP ? R + 2 * (t2 % ((TX - 2 * R) / 2)) : x0;
+  const int l2y = C::REMAP ? R + 2 * (t2 / ((TX - 2 * R) / 2)) : ly0;
   const bool topB = CLU > 1 && warp == 0 && crank > 0;                        // needs rows of rank - 1
   const bool botB = CLU > 1 && warp == NW - 1 && crank < (uint32_t)CLU - 1;  // needs rows of rank + 1
   const bool bnd = topB || botB;
@@ -309,12 +318,19 @@ __global__ void __launch_bounds__(P25Cfg<TX, TY, D, CLU>::THREADS, 1)
 #pragma unroll
     for (int j = 0; j < CY; ++j) {
       const int ly = ly0 + j, gy = it.gy0 + ly;
-      col[j] = (long long)gy * p.pitch + it.gx0 + x0;
 #pragma unroll
       for (int i = 0; i < CX; ++i) {
-        const int lx = x0 + i, gx = it.gx0 + lx;
+        const int gx = it.gx0 + x0 + i;
         act1[j][i] = gx >= R && gx < p.nx + R && gy >= R && gy < p.ny + R;
-        outc[j][i] = act1[j][i] && lx >= R && lx < TX - R && ly >= ylo && ly < yhi;
+      }
+      // level-2 cells: stored output columns / rows of the tile, interior of the grid
+      const int ly2 = l2y + j, gy2 = it.gy0 + ly2;
+      col[j] = (long long)gy2 * p.pitch + it.gx0 + l2x;
+#pragma unroll
+      for (int i = 0; i < CX; ++i) {
+        const int lx = l2x + i, gx = it.gx0 + lx;
+        outc[j][i] = gx >= R && gx < p.nx + R && gy2 >= R && gy2 < p.ny + R && lx >= R && lx < TX - R &&
+                     ly2 >= ylo && ly2 < yhi;
       }
     }
 
@@ -419,8 +435,8 @@ __global__ void __launch_bounds__(P25Cfg<TX, TY, D, CLU>::THREADS, 1)
         if (!bnd) {
 #pragma unroll
           for (int r = 0; r < CY + 2 * R; ++r) {
-            const int row = min(max(ly0 - R + r, 0), TY - 1);  // rows outside E1 only feed discarded cells
-            lds_row<CX, true>(P + row * TX + x0, ys[r]);
+            const int row = min(max(l2y - R + r, 0), TY - 1);  // rows outside E1 only feed discarded cells
+            lds_row<CX, true>(P + row * TX + l2x, ys[r]);
           }
         } else if constexpr (CLU > 1) {
           // the y chain of plane q-1, one step late: level-1 plane q-1 and the neighbour's rows of it,
@@ -432,10 +448,10 @@ __global__ void __launch_bounds__(P25Cfg<TX, TY, D, CLU>::THREADS, 1)
           const double* rx = (topB ? rxTop : rxBot) + (size_t)k * C::RXEL;
 #pragma unroll
           for (int r = 0; r < CY + 2 * R; ++r) {
-            const int row = ly0 - R + r;
-            if (row < 0) lds_row<CX, true>(rx + (row + R) * TX + x0, ys[r]);
-            else if (row >= TY) lds_row<CX, true>(rx + (row - TY) * TX + x0, ys[r]);
-            else lds_row<CX, true>(Pp + row * TX + x0, ys[r]);
+            const int row = l2y - R + r;
+            if (row < 0) lds_row<CX, true>(rx + (row + R) * TX + l2x, ys[r]);
+            else if (row >= TY) lds_row<CX, true>(rx + (row - TY) * TX + l2x, ys[r]);
+            else lds_row<CX, true>(Pp + row * TX + l2x, ys[r]);
           }
 #pragma unroll
           for (int j = 0; j < CY; ++j)
@@ -456,6 +472,13 @@ __global__ void __launch_bounds__(P25Cfg<TX, TY, D, CLU>::THREADS, 1)
               Pprev[j][i] = __dadd_rn(sv[0], point_25v_y(m, pl, W));
             }
         }
+        // level-1 value of plane q at this thread's level-2 cells: the centre rows of the strip just loaded
+        // (boundary warps' strip holds plane q-1: they are never remapped and use their own results)
+        double vc[CY][CX];
+#pragma unroll
+        for (int j = 0; j < CY; ++j)
+#pragma unroll
+          for (int i = 0; i < CX; ++i) vc[j][i] = bnd ? v1[j][i] : ys[R + j][i];
         const int c4 = q - R;  // the plane level 2 finishes this step
         const bool store = c4 >= it.zc0 && c4 < it.zc1 && !((p.dbg & 4) && c4 == it.zc1 - 1);
 #pragma unroll
@@ -463,14 +486,14 @@ __global__ void __launch_bounds__(P25Cfg<TX, TY, D, CLU>::THREADS, 1)
           double Pq[CX];  // x/y half of plane q (boundary warps: its x chain goes to the stash)
           {
             double xr[R + CX + R];
-            lds_row<R, true>(P + (ly0 + j) * TX + x0 - R, xr);
-            lds_row<R, true>(P + (ly0 + j) * TX + x0 + CX, xr + R + CX);
+            lds_row<R, true>(P + (l2y + j) * TX + l2x - R, xr);
+            lds_row<R, true>(P + (l2y + j) * TX + l2x + CX, xr + R + CX);
 #pragma unroll
-            for (int i = 0; i < CX; ++i) xr[R + i] = v1[j][i];
+            for (int i = 0; i < CX; ++i) xr[R + i] = vc[j][i];
             double Wr[NC][CX];
 #pragma unroll
             for (int f = 0; f < NC; ++f)
-              if (f % 3 != 0 || f == 0) lds_row<CX, true>(Cs + f * C::CFIELD + (ly0 + j) * TX + x0, Wr[f]);
+              if (f % 3 != 0 || f == 0) lds_row<CX, true>(Cs + f * C::CFIELD + (l2y + j) * TX + l2x, Wr[f]);
 #pragma unroll
             for (int i = 0; i < CX; ++i) {
               double m[3][R], pl[3][R], W[NC];
@@ -485,10 +508,10 @@ __global__ void __launch_bounds__(P25Cfg<TX, TY, D, CLU>::THREADS, 1)
 #pragma unroll
               for (int f = 0; f < NC; ++f) W[f] = (f % 3 != 0 || f == 0) ? Wr[f][i] : 0.0;
               if (!bnd) {
-                Pq[i] = point_25v_xy(v1[j][i], m, pl, W);
+                Pq[i] = point_25v_xy(vc[j][i], m, pl, W);
               } else {  // carried to the next step with plane q's y coefficients
                 double* sv = myst + (j * CX + i) * 5;
-                sv[0] = point_25v_x(v1[j][i], m, pl, W);
+                sv[0] = point_25v_x(vc[j][i], m, pl, W);
 #pragma unroll
                 for (int r = 1; r <= R; ++r) sv[r] = W[3 * r - 1];
                 Pq[i] = 0.0;
@@ -497,7 +520,7 @@ __global__ void __launch_bounds__(P25Cfg<TX, TY, D, CLU>::THREADS, 1)
           }
           double Wz[4][CX];  // z coefficients of plane q, carried for its chain
 #pragma unroll
-          for (int r = 1; r <= 4; ++r) lds_row<CX, true>(Cs + 3 * r * C::CFIELD + (ly0 + j) * TX + x0, Wz[r - 1]);
+          for (int r = 1; r <= 4; ++r) lds_row<CX, true>(Cs + 3 * r * C::CFIELD + (l2y + j) * TX + l2x, Wz[r - 1]);
           double vout[CX];
 #pragma unroll
           for (int i = 0; i < CX; ++i) {
@@ -506,7 +529,7 @@ __global__ void __launch_bounds__(P25Cfg<TX, TY, D, CLU>::THREADS, 1)
             tmem_ld32(tq + kColS1 + (uint32_t)cell * 32, st);
             tmem_ld8(tq + colR + (uint32_t)cell * 8, rv);
             tmem_wait_ld();
-            const double v = v1[j][i];
+            const double v = vc[j][i];
             double vr[4];  // V1(q-2), V1(q-4), V1(q-6), V1(q-8)
 #pragma unroll
             for (int k = 0; k < 4; ++k) vr[k] = dbl(rv[2 * k], rv[2 * k + 1]);

@@ -285,7 +285,7 @@ constexpr double kCoopAutoCells = 3.0e6;
 int default_bt(int kind) {
   switch (kind) {
     case ST_7PT_CONST: return 4;  // tools/sweep.py on B200
-    case ST_7PT_VAR: return 3;  // TMEM coefficient window (session 2): 188 vs 154 GLUP/s at bt = 2
+    case ST_7PT_VAR: return 4;  // tools/tune.py (round 2, sustained): 196.1 vs 190.1 GLUP/s at bt = 3
     case ST_25PT_VAR: return 2;  // pipe25.cu (round 2): C4 57.8 vs 52.8 GLUP/s at bt = 1, same box
     default: return 1;
   }
