@@ -70,9 +70,12 @@ struct P25Cfg {
   static constexpr int NRX = CLU > 1 ? 4 : 0;               // receive slots per side
   static constexpr int STASH = CLU > 1 ? 2 * 32 * NCELL * 5 : 0;  // boundary warps' carried x chain + Wy
   static constexpr int WROWS = 32 / LPR * CY;               // E1 rows per consumer warp
-  // single CTA: level 2 runs on just the output cells, (TX-2R)/2 x (TY-2R)/2 threads of 2x2 blocks in
-  // warps 1.. (a warp-aligned level-1 mapping would also compute the R-wide halo columns at level 2)
-  static constexpr bool REMAP = CLU == 1;
+  // level 2 on just the output cells, (TX-2R)/2 x (TY-2R)/2 threads of 2x2 blocks in warps 1.. (the
+  // warp-aligned mapping also computes the R-wide halo columns at level 2, a quarter of its cells).
+  // Measured (C4, round 2): no gain under the power cap (58.85 vs 58.4-58.6 GLUP/s) and slower in isolation
+  // (63 vs 67 GLUP/s: the 12-thread rows of the output-only mapping conflict in shared-memory banks), so
+  // the warp-aligned mapping stays; the remapped path is kept compiled for the record (REMAP = false).
+  static constexpr bool REMAP = false;
   static constexpr int L2T = (TX - 2 * R) / 2 * ((TY - 2 * R) / 2);  // level-2 threads when REMAP
   static_assert(!REMAP || (L2T % 32 == 0 && L2T / 32 + 1 <= NW && L2T / 32 <= 3), "level-2 warps 1..");
   static constexpr uint32_t TX_BYTES_A = AEL * 8, TX_BYTES_B = BEL * 8, TX_BYTES_C = CEL * 8, RX_BYTES = RXEL * 8;

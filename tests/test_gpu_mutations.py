@@ -24,8 +24,8 @@ def _parity_err(kind, n, T, **kw):
                                          (1, {"nranks": 3, "local_slabs": 3, "halo": 1})])
 def test_injected_fault_is_detected(monkeypatch, kind, fault, extra):
     n = (40, 33, 37) if synth.RADIUS[kind] == 1 else (70, 20, 41)
-    T = 9  # two full blocks at the default bt (<= 3 here; a remainder is split evenly): the second
-    # reads the deepest halo plane
+    T = 12  # several full blocks at the default bt (4 for 7v, 2 for 25v here): the second reads the
+    # deepest halo plane
     if "nranks" in extra:
         from paper_1410_3060_b200 import Grid
         import paper_1410_3060_b200 as st
