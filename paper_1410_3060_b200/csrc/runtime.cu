@@ -183,7 +183,7 @@ struct stencil_ctx {
   cudaStream_t comm_stream = nullptr;
   cudaEvent_t ev_edge = nullptr, ev_halo = nullptr;
   bool halo_pending = false;
-  bool overlap = true;  // STENCIL_NO_OVERLAP=1: bulk-synchronous schedule (one launch, then exchange)
+  bool overlap = false;  // STENCIL_OVERLAP=1: halo-first schedule (edge kernels, exchange, interior kernel)
 
   // ST_HALO_PEER (fused halo exchange)
   int halo = ST_HALO_COPY;
@@ -471,8 +471,13 @@ int create_common(stencil_ctx** out, int kind, int64_t nx, int64_t ny, int64_t n
     CK(cudaStreamCreateWithFlags(&h->comm_stream, cudaStreamNonBlocking), "comm stream");
     CK(cudaEventCreateWithFlags(&h->ev_edge, cudaEventDisableTiming), "event");
     CK(cudaEventCreateWithFlags(&h->ev_halo, cudaEventDisableTiming), "event");
-    const char* no = getenv("STENCIL_NO_OVERLAP");
-    h->overlap = !(no && atoi(no));
+    // Bulk-synchronous by default (one launch per slab and block, then the exchange): the halo-first
+    // overlap's edge kernels stream R*bt-plane slabs through a z-stream that needs 2*R*bt fill/drain planes,
+    // ~3x their output, which costs more than the exchange it hides over NVLink (C5 at bt = 2, 256-plane
+    // slabs: ~12 % edge overhead vs a 0.2 ms exchange per 9 ms block).  STENCIL_OVERLAP=1
+    // selects the halo-first schedule.
+    const char* ov = getenv("STENCIL_OVERLAP");
+    h->overlap = ov && atoi(ov);
   }
   if (use_nccl) {
     Nccl* n = nccl();

@@ -100,10 +100,11 @@ def test_weak_shape_medium():
 
 @pytest.mark.parametrize("kind,n,T", CASES)
 def test_overlap_schedule_equals_bulk_synchronous(kind, n, T, monkeypatch):
-    """Halo-first schedule (edge kernels, exchange on a comm stream, interior kernel) == one launch per
-    slab followed by the exchange (STENCIL_NO_OVERLAP=1), bitwise."""
+    """Halo-first schedule (edge kernels, exchange on a comm stream, interior kernel; STENCIL_OVERLAP=1) ==
+    one launch per slab followed by the exchange (the default), bitwise."""
+    monkeypatch.setenv("STENCIL_OVERLAP", "1")
     a = run(kind, n, T, nranks=3, local_slabs=3)
-    monkeypatch.setenv("STENCIL_NO_OVERLAP", "1")
+    monkeypatch.delenv("STENCIL_OVERLAP")
     b = run(kind, n, T, nranks=3, local_slabs=3)
     assert np.array_equal(a[0], b[0])
     assert a[2]["launches"] > b[2]["launches"]  # the split schedule launches edge + interior kernels
