@@ -19,7 +19,7 @@ from ._binding import (  # noqa: F401
     stencil_kernel_time, stencil_destroy, stencil_last_error, stencil_nccl_unique_id,
     stencil_plan_slab, stencil_version, stencil_peer_export, stencil_peer_import, stencil_peer_handshake, stencil_generate, peer_neighbours,
     exchange_peer_descriptors, wire_peer_halos,
-    Grid, RADIUS,
+    Grid, RADIUS, tuned_plan,
 )
 
 __version__ = "0.1.0"

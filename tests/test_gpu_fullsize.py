@@ -112,18 +112,22 @@ def test_C5_full_size_sampled_and_bitwise():
 
 
 def test_C2_full_size_every_plan_bitwise():
-    """C2 at its full 512^3 size: the default plan (bt = 3, TMEM window), bt = 2, bt = 4 and the NEXT-3
-    cluster-pair tiles (tile_cfg 9 at bt = 3, 4 at bt = 4) all give the naive sweeps' bits on every
+    """C2 at its full 512^3 size: the default (tuned.json) plan (bt = 4, TMEM window), bt = 2, bt = 3 and the
+    NEXT-3 cluster-pair tiles (tile_cfg 9 at bt = 3, 4 at bt = 4) all give the naive sweeps' bits on every
     plane, T = 12 (whole blocks of 2, 3 and 4, and a remainder-free run for each)."""
     w = workloads.C2
     T = 12
     full = []
+    tuned = st.tuned_plan(w.kind, w.nx, w.ny, w.nz)  # Grid() applies tools/tune.py's plan by default
+    assert tuned is not None
     for kw in (dict(variant=st.ST_VARIANT_NAIVE), dict(), dict(variant=st.ST_VARIANT_PIPE, bt=2),
-               dict(variant=st.ST_VARIANT_PIPE, bt=4), dict(variant=st.ST_VARIANT_PIPE, bt=3, tile_cfg=9),
+               dict(variant=st.ST_VARIANT_PIPE, bt=3), dict(variant=st.ST_VARIANT_PIPE, bt=3, tile_cfg=9),
                dict(variant=st.ST_VARIANT_PIPE, bt=4, tile_cfg=4)):
         with st.Grid(w.kind, w.nx, w.ny, w.nz, seed=synth.DEFAULT_SEED, **kw) as g:
             g.run(T)
             full.append(g.read(0))
+            if not kw:
+                assert g.info()["bt"] == tuned["bt"]
     for i, a in enumerate(full[1:]):
         assert np.array_equal(a, full[0]), i
 
