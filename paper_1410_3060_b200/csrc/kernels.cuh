@@ -91,6 +91,9 @@ int max_pipe_bt(int kind);
 // launch_pipe for (K25V, b = 2); cfg selects a tile configuration (0 = default).
 cudaError_t launch_pipe25v2(const KParams& p, int zchunk_req, int num_sms, int cfg, cudaStream_t stream,
                             LaunchInfo* info);
+// The 25-point wave with two fused levels (pipe25.cu): contract of launch_pipe for (K25W, b = 2).
+cudaError_t launch_pipe25w2(const KParams& p, int zchunk_req, int num_sms, int cfg, cudaStream_t stream,
+                            LaunchInfo* info);
 
 // Tensor map (cuTensorMapEncodeTiled) of fp64 padded arrays in the library's layout: rank 3 (x, y, z)
 // or 4 (x, y, z, field); box bx x by x 1 (x bf).  The map covers columns [0, X) from `base` (the row

@@ -915,8 +915,11 @@ cudaError_t launch_pipe(int kind, int b, const KParams& p, int zchunk_req, int n
         CFGU(K25W, 1, 64, 14, 2, 2, 8, 8, 0, 1);  // merged V/U rings; C3: 165-169 (round 1) -> 185-196 GLUP/s
       }
       if (b == 2) {  // the leapfrog with two fused levels: both time levels in, both out (32 B/cell)
+        // round 2: the two-level kernel of pipe25.cu (TMEM z-rings, 24 x 24 tiles) by default; the
+        // round-1 generic kernel (register rings, 24 x 16 tiles) as tile_cfg 1 / 2
         if (cfg == 1) CFGU(K25W, 2, 32, 24, 2, 2, 7, 3, 0, 1);
-        CFG(K25W, 2, 32, 24, 2, 2, 7, 3, 0, 1);
+        if (cfg == 2) CFG(K25W, 2, 32, 24, 2, 2, 7, 3, 0, 1);
+        return launch_pipe25w2(p, zchunk_req, num_sms, 0, stream, info);
       }
       break;
     case K25WA:

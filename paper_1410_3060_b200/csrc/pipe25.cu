@@ -51,9 +51,13 @@
 
 namespace st {
 
-template <int TX, int TY, int D, int CLU>
+template <int KIND, int TX, int TY, int D, int CLU>
 struct P25Cfg {
-  static constexpr int R = 4, NC = 13, CX = 2, CY = 2, NCELL = CX * CY;
+  // KIND = K25V (Fig. 1d, 13 coefficient fields) or K25W (Fig. 1e with a scalar alpha: box C carries
+  // Omega^{t-1} instead of coefficients, and the carried state has no z-coefficients)
+  static constexpr bool WAVE = KIND == K25W;
+  static constexpr int R = 4, NC = WAVE ? 0 : 13, CX = 2, CY = 2, NCELL = CX * CY;
+  static constexpr int CF = WAVE ? 1 : NC;  // fields of box C
   static constexpr int LPR = TX / CX;             // threads per block row
   static constexpr int NCONS = LPR * (TY / CY);   // consumer threads
   static constexpr int NW = NCONS / 32;           // consumer warps
@@ -61,7 +65,7 @@ struct P25Cfg {
   static constexpr int OX = TX - 2 * R;           // output columns of a tile
   static constexpr int OYP = CLU * TY - 2 * R;    // output rows of a (cluster) tile
   static constexpr int FX = TX + 2 * R, FY = TY + 2 * R;  // box B (level-1 footprint)
-  static constexpr int AEL = TX * TY, BEL = FX * FY, CFIELD = TX * TY, CEL = NC * CFIELD;
+  static constexpr int AEL = TX * TY, BEL = FX * FY, CFIELD = TX * TY, CEL = CF * CFIELD;
   static constexpr int BOFF = (AEL + 15) / 16 * 16, COFF = BOFF + (BEL + 15) / 16 * 16;
   static constexpr int SLOT = COFF + (CEL + 15) / 16 * 16;  // doubles per ring slot (128-byte aligned parts)
   static constexpr int PEL = TX * TY;                       // one shared level-1 plane
@@ -85,6 +89,8 @@ struct P25Cfg {
   static_assert(TY % WROWS == 0 && WROWS == R, "one warp = R rows (the pushed strip)");
   static_assert(OX > 0 && TY > 2 * R && (OX & 3) == 0, "output tile (whole 32-byte sectors per row)");
   static_assert(CLU == 1 || CLU == 2 || CLU == 4, "clusters of 1, 2 or 4 CTAs along y");
+  static_assert(!WAVE || CLU == 1, "wave: single-CTA tiles");
+  static_assert(KIND == K25V || KIND == K25W, "25-point kinds");
   // TMEM (512 columns x 128 lanes; warp w reaches lanes 32*(w%4)..): warp w uses columns
   // [256*(w/4), +256): at most two warps per lane quadrant.
   static_assert(NW <= 8, "TMEM quadrants");
@@ -152,12 +158,13 @@ __device__ __forceinline__ void v0ring_st(uint32_t t, const uint32_t (&w)[28]) {
   }
 }
 
-template <int TX, int TY, int D, int CLU>
-__global__ void __launch_bounds__(P25Cfg<TX, TY, D, CLU>::THREADS, 1)
+template <int KIND, int TX, int TY, int D, int CLU>
+__global__ void __launch_bounds__(P25Cfg<KIND, TX, TY, D, CLU>::THREADS, 1)
     pipe25_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                   const __grid_constant__ CUtensorMap mapC, const KParams p, int ntx, int nty, int items) {
-  using C = P25Cfg<TX, TY, D, CLU>;
+  using C = P25Cfg<KIND, TX, TY, D, CLU>;
   constexpr int R = C::R, NC = C::NC, NCONS = C::NCONS, FX = C::FX, CX = C::CX, CY = C::CY, NW = C::NW;
+  constexpr bool WAVE = C::WAVE;
 
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double* ring = reinterpret_cast<double*>(smem_raw);
@@ -255,10 +262,16 @@ __global__ void __launch_bounds__(P25Cfg<TX, TY, D, CLU>::THREADS, 1)
           double* slot = ring + (size_t)sl * C::SLOT;
           tma_load_3d(slot, &mapA, &full[sl], xa, it.gy0, s);
           if (needB) tma_load_3d(slot + C::BOFF, &mapB, &full[sl], xb, it.gy0 - R, q);
-          if (need1) tma_load_4d(slot + C::COFF, &mapC, &full[sl], xa, it.gy0, q, 0);
+          if (need1) {
+            if constexpr (WAVE) tma_load_3d(slot + C::COFF, &mapC, &full[sl], xa, it.gy0, q);  // Omega^{t-1}
+            else tma_load_4d(slot + C::COFF, &mapC, &full[sl], xa, it.gy0, q, 0);
+          }
           if (p.pfd > 0 && s + p.pfd <= it.s_end) {  // warm L2 for the loads pfd steps ahead (beyond the ring)
             tma_prefetch_3d(&mapA, xa, it.gy0, s + p.pfd);
-            if (q + p.pfd >= 0) tma_prefetch_4d(&mapC, xa, it.gy0, q + p.pfd, 0);
+            if (q + p.pfd >= 0) {
+              if constexpr (WAVE) tma_prefetch_3d(&mapC, xa, it.gy0, q + p.pfd);
+              else tma_prefetch_4d(&mapC, xa, it.gy0, q + p.pfd, 0);
+            }
           }
         }
         if (CLU == 1 && p.lockstep) {
@@ -304,6 +317,7 @@ __global__ void __launch_bounds__(P25Cfg<TX, TY, D, CLU>::THREADS, 1)
   const bool bnd = topB || botB;
   const uint32_t tq = tmem_base + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)((warp >> 2) * 256);
   double* myst = stash + (size_t)((topB ? 0 : 1) * 32 + lane) * C::NCELL * 5;  // boundary warps only
+  const double ps[6] = {p.s[0], p.s[1], p.s[2], p.s[3], p.s[4], p.s[5]};  // the wave's w0, w1..w4, alpha
   uint32_t iv = 0;
 
   for (uint32_t n = 0;; ++n) {
@@ -348,6 +362,7 @@ __global__ void __launch_bounds__(P25Cfg<TX, TY, D, CLU>::THREADS, 1)
       const double* Bb = slot + C::BOFF + R * FX + R;  // Bb[y * FX + x] = E1 cell (x, y) of plane q
       const double* Cs = slot + C::COFF;               // Cs[f * CFIELD + y * TX + x]: field f at E1 (x, y)
       double v1[CY][CX];
+      double v0c4[CY][CX];  // the wave: level 0 of plane q - R, the Omega^t of level 2's output plane
       {
         double ys[CY + 2 * R][CX];
 #pragma unroll
@@ -365,9 +380,11 @@ __global__ void __launch_bounds__(P25Cfg<TX, TY, D, CLU>::THREADS, 1)
           lds_row<R, true>(Bb + (ly0 + j) * FX + x0 + CX, xr + R + CX);
 #pragma unroll
           for (int i = 0; i < CX; ++i) xr[R + i] = ys[R + j][i];
-          double Wr[NC][CX];
+          double Wr[NC > 0 ? NC : 1][CX];
 #pragma unroll
           for (int f = 0; f < NC; ++f) lds_row<CX, true>(Cs + f * C::CFIELD + (ly0 + j) * TX + x0, Wr[f]);
+          double urow[CX];  // the wave: Omega^{t-1} of plane q (box C)
+          if constexpr (WAVE) lds_row<CX, true>(Cs + (ly0 + j) * TX + x0, urow);
           auto V0 = [&](int k, int i) -> double {  // plane s - 8 + k of cell (j, i)
             if (k == 8) return vnew[i];
             if (k == R) return ys[R + j][i];
@@ -377,7 +394,7 @@ __global__ void __launch_bounds__(P25Cfg<TX, TY, D, CLU>::THREADS, 1)
           uint32_t zn[28];
 #pragma unroll
           for (int i = 0; i < CX; ++i) {
-            double m[3][R], pl[3][R], W[NC];
+            double m[3][R], pl[3][R], W[NC > 0 ? NC : 1];
 #pragma unroll
             for (int r = 1; r <= R; ++r) {
               m[0][r - 1] = xr[R + i - r];
@@ -390,7 +407,13 @@ __global__ void __launch_bounds__(P25Cfg<TX, TY, D, CLU>::THREADS, 1)
 #pragma unroll
             for (int f = 0; f < NC; ++f) W[f] = Wr[f][i];
             const double c = V0(R, i);
-            const double v = point_25v(c, m, pl, W);
+            double v;
+            if constexpr (WAVE) {
+              v = point_25w(c, urow[i], m, pl, ps, ps[5]);
+              v0c4[j][i] = V0(0, i);
+            } else {
+              v = point_25v(c, m, pl, W);
+            }
             // ghosts, cells outside the grid and planes not computed at level 1 keep their input value
             v1[j][i] = (zv1 && act1[j][i]) ? v : c;
             // the ring moves on a plane: next step's entries are this step's k = 1..3, 4 (box B), 6, 7, 8
@@ -432,7 +455,7 @@ __global__ void __launch_bounds__(P25Cfg<TX, TY, D, CLU>::THREADS, 1)
       if (lvl2) {
         const uint32_t colR = kColV1 + (uint32_t)(q & 1) * 32;  // level-1 z-ring of q's parity, per cell:
         uint32_t s2[8], s2n[8];                                  // V1(q-2), V1(q-4), V1(q-6), V1(q-8)
-        tmem_ld8(tq + kColS2, s2);  // Z(q-2) of the 4 cells
+        if constexpr (!WAVE) tmem_ld8(tq + kColS2, s2);  // Z(q-2) of the 4 cells
         double ys[CY + 2 * R][CX];
         double Pprev[CY][CX];  // boundary warps: P(q-1), completed this step
         if (!bnd) {
@@ -461,7 +484,7 @@ __global__ void __launch_bounds__(P25Cfg<TX, TY, D, CLU>::THREADS, 1)
 #pragma unroll
             for (int i = 0; i < CX; ++i) {
               const double* sv = myst + (j * CX + i) * 5;  // x chain and Wy_1..4 of plane q-1
-              double m[3][R], pl[3][R], W[NC];
+              double m[3][R], pl[3][R], W[NC > 0 ? NC : 1];
 #pragma unroll
               for (int r = 1; r <= R; ++r) {
                 m[1][r - 1] = ys[R + j - r][i];
@@ -493,13 +516,13 @@ __global__ void __launch_bounds__(P25Cfg<TX, TY, D, CLU>::THREADS, 1)
             lds_row<R, true>(P + (l2y + j) * TX + l2x + CX, xr + R + CX);
 #pragma unroll
             for (int i = 0; i < CX; ++i) xr[R + i] = vc[j][i];
-            double Wr[NC][CX];
+            double Wr[NC > 0 ? NC : 1][CX];
 #pragma unroll
             for (int f = 0; f < NC; ++f)
               if (f % 3 != 0 || f == 0) lds_row<CX, true>(Cs + f * C::CFIELD + (l2y + j) * TX + l2x, Wr[f]);
 #pragma unroll
             for (int i = 0; i < CX; ++i) {
-              double m[3][R], pl[3][R], W[NC];
+              double m[3][R], pl[3][R], W[NC > 0 ? NC : 1];
 #pragma unroll
               for (int r = 1; r <= R; ++r) {
                 m[0][r - 1] = xr[R + i - r];
@@ -510,61 +533,96 @@ __global__ void __launch_bounds__(P25Cfg<TX, TY, D, CLU>::THREADS, 1)
               }
 #pragma unroll
               for (int f = 0; f < NC; ++f) W[f] = (f % 3 != 0 || f == 0) ? Wr[f][i] : 0.0;
-              if (!bnd) {
-                Pq[i] = point_25v_xy(vc[j][i], m, pl, W);
-              } else {  // carried to the next step with plane q's y coefficients
-                double* sv = myst + (j * CX + i) * 5;
-                sv[0] = point_25v_x(vc[j][i], m, pl, W);
+              if constexpr (WAVE) {
+                Pq[i] = point_25w_xy(vc[j][i], m, pl, ps);
+              } else {
+                if (!bnd) {
+                  Pq[i] = point_25v_xy(vc[j][i], m, pl, W);
+                } else {  // carried to the next step with plane q's y coefficients
+                  double* sv = myst + (j * CX + i) * 5;
+                  sv[0] = point_25v_x(vc[j][i], m, pl, W);
 #pragma unroll
-                for (int r = 1; r <= R; ++r) sv[r] = W[3 * r - 1];
-                Pq[i] = 0.0;
+                  for (int r = 1; r <= R; ++r) sv[r] = W[3 * r - 1];
+                  Pq[i] = 0.0;
+                }
               }
             }
           }
           double Wz[4][CX];  // z coefficients of plane q, carried for its chain
+          if constexpr (!WAVE) {
 #pragma unroll
-          for (int r = 1; r <= 4; ++r) lds_row<CX, true>(Cs + 3 * r * C::CFIELD + (l2y + j) * TX + l2x, Wz[r - 1]);
-          double vout[CX];
+            for (int r = 1; r <= 4; ++r) lds_row<CX, true>(Cs + 3 * r * C::CFIELD + (l2y + j) * TX + l2x, Wz[r - 1]);
+          }
+          double vout[CX], uout[CX];
 #pragma unroll
           for (int i = 0; i < CX; ++i) {
             const int cell = j * CX + i;
-            uint32_t st[32], rv[8];
-            tmem_ld32(tq + kColS1 + (uint32_t)cell * 32, st);
+            uint32_t rv[8];
             tmem_ld8(tq + colR + (uint32_t)cell * 8, rv);
-            tmem_wait_ld();
             const double v = vc[j][i];
             double vr[4];  // V1(q-2), V1(q-4), V1(q-6), V1(q-8)
+            if constexpr (WAVE) {
+              // carried state (8 doubles): P(q-4..q-1) [0..3], Z(q-4) [4], Z(q-3) [5], Z(q-2) [6]
+              uint32_t st[16];
+              tmem_ld16(tq + kColS1 + (uint32_t)cell * 16, st);
+              tmem_wait_ld();
 #pragma unroll
-            for (int k = 0; k < 4; ++k) vr[k] = dbl(rv[2 * k], rv[2 * k + 1]);
-            // carried state S1 (16 doubles): P(q-4..q-1) [0..3], Z(q-4) [4], Z(q-3) [5], the z coefficients
-            // still pending: plane q-4 {r4} [6], q-3 {r3, r4} [7, 8], q-2 {r2, r3, r4} [9..11],
-            // q-1 {r1..r4} [12..15];  S2: Z(q-2)
-            double S[16];
+              for (int k = 0; k < 4; ++k) vr[k] = dbl(rv[2 * k], rv[2 * k + 1]);
+              double S[8];
 #pragma unroll
-            for (int k = 0; k < 16; ++k) S[k] = dbl(st[2 * k], st[2 * k + 1]);
-            const double z2 = dbl(s2[2 * cell], s2[2 * cell + 1]);
-            const double z4 = point_25v_zterm(4, S[4], S[6], vr[3], v);   // plane q-4: last term
-            const double z3 = point_25v_zterm(3, S[5], S[7], vr[2], v);   // plane q-3
-            const double z2n = point_25v_zterm(2, z2, S[9], vr[1], v);    // plane q-2
-            const double z1 = point_25v_zterm(1, 0.0, S[12], vr[0], v);   // plane q-1: first term
-            vout[i] = __dadd_rn(S[0], z4);  // point_25v: (x/y half) + z chain
-            // boundary warps complete P(q-1) only now (its slot held a placeholder)
-            const double Pq1 = bnd ? Pprev[j][i] : S[3];
-            const double N[16] = {S[1], S[2], Pq1, Pq[i], z3, z2n, S[8], S[10], S[11], S[13], S[14], S[15],
-                                  Wz[0][i], Wz[1][i], Wz[2][i], Wz[3][i]};
+              for (int k = 0; k < 8; ++k) S[k] = dbl(st[2 * k], st[2 * k + 1]);
+              const double z4 = point_25w_zterm(4, S[4], ps[4], vr[3], v);  // plane q-4: last term
+              const double z3 = point_25w_zterm(3, S[5], ps[3], vr[2], v);
+              const double z2n = point_25w_zterm(2, S[6], ps[2], vr[1], v);
+              const double z1 = point_25w_zterm(1, 0.0, ps[1], vr[0], v);
+              // plane q-4 = c4: Omega^{t+2} = 2 Omega^{t+1} - Omega^t + alpha L(Omega^{t+1}); the new
+              // "previous level" is Omega^{t+1}(c4) = V1(q-4)
+              vout[i] = point_25w_final(vr[1], v0c4[j][i], S[0], z4, ps[5]);
+              uout[i] = vr[1];
+              const double N[8] = {S[1], S[2], S[3], Pq[i], z3, z2n, z1, 0.0};
 #pragma unroll
-            for (int k = 0; k < 16; ++k) put(st + 2 * k, N[k]);
-            tmem_st32(tq + kColS1 + (uint32_t)cell * 32, st);
-            put(s2n + 2 * cell, z1);
+              for (int k = 0; k < 8; ++k) put(st + 2 * k, N[k]);
+              tmem_st16(tq + kColS1 + (uint32_t)cell * 16, st);
+            } else {
+              uint32_t st[32];
+              tmem_ld32(tq + kColS1 + (uint32_t)cell * 32, st);
+              tmem_wait_ld();
+#pragma unroll
+              for (int k = 0; k < 4; ++k) vr[k] = dbl(rv[2 * k], rv[2 * k + 1]);
+              // carried state S1 (16 doubles): P(q-4..q-1) [0..3], Z(q-4) [4], Z(q-3) [5], the z coefficients
+              // still pending: plane q-4 {r4} [6], q-3 {r3, r4} [7, 8], q-2 {r2, r3, r4} [9..11],
+              // q-1 {r1..r4} [12..15];  S2: Z(q-2)
+              double S[16];
+#pragma unroll
+              for (int k = 0; k < 16; ++k) S[k] = dbl(st[2 * k], st[2 * k + 1]);
+              const double z2 = dbl(s2[2 * cell], s2[2 * cell + 1]);
+              const double z4 = point_25v_zterm(4, S[4], S[6], vr[3], v);   // plane q-4: last term
+              const double z3 = point_25v_zterm(3, S[5], S[7], vr[2], v);   // plane q-3
+              const double z2n = point_25v_zterm(2, z2, S[9], vr[1], v);    // plane q-2
+              const double z1 = point_25v_zterm(1, 0.0, S[12], vr[0], v);   // plane q-1: first term
+              vout[i] = __dadd_rn(S[0], z4);  // point_25v: (x/y half) + z chain
+              uout[i] = 0.0;
+              // boundary warps complete P(q-1) only now (its slot held a placeholder)
+              const double Pq1 = bnd ? Pprev[j][i] : S[3];
+              const double N[16] = {S[1], S[2], Pq1, Pq[i], z3, z2n, S[8], S[10], S[11], S[13], S[14], S[15],
+                                    Wz[0][i], Wz[1][i], Wz[2][i], Wz[3][i]};
+#pragma unroll
+              for (int k = 0; k < 16; ++k) put(st + 2 * k, N[k]);
+              tmem_st32(tq + kColS1 + (uint32_t)cell * 32, st);
+              put(s2n + 2 * cell, z1);
+            }
             // the ring of q's parity moves on: V1(q), V1(q-2), V1(q-4), V1(q-6)
             put(rv, v);
 #pragma unroll
             for (int k = 1; k < 4; ++k) put(rv + 2 * k, vr[k - 1]);
             tmem_st8(tq + colR + (uint32_t)cell * 8, rv);
           }
-          if (store) stg_row<CX, true>(p.dst + (long long)c4 * p.plane + col[j], vout, outc[j]);
+          if (store) {
+            stg_row<CX, true>(p.dst + (long long)c4 * p.plane + col[j], vout, outc[j]);
+            if constexpr (WAVE) stg_row<CX, true>(p.dstu + (long long)c4 * p.plane + col[j], uout, outc[j]);
+          }
         }
-        tmem_st8(tq + kColS2, s2n);
+        if constexpr (!WAVE) tmem_st8(tq + kColS2, s2n);
       }
       tmem_wait_st();  // this step's TMEM stores land before the next step's loads
       __syncwarp();
@@ -586,10 +644,15 @@ __global__ void __launch_bounds__(P25Cfg<TX, TY, D, CLU>::THREADS, 1)
             const long long o = (long long)c * p.plane + col[j];
             if (outc[j][0] && outc[j][1]) {
               *reinterpret_cast<double2*>(p.rdst[qd] + o) = __ldcg(reinterpret_cast<const double2*>(p.dst + o));
+              if constexpr (WAVE)  // the wave's second new level (Omega^{t+1})
+                *reinterpret_cast<double2*>(p.rdstu[qd] + o) = __ldcg(reinterpret_cast<const double2*>(p.dstu + o));
             } else {
 #pragma unroll
               for (int i = 0; i < CX; ++i)
-                if (outc[j][i]) p.rdst[qd][o + i] = __ldcg(p.dst + o + i);
+                if (outc[j][i]) {
+                  p.rdst[qd][o + i] = __ldcg(p.dst + o + i);
+                  if constexpr (WAVE) p.rdstu[qd][o + i] = __ldcg(p.dstu + o + i);
+                }
             }
           }
         }
@@ -609,10 +672,10 @@ __global__ void __launch_bounds__(P25Cfg<TX, TY, D, CLU>::THREADS, 1)
 
 namespace {
 
-template <int TX, int TY, int D, int CLU>
+template <int KIND, int TX, int TY, int D, int CLU>
 cudaError_t run_pipe25(const KParams& p0, int zchunk_req, int num_sms, cudaStream_t stream, LaunchInfo* info) {
-  using C = P25Cfg<TX, TY, D, CLU>;
-  auto kern = pipe25_kernel<TX, TY, D, CLU>;
+  using C = P25Cfg<KIND, TX, TY, D, CLU>;
+  auto kern = pipe25_kernel<KIND, TX, TY, D, CLU>;
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
@@ -667,7 +730,9 @@ cudaError_t run_pipe25(const KParams& p0, int zchunk_req, int num_sms, cudaStrea
   const long long MX = p.xoff + p.nx + 2 * C::R - X0, MY = p.ny + 2 * C::R;
   if (!make_tensor_map(&mapA, p.src_raw + X0, 3, p.pitch, MX, MY, p.zl, 1, p.plane, 0, TX, TY, 1) ||
       !make_tensor_map(&mapB, p.src_raw + X0, 3, p.pitch, MX, MY, p.zl, 1, p.plane, 0, C::FX, C::FY, 1) ||
-      !make_tensor_map(&mapC, p.coef_raw + X0, 4, p.pitch, MX, MY, p.zl, C::NC, p.plane, p.cstride, TX, TY, C::NC))
+      !(C::WAVE ? make_tensor_map(&mapC, p.srcu_raw + X0, 3, p.pitch, MX, MY, p.zl, 1, p.plane, 0, TX, TY, 1)
+                : make_tensor_map(&mapC, p.coef_raw + X0, 4, p.pitch, MX, MY, p.zl, C::NC, p.plane, p.cstride, TX, TY,
+                                  C::NC)))
     return cudaErrorInvalidValue;
   const int grid = (int)std::min<long long>(items, clusters) * CLU;
   static const int pfd_env = getenv("STENCIL_PF") ? atoi(getenv("STENCIL_PF")) : 0;
@@ -706,9 +771,19 @@ cudaError_t launch_pipe25v2(const KParams& p, int zchunk_req, int num_sms, int c
   // Measured on B200 (C4, sustained, profiles/r02_summary.md): the single-CTA tile is the fastest; the
   // cluster tiles move 15 % fewer L2->SM bytes but stall on their boundary warps (ncu: barrier stalls).
   switch (cfg) {
-    case 1: return run_pipe25<32, 20, 2, 2>(p, zchunk_req, num_sms, stream, info);   // cluster pair: 24 x 32
-    case 2: return run_pipe25<32, 20, 2, 4>(p, zchunk_req, num_sms, stream, info);   // cluster of 4: 24 x 72
-    default: return run_pipe25<32, 24, 2, 1>(p, zchunk_req, num_sms, stream, info);  // single CTA: 24 x 16
+    case 1: return run_pipe25<K25V, 32, 20, 2, 2>(p, zchunk_req, num_sms, stream, info);   // cluster pair: 24 x 32
+    case 2: return run_pipe25<K25V, 32, 20, 2, 4>(p, zchunk_req, num_sms, stream, info);   // cluster of 4: 24 x 72
+    default: return run_pipe25<K25V, 32, 24, 2, 1>(p, zchunk_req, num_sms, stream, info);  // single CTA: 24 x 16
+  }
+}
+
+// The 25-point wave (Fig. 1e, scalar alpha) with two fused levels: no coefficient fields, so a bigger
+// tile (32 x 32 -> 24 x 24 output) and a 4-slot ring fit; both new levels are stored (Omega^{t+2} and
+// Omega^{t+1}: 32 B per cell per block).
+cudaError_t launch_pipe25w2(const KParams& p, int zchunk_req, int num_sms, int cfg, cudaStream_t stream,
+                            LaunchInfo* info) {
+  switch (cfg) {
+    default: return run_pipe25<K25W, 32, 32, 4, 1>(p, zchunk_req, num_sms, stream, info);  // 24 x 24
   }
 }
 

@@ -84,17 +84,33 @@ __device__ __forceinline__ double point_25v(double c, const double (&m)[3][4], c
 
 // Fig. 1e: 2*O^t - O^{t-1} + alpha*[w0*O^t + sum_r w_r*(x+y+z pairs_r)].
 // s = {w0, w1, w2, w3, w4, *}; alpha = the scalar s[5] (kind 3) or the field value at the point
-// (kind 5); u = O^{t-1} at the point.
-__device__ __forceinline__ double point_25w(double c, double u, const double (&m)[3][4],
-                                            const double (&p)[3][4], const double (&s)[6], double alpha) {
+// (kind 5); u = O^{t-1} at the point.  The Laplacian is summed as an x/y chain (the centre term starts
+// it) plus a z chain, L = xy + z (round 2: the two-level wave kernel, pipe25.cu, finishes the x/y chain
+// of plane z in the step level 1 computes that plane and accumulates the z chain as planes z+1..z+4
+// arrive -- the same operations as here).
+__device__ __forceinline__ double point_25w_xy(double c, const double (&m)[3][4], const double (&p)[3][4],
+                                               const double (&s)[6]) {
   double L = __dmul_rn(s[0], c);
 #pragma unroll
-  for (int r = 0; r < 4; ++r) {
-    double S = __dadd_rn(__dadd_rn(__dadd_rn(m[0][r], p[0][r]), __dadd_rn(m[1][r], p[1][r])),
-                         __dadd_rn(m[2][r], p[2][r]));
-    L = __fma_rn(s[1 + r], S, L);
-  }
-  return __fma_rn(alpha, L, __dsub_rn(__dmul_rn(2.0, c), u));
+  for (int r = 0; r < 4; ++r)
+    L = __fma_rn(s[1 + r], __dadd_rn(__dadd_rn(m[0][r], p[0][r]), __dadd_rn(m[1][r], p[1][r])), L);
+  return L;
+}
+// term r (1..4) of the wave's z chain: w_r * (O[z-r] + O[z+r]) (r = 1 starts the chain) added to z
+__device__ __forceinline__ double point_25w_zterm(int r, double z, double w, double vm, double vp) {
+  return r == 1 ? __dmul_rn(w, __dadd_rn(vm, vp)) : __fma_rn(w, __dadd_rn(vm, vp), z);
+}
+// the update from the two halves of the Laplacian
+__device__ __forceinline__ double point_25w_final(double c, double u, double xy, double z, double alpha) {
+  return __fma_rn(alpha, __dadd_rn(xy, z), __dsub_rn(__dmul_rn(2.0, c), u));
+}
+__device__ __forceinline__ double point_25w(double c, double u, const double (&m)[3][4],
+                                            const double (&p)[3][4], const double (&s)[6], double alpha) {
+  const double xy = point_25w_xy(c, m, p, s);
+  double z = 0.0;
+#pragma unroll
+  for (int r = 1; r <= 4; ++r) z = point_25w_zterm(r, z, s[r], m[2][r - 1], p[2][r - 1]);
+  return point_25w_final(c, u, xy, z, alpha);
 }
 
 // Dispatch on the kind; W = the coefficient values at the point (variable kinds), u = O^{t-1} (wave),

@@ -65,3 +65,43 @@ def test_bt2_loopback_slabs(halo, P):
         g.run(6)
         assert g.info()["bt"] == 2
         assert np.array_equal(g.read(0), ref[0])
+
+
+# ------------------------------------------------------------------ the wave (Fig. 1e) on the same kernel
+W = synth.K25W
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+def test_wave_bt2_bitwise_equal_naive(shape):
+    """pipe25.cu's wave instance (tile_cfg 0; 1 and 2 = the round-1 generic kernel): both new levels
+    (Omega^T and Omega^{T-1}) bitwise equal to the naive sweeps."""
+    for T in (1, 2, 3, 6):
+        ref = gpu_run(W, *shape, T, seed=23, variant=st.ST_VARIANT_NAIVE)
+        for cfg in (0, 1):
+            for zc in (0, 1, 3, 1000):
+                got = gpu_run(W, *shape, T, seed=23, variant=st.ST_VARIANT_PIPE, bt=2, zchunk=zc, tile_cfg=cfg)
+                assert got[2]["bt"] == 2
+                assert np.array_equal(got[0], ref[0]), (shape, T, cfg, zc)
+                assert np.array_equal(got[1], ref[1]), (shape, T, cfg, zc)
+
+
+def test_wave_bt2_oracle_short_T():
+    nx, ny, nz = 130, 37, 41
+    inp = synth.make_inputs(W, nx, ny, nz, seed=8)
+    o_new, o_old = inp.V.copy(), inp.U.copy()
+    done = 0
+    for T in (1, 2, 3, 4, 5):
+        oracle.run_arrays(W, nx, ny, nz, o_new, o_old, inp.coef, inp.scalars, T - done)
+        done = T
+        g_new, g_old, info = gpu_run(W, nx, ny, nz, T, seed=8, bt=2)
+        assert info["bt"] == 2
+        assert_parity(W, g_new, g_old, o_new, o_old, inp.R, 1e-13, inputs=inp)
+
+
+@pytest.mark.parametrize("halo", [st.ST_HALO_COPY, st.ST_HALO_PEER])
+def test_wave_bt2_loopback_slabs(halo):
+    nx, ny, nz = 70, 33, 40
+    ref = gpu_run(W, nx, ny, nz, 6, seed=6, variant=st.ST_VARIANT_NAIVE)
+    with st.Grid(W, nx, ny, nz, seed=6, bt=2, nranks=3, local_slabs=3, halo=halo) as g:
+        g.run(6)
+        assert np.array_equal(g.read(0), ref[0]) and np.array_equal(g.read(1), ref[1])
