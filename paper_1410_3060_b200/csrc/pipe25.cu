@@ -250,26 +250,7 @@ __global__ void __launch_bounds__(P25Cfg<KIND, TX, TY, D, CLU>::THREADS, 1)
         it.gy0 += (int)crank * TY;
         const int xb = ((it.gx0 - R + p.xoff) & ~1) - (p.xoff & ~1);  // box B (footprint)
         const int xa = ((it.gx0 + p.xoff) & ~1) - (p.xoff & ~1);      // boxes A, C (level-1 extent)
-        // lockstep inside a round (one z-chunk per tile, so every item of the launch has the same steps):
-        // every SY steps the producers meet at a grid-wide counter, so the CTAs of a round -- neighbouring
-        // tiles -- stay within SY + 2 planes of each other and their shared halo boxes stay in L2
-        constexpr int SY = 32;
-        const bool isync = CLU == 1 && p.lockstep == 1 && p.nzc == 1;
-        const int nsync = (it.s_end - it.s_begin) / SY;  // sync points per item
-        const unsigned int sbase = (unsigned int)((long long)nsync * min((long long)n * gridDim.x, (long long)items));
-        const unsigned int sact = (unsigned int)min((long long)gridDim.x, (long long)items - (long long)n * gridDim.x);
-        if (isync && skip) atomicAdd(p.sched + 2, (unsigned int)nsync);  // fault injection still arrives
         for (int s = it.s_begin; s <= it.s_end && !skip; ++s, ++iv) {
-          if (isync && s > it.s_begin && (s - it.s_begin) % SY == 0) {
-            const unsigned int want = sbase + sact * (unsigned int)((s - it.s_begin) / SY);
-            atomicAdd(p.sched + 2, 1u);
-            unsigned int v;
-            for (;;) {
-              asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p.sched + 2) : "memory");
-              if (v >= want) break;
-              __nanosleep(64);
-            }
-          }
           const uint32_t sl = iv % D;
           mbar_wait(&empty[sl], ((iv / D) & 1) ^ 1);
           // level 1 computes plane q = s - R this step only once its z-neighbours are in the ring (then it
@@ -312,7 +293,6 @@ __global__ void __launch_bounds__(P25Cfg<KIND, TX, TY, D, CLU>::THREADS, 1)
       if ((CLU == 1 || crank == 0) && atomicAdd(p.sched + 1, 1u) == gridDim.x / CLU - 1) {
         p.sched[0] = 0;
         p.sched[1] = 0;
-        p.sched[2] = 0;
         __threadfence();
       }
     }
@@ -760,8 +740,7 @@ cudaError_t run_pipe25(const KParams& p0, int zchunk_req, int num_sms, cudaStrea
   // single-CTA tiles: lockstep rounds over compact patches of tiles (STENCIL_SCHED=0: dynamic, row-major)
   static const int sched_env = getenv("STENCIL_SCHED") ? atoi(getenv("STENCIL_SCHED")) : 1;
   if (CLU == 1 && sched_env && p.nblk <= 1 && p.tband == 0) {
-    static const int isync_env = getenv("STENCIL_ISYNC") ? atoi(getenv("STENCIL_ISYNC")) : 1;
-    p.lockstep = isync_env ? 1 : 2;  // 2: rounds without the meeting points inside an item
+    p.lockstep = 1;
     // patch shape: a missed block edge costs R*2 halo rows x TX (bottom) or R*2 columns x TY (right)
     static const int bw_env = getenv("STENCIL_TILE_BLOCK") ? atoi(getenv("STENCIL_TILE_BLOCK")) : 0;
     int bw = bw_env > 0 ? bw_env : (int)(std::sqrt((double)grid * TY / TX) + 0.5);
