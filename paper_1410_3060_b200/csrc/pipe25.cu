@@ -215,7 +215,11 @@ __global__ void __launch_bounds__(P25Cfg<KIND, TX, TY, D, CLU>::THREADS, 1)
         const uint32_t qs = n & 3;
         mbar_wait(&itemEmpty[qs], ((n >> 2) & 1) ^ 1);
         int g;
-        if constexpr (CLU > 1) {
+        if (CLU > 1 && p.lockstep) {
+          // static rounds of whole clusters: every CTA of cluster k takes item n * (G / CLU) + k
+          g = (int)(n * (gridDim.x / CLU) + blockIdx.x / CLU);
+          if (g >= items) g = -1;
+        } else if constexpr (CLU > 1) {
           // every CTA of a cluster takes the same items: rank 0 draws from the global counter and passes
           // the id to the others through a 4-entry queue in their shared memory
           if (crank == 0) {
@@ -274,10 +278,11 @@ __global__ void __launch_bounds__(P25Cfg<KIND, TX, TY, D, CLU>::THREADS, 1)
             }
           }
         }
-        if (CLU == 1 && p.lockstep) {
+        if (p.lockstep) {
           // round n issued: wait until every CTA with an item in round n has issued its loads too (all CTAs
           // are resident, one per SM, so this grid-wide wait cannot deadlock)
-          const unsigned int want = (unsigned int)min((long long)(n + 1) * gridDim.x, (long long)items);
+          const unsigned int want =
+              (unsigned int)(CLU * min((long long)(n + 1) * (gridDim.x / CLU), (long long)items));
           __threadfence();
           atomicAdd(p.sched, 1u);
           unsigned int v;
@@ -737,16 +742,17 @@ cudaError_t run_pipe25(const KParams& p0, int zchunk_req, int num_sms, cudaStrea
   const int grid = (int)std::min<long long>(items, clusters) * CLU;
   static const int pfd_env = getenv("STENCIL_PF") ? atoi(getenv("STENCIL_PF")) : 0;
   p.pfd = pfd_env;  // L2 prefetch distance in steps (0 = none)
-  // single-CTA tiles: lockstep rounds over compact patches of tiles (STENCIL_SCHED=0: dynamic, row-major)
+  // lockstep rounds over compact patches of tiles (STENCIL_SCHED=0: dynamic, row-major); a round is one
+  // item per cluster (one CTA per SM), the patch about square in cells
   static const int sched_env = getenv("STENCIL_SCHED") ? atoi(getenv("STENCIL_SCHED")) : 1;
-  if (CLU == 1 && sched_env && p.nblk <= 1 && p.tband == 0) {
+  if (sched_env && p.nblk <= 1 && p.tband == 0) {
     p.lockstep = 1;
-    // patch shape: a missed block edge costs R*2 halo rows x TX (bottom) or R*2 columns x TY (right)
+    const int conc = grid / CLU;
     static const int bw_env = getenv("STENCIL_TILE_BLOCK") ? atoi(getenv("STENCIL_TILE_BLOCK")) : 0;
-    int bw = bw_env > 0 ? bw_env : (int)(std::sqrt((double)grid * TY / TX) + 0.5);
+    int bw = bw_env > 0 ? bw_env : (int)(std::sqrt((double)conc * C::OYP / C::OX) + 0.5);
     bw = std::max(1, std::min(bw, ntx));
     p.tblk_w = bw;
-    p.tblk_h = std::max(1, (grid + bw - 1) / bw);
+    p.tblk_h = std::max(1, (conc + bw - 1) / bw);
   }
   if constexpr (CLU == 1) {
     kern<<<grid, C::THREADS, C::SMEM, stream>>>(mapA, mapB, mapC, p, ntx, nty, (int)items);
