@@ -73,6 +73,10 @@ struct P25Cfg {
   static constexpr int RXEL = R * TX;                       // one pushed boundary strip (R rows)
   static constexpr int NRX = CLU > 1 ? 4 : 0;               // receive slots per side
   static constexpr int STASH = CLU > 1 ? 2 * 32 * NCELL * 5 : 0;  // boundary warps' carried x chain + Wy
+  // CLU = 2: the warp without level-2 rows ("helper") finishes the boundary warp's y chains; it hands the
+  // x/y halves back through a mailbox (double-buffered by step parity; the stash is too)
+  static constexpr bool HELPER = CLU == 2;
+  static constexpr int MBOX = HELPER ? 2 * 32 * NCELL : 0;
   static constexpr int WROWS = 32 / LPR * CY;               // E1 rows per consumer warp
   // level 2 on just the output cells, (TX-2R)/2 x (TY-2R)/2 threads of 2x2 blocks in warps 1.. (the
   // warp-aligned mapping also computes the R-wide halo columns at level 2, a quarter of its cells).
@@ -83,7 +87,7 @@ struct P25Cfg {
   static constexpr int L2T = (TX - 2 * R) / 2 * ((TY - 2 * R) / 2);  // level-2 threads when REMAP
   static_assert(!REMAP || (L2T % 32 == 0 && L2T / 32 + 1 <= NW && L2T / 32 <= 3), "level-2 warps 1..");
   static constexpr uint32_t TX_BYTES_A = AEL * 8, TX_BYTES_B = BEL * 8, TX_BYTES_C = CEL * 8, RX_BYTES = RXEL * 8;
-  static constexpr size_t SMEM = 8 * ((size_t)D * SLOT + (size_t)NPB * PEL + 2 * (size_t)NRX * RXEL + STASH) +
+  static constexpr size_t SMEM = 8 * ((size_t)D * SLOT + (size_t)NPB * PEL + 2 * (size_t)NRX * RXEL + STASH + MBOX) +
                                  8 * (2 * D + 8 + 2 * NRX + 8) + 4 * 8 + 128;
   static_assert(TX % 16 == 0 && TY % CY == 0 && NCONS % 32 == 0 && 32 % LPR == 0, "thread layout");
   static_assert(TY % WROWS == 0 && WROWS == R, "one warp = R rows (the pushed strip)");
@@ -171,8 +175,9 @@ __global__ void __launch_bounds__(P25Cfg<KIND, TX, TY, D, CLU>::THREADS, 1)
   double* sP = ring + (size_t)D * C::SLOT;
   double* rxTop = sP + (size_t)C::NPB * C::PEL;      // rows -R..-1 (the CTA above, rank - 1), per slot
   double* rxBot = rxTop + (size_t)C::NRX * C::RXEL;  // rows TY..TY+R-1 (the CTA below, rank + 1)
-  double* stash = rxBot + (size_t)C::NRX * C::RXEL;  // [boundary warp top/bottom][lane][cell][5]
-  uint64_t* full = reinterpret_cast<uint64_t*>(stash + C::STASH);
+  double* stash = rxBot + (size_t)C::NRX * C::RXEL;  // [boundary warp top/bottom | step parity][lane][cell][5]
+  double* mbox = stash + C::STASH;                    // HELPER: [step parity][lane][cell]
+  uint64_t* full = reinterpret_cast<uint64_t*>(mbox + C::MBOX);
   uint64_t* empty = full + D;
   uint64_t* itemFull = empty + D;
   uint64_t* itemEmpty = itemFull + 4;
@@ -320,8 +325,13 @@ __global__ void __launch_bounds__(P25Cfg<KIND, TX, TY, D, CLU>::THREADS, 1)
   const bool topB = CLU > 1 && warp == 0 && crank > 0;                        // needs rows of rank - 1
   const bool botB = CLU > 1 && warp == NW - 1 && crank < (uint32_t)CLU - 1;  // needs rows of rank + 1
   const bool bnd = topB || botB;
+  // HELPER (pairs): rank 0's warp 0 / rank 1's last warp has no level-2 rows; it computes the delayed y
+  // chains of the boundary warp (rank 0's last warp / rank 1's warp 0) -- same lanes, same columns
+  const bool helper = C::HELPER && !lvl2;
+  const int bwarp = crank == 0 ? NW - 1 : 0;                          // the boundary warp a helper serves
+  const int hly0 = ((bwarp * 32 + lane) / C::LPR) * CY;               // its lane's first row
   const uint32_t tq = tmem_base + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)((warp >> 2) * 256);
-  double* myst = stash + (size_t)((topB ? 0 : 1) * 32 + lane) * C::NCELL * 5;  // boundary warps only
+  double* myst = stash + (size_t)((topB ? 0 : 1) * 32 + lane) * C::NCELL * 5;  // boundary warps (CLU = 4)
   const double ps[6] = {p.s[0], p.s[1], p.s[2], p.s[3], p.s[4], p.s[5]};  // the wave's w0, w1..w4, alpha
   uint32_t iv = 0;
 
@@ -469,7 +479,7 @@ __global__ void __launch_bounds__(P25Cfg<KIND, TX, TY, D, CLU>::THREADS, 1)
             const int row = min(max(l2y - R + r, 0), TY - 1);  // rows outside E1 only feed discarded cells
             lds_row<CX, true>(P + row * TX + l2x, ys[r]);
           }
-        } else if constexpr (CLU > 1) {
+        } else if constexpr (CLU > 1 && !C::HELPER) {
           // the y chain of plane q-1, one step late: level-1 plane q-1 and the neighbour's rows of it,
           // received during the last step
           const double* Pp = sP + (size_t)((iv + C::NPB - 1) % C::NPB) * C::PEL;
@@ -544,7 +554,8 @@ __global__ void __launch_bounds__(P25Cfg<KIND, TX, TY, D, CLU>::THREADS, 1)
                 if (!bnd) {
                   Pq[i] = point_25v_xy(vc[j][i], m, pl, W);
                 } else {  // carried to the next step with plane q's y coefficients
-                  double* sv = myst + (j * CX + i) * 5;
+                  double* sv = (C::HELPER ? stash + (size_t)((iv & 1u) * 32 + lane) * C::NCELL * 5 : myst) +
+                               (j * CX + i) * 5;
                   sv[0] = point_25v_x(vc[j][i], m, pl, W);
 #pragma unroll
                   for (int r = 1; r <= R; ++r) sv[r] = W[3 * r - 1];
@@ -607,9 +618,15 @@ __global__ void __launch_bounds__(P25Cfg<KIND, TX, TY, D, CLU>::THREADS, 1)
               const double z1 = point_25v_zterm(1, 0.0, S[12], vr[0], v);   // plane q-1: first term
               vout[i] = __dadd_rn(S[0], z4);  // point_25v: (x/y half) + z chain
               uout[i] = 0.0;
-              // boundary warps complete P(q-1) only now (its slot held a placeholder)
-              const double Pq1 = bnd ? Pprev[j][i] : S[3];
-              const double N[16] = {S[1], S[2], Pq1, Pq[i], z3, z2n, S[8], S[10], S[11], S[13], S[14], S[15],
+              // boundary warps complete P(q-1) only now (its slot held a placeholder); with a helper warp the
+              // completed P(q-2) arrives from the mailbox, written by the helper last step
+              double Pq1 = S[3], Pq2 = S[2];
+              if constexpr (C::HELPER) {
+                if (bnd) Pq2 = mbox[(size_t)((iv - 1u) & 1u) * 32 * C::NCELL + lane * C::NCELL + cell];
+              } else {
+                if (bnd) Pq1 = Pprev[j][i];
+              }
+              const double N[16] = {S[1], Pq2, Pq1, Pq[i], z3, z2n, S[8], S[10], S[11], S[13], S[14], S[15],
                                     Wz[0][i], Wz[1][i], Wz[2][i], Wz[3][i]};
 #pragma unroll
               for (int k = 0; k < 16; ++k) put(st + 2 * k, N[k]);
@@ -628,6 +645,46 @@ __global__ void __launch_bounds__(P25Cfg<KIND, TX, TY, D, CLU>::THREADS, 1)
           }
         }
         if constexpr (!WAVE) tmem_st8(tq + kColS2, s2n);
+      }
+      if constexpr (C::HELPER && !WAVE) {
+        if (helper) {
+          // the boundary warp's y chains of plane q-1: level-1 plane q-1 (this CTA's rows) and the cluster
+          // neighbour's R rows of it (pushed last step), plus the x chain and y coefficients the boundary
+          // warp left in the stash; P(q-1) = x + y goes to the mailbox for the boundary warp's next step
+          const double* Pp = sP + (size_t)((iv + C::NPB - 1) % C::NPB) * C::PEL;
+          const uint32_t k = (iv + C::NRX - 1) % C::NRX;
+          // acquire at cluster scope: the rows were written by the neighbour's bulk copy
+          if (iv > 0) mbar_wait_cluster(crank == 0 ? &rxbBot[k] : &rxbTop[k], ((iv - 1) / C::NRX) & 1);
+          const double* rx = (crank == 0 ? rxBot : rxTop) + (size_t)k * C::RXEL;
+          double ys[CY + 2 * R][CX];
+#pragma unroll
+          for (int r = 0; r < CY + 2 * R; ++r) {
+            const int row = hly0 - R + r;
+            if (row < 0) lds_row<CX, true>(rx + (row + R) * TX + x0, ys[r]);
+            else if (row >= TY) lds_row<CX, true>(rx + (row - TY) * TX + x0, ys[r]);
+            else lds_row<CX, true>(Pp + row * TX + x0, ys[r]);
+          }
+          const double* sv0 = stash + (size_t)(((iv - 1u) & 1u) * 32 + lane) * C::NCELL * 5;
+          double* mb = mbox + (size_t)(iv & 1u) * 32 * C::NCELL + lane * C::NCELL;
+#pragma unroll
+          for (int j = 0; j < CY; ++j)
+#pragma unroll
+            for (int i = 0; i < CX; ++i) {
+              const double* sv = sv0 + (j * CX + i) * 5;  // x chain and Wy_1..4 of plane q-1
+              double m[3][R], pl[3][R], W[NC > 0 ? NC : 1];
+#pragma unroll
+              for (int r = 1; r <= R; ++r) {
+                m[1][r - 1] = ys[R + j - r][i];
+                pl[1][r - 1] = ys[R + j + r][i];
+                m[0][r - 1] = pl[0][r - 1] = m[2][r - 1] = pl[2][r - 1] = 0.0;
+              }
+#pragma unroll
+              for (int f = 0; f < NC; ++f) W[f] = 0.0;
+#pragma unroll
+              for (int r = 1; r <= R; ++r) W[3 * r - 1] = sv[r];
+              mb[j * CX + i] = __dadd_rn(sv[0], point_25v_y(m, pl, W));
+            }
+        }
       }
       tmem_wait_st();  // this step's TMEM stores land before the next step's loads
       __syncwarp();
