@@ -79,7 +79,12 @@ enum {
                             loads through registers, one CTA per tile and z-chunk */
   ST_VARIANT_PIPE = 3,   /* the same wavefront with TMA-fed shared-memory rings: a producer warp
                             streams planes and coefficient fields ahead with cp.async.bulk.tensor +
-                            mbarriers; persistent CTAs.  The default. */
+                            mbarriers; persistent CTAs.  The default.  bt per kind:
+                            7c <= 8, 7v <= 4, the 25-point kinds <= 2 (two fused levels of the
+                            25-point stencils run the two-level kernel of DESIGN.md §5b, whose
+                            z-chains are carried in tensor memory), the alpha-field wave 1.  Library
+                            defaults: 7c 4, 7v 4, 25v 2, the waves 1 (the Python binding applies
+                            tools/tune.py's measured plan for known shapes). */
   ST_VARIANT_COOP = 4    /* small, latency-bound grids (their arrays fit in L2): all T steps of a
                             stencil_run in ONE cooperative launch, a grid-wide barrier between
                             sweeps.  Single slab only.  Auto-selected below a size threshold.
@@ -89,16 +94,19 @@ enum {
 
 /* Halo exchange between z-slabs. */
 enum {
-  ST_HALO_COPY = 0, /* after every fused block: edge kernels, then the R*bt boundary planes are copied
-                       (device copies between the slabs of one handle; NCCL send/recv between
-                       processes on a comm stream) while the interior kernel runs ("halo-first",
-                       P:833-836).  The default. */
+  ST_HALO_COPY = 0, /* after every fused block the R*bt boundary planes are copied (device copies
+                       between the slabs of one handle; NCCL send/recv between processes on a comm
+                       stream).  Bulk-synchronous by default (one launch per slab, then the copy);
+                       STENCIL_OVERLAP=1: edge kernels first and the copy overlapping the interior
+                       kernel ("halo-first").  The default mode. */
   ST_HALO_PEER = 1  /* fused: one kernel per slab and block; the kernel stores the planes that are a
                        z-neighbour's halo straight into the neighbour's buffer as it produces them
                        (another slab of this handle, or the neighbour process's GPU memory mapped over
                        NVLink with CUDA IPC), then a stream-ordered flag write in the neighbour's
-                       memory tells it the block's halos have landed (cuStreamWriteValue64 /
-                       cuStreamWaitValue64).  No edge/interior split, no copy, no NCCL at all (no
+                       memory tells it the block's halos have landed (cuStreamWriteValue64); before
+                       its next block each rank's host polls its flags (timeout
+                       STENCIL_PEER_TIMEOUT_MS, default 120 s -> ST_E_STATE), so no GPU stream waits
+                       on another process.  No edge/interior split, no copy, no NCCL at all (no
                        nccl_id needed).  Pipe variant only.  With one slab per handle every rank must
                        call stencil_peer_export / stencil_peer_import after creating and before
                        running (ranks may also be several handles of one process: their descriptors
