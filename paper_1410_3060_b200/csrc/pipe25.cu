@@ -78,14 +78,6 @@ struct P25Cfg {
   static constexpr bool HELPER = CLU == 2;
   static constexpr int MBOX = HELPER ? 2 * 32 * NCELL : 0;
   static constexpr int WROWS = 32 / LPR * CY;               // E1 rows per consumer warp
-  // level 2 on just the output cells, (TX-2R)/2 x (TY-2R)/2 threads of 2x2 blocks in warps 1.. (the
-  // warp-aligned mapping also computes the R-wide halo columns at level 2, a quarter of its cells).
-  // Measured (C4, round 2): no gain under the power cap (58.85 vs 58.4-58.6 GLUP/s) and slower in isolation
-  // (63 vs 67 GLUP/s: the 12-thread rows of the output-only mapping conflict in shared-memory banks), so
-  // the warp-aligned mapping stays; the remapped path is kept compiled for the record (REMAP = false).
-  static constexpr bool REMAP = false;
-  static constexpr int L2T = (TX - 2 * R) / 2 * ((TY - 2 * R) / 2);  // level-2 threads when REMAP
-  static_assert(!REMAP || (L2T % 32 == 0 && L2T / 32 + 1 <= NW && L2T / 32 <= 3), "level-2 warps 1..");
   static constexpr uint32_t TX_BYTES_A = AEL * 8, TX_BYTES_B = BEL * 8, TX_BYTES_C = CEL * 8, RX_BYTES = RXEL * 8;
   static constexpr size_t SMEM = 8 * ((size_t)D * SLOT + (size_t)NPB * PEL + 2 * (size_t)NRX * RXEL + STASH + MBOX) +
                                  8 * (2 * D + 8 + 2 * NRX + 8) + 4 * 8 + 128;
@@ -317,11 +309,10 @@ __global__ void __launch_bounds__(P25Cfg<KIND, TX, TY, D, CLU>::THREADS, 1)
   // level-2 rows of this CTA (the trapezoid shrinks by R only at the cluster's outer rows)
   const int ylo = crank == 0 ? R : 0, yhi = crank == (uint32_t)CLU - 1 ? TY - R : TY;
   const int wr0 = warp * C::WROWS;  // the warp's first row (warp-uniform)
-  const bool lvl2 = C::REMAP ? (warp >= 1 && warp <= C::L2T / 32) : (wr0 + C::WROWS > ylo && wr0 < yhi);
-  // this thread's level-2 cell block (REMAP: blocks of the output region only)
-  const int t2 = tid - 32;
-  const int l2x = C::REMAP ? R + 2 * (t2 % ((TX - 2 * R) / 2)) : x0;
-  const int l2y = C::REMAP ? R + 2 * (t2 / ((TX - 2 * R) / 2)) : ly0;
+  // level 2 runs on the warps whose rows hold output cells, on the same 2x2 blocks as level 1 (an
+  // output-only mapping measured no faster)
+  const bool lvl2 = wr0 + C::WROWS > ylo && wr0 < yhi;
+  const int l2x = x0, l2y = ly0;
   const bool topB = CLU > 1 && warp == 0 && crank > 0;                        // needs rows of rank - 1
   const bool botB = CLU > 1 && warp == NW - 1 && crank < (uint32_t)CLU - 1;  // needs rows of rank + 1
   const bool bnd = topB || botB;
@@ -513,8 +504,8 @@ __global__ void __launch_bounds__(P25Cfg<KIND, TX, TY, D, CLU>::THREADS, 1)
               Pprev[j][i] = __dadd_rn(sv[0], point_25v_y(m, pl, W));
             }
         }
-        // level-1 value of plane q at this thread's level-2 cells: the centre rows of the strip just loaded
-        // (boundary warps' strip holds plane q-1: they are never remapped and use their own results)
+        // level-1 value of plane q at this thread's cells: the centre rows of the strip just loaded
+        // (a boundary warp's strip may hold plane q-1: it uses its own results)
         double vc[CY][CX];
 #pragma unroll
         for (int j = 0; j < CY; ++j)
