@@ -57,6 +57,7 @@ struct KParams {
   int tblk_w, tblk_h;  // tile order in blocks of tblk_w x tblk_h tiles (0 = row-major; set by launchers)
   int lockstep;        // pipe kernels: static round-robin items, CTAs start each round together (launcher)
   int pfd;             // pipe25: TMA L2-prefetch distance in steps (launcher; STENCIL_PF)
+  int skew_ns;         // pipe25 experiment (STENCIL_SKEW_NS): checkerboard-odd tiles start an item later
   int walign;  // pipe kernel: tiles write sector-aligned output segments (STENCIL_WALIGN=1; default 0:
                // measured slower under the power cap for OX % 4 != 0, profiles/r01_summary.md)
 };

@@ -790,7 +790,10 @@ cudaError_t run_pipe(const KParams& p0, int zchunk_req, int num_sms, cudaStream_
   if (CLU == 1 && sched_env && p.nblk <= 1 && p.tband == 0 && occ <= 1) {
     p.lockstep = 1;
     static const int bw_env = getenv("STENCIL_TILE_BLOCK") ? atoi(getenv("STENCIL_TILE_BLOCK")) : 0;
-    int bw = bw_env > 0 ? bw_env : (int)(std::sqrt((double)grid * TY / TX) + 0.5);
+    // blocks of about sqrt(grid * OY / OX) tile columns, sized so that a tile row splits into equal blocks
+    const double target = std::sqrt((double)grid * C::OYP / oxw);
+    const int nb = std::max(1, (int)(ntx / target + 0.5));
+    int bw = bw_env > 0 ? bw_env : (ntx + nb - 1) / nb;
     bw = std::max(1, std::min(bw, ntx));
     p.tblk_w = bw;
     p.tblk_h = std::max(1, (grid + bw - 1) / bw);

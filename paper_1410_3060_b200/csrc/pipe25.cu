@@ -249,6 +249,9 @@ __global__ void __launch_bounds__(P25Cfg<KIND, TX, TY, D, CLU>::THREADS, 1)
         const bool skip = (p.dbg & 8) && g == 0;  // fault injection: item 0 never loaded (nor computed)
         Item it = decode<R, 1, C::OX, C::OYP>(g, ntx, nty, p);
         it.gy0 += (int)crank * TY;
+        if (p.skew_ns > 0 && (((it.gx0 / C::OX) + (it.gy0 / C::OYP)) & 1)) {  // experiment: offset neighbours
+          for (int w = 0; w < p.skew_ns; w += 1000) __nanosleep(1000);
+        }
         const int xb = ((it.gx0 - R + p.xoff) & ~1) - (p.xoff & ~1);  // box B (footprint)
         const int xa = ((it.gx0 + p.xoff) & ~1) - (p.xoff & ~1);      // boxes A, C (level-1 extent)
         for (int s = it.s_begin; s <= it.s_end && !skip; ++s, ++iv) {
@@ -790,6 +793,8 @@ cudaError_t run_pipe25(const KParams& p0, int zchunk_req, int num_sms, cudaStrea
   const int grid = (int)std::min<long long>(items, clusters) * CLU;
   static const int pfd_env = getenv("STENCIL_PF") ? atoi(getenv("STENCIL_PF")) : 0;
   p.pfd = pfd_env;  // L2 prefetch distance in steps (0 = none)
+  static const int skew_env = getenv("STENCIL_SKEW_NS") ? atoi(getenv("STENCIL_SKEW_NS")) : 0;
+  p.skew_ns = skew_env;
   // lockstep rounds over compact patches of tiles (STENCIL_SCHED=0: dynamic, row-major); a round is one
   // item per cluster (one CTA per SM), the patch about square in cells
   static const int sched_env = getenv("STENCIL_SCHED") ? atoi(getenv("STENCIL_SCHED")) : 1;
@@ -797,7 +802,11 @@ cudaError_t run_pipe25(const KParams& p0, int zchunk_req, int num_sms, cudaStrea
     p.lockstep = 1;
     const int conc = grid / CLU;
     static const int bw_env = getenv("STENCIL_TILE_BLOCK") ? atoi(getenv("STENCIL_TILE_BLOCK")) : 0;
-    int bw = bw_env > 0 ? bw_env : (int)(std::sqrt((double)conc * C::OYP / C::OX) + 0.5);
+    // blocks of about sqrt(conc * OYP / OX) tile columns, sized so that a tile row splits into equal blocks
+    // (a narrow remainder block makes its patch tall and thin: C4 74.6 vs 70.6 DRAM B per update)
+    const double target = std::sqrt((double)conc * C::OYP / C::OX);
+    const int nb = std::max(1, (int)(ntx / target + 0.5));
+    int bw = bw_env > 0 ? bw_env : (ntx + nb - 1) / nb;
     bw = std::max(1, std::min(bw, ntx));
     p.tblk_w = bw;
     p.tblk_h = std::max(1, (conc + bw - 1) / bw);
