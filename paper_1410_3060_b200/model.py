@@ -155,7 +155,7 @@ def pipe25_plans():
     src = open(__import__("os").path.join(_CSRC, "pipe25.cu")).read()
     body = src[src.index("cudaError_t launch_pipe25v2("):]
     out = []
-    for m in re.finditer(r"(case (\d+)|default): return run_pipe25<([\d,\s]+)>", body):
+    for m in re.finditer(r"(case (\d+)|default): return run_pipe25<K25V,\s*([\d,\s]+)>", body[:body.index("cudaError_t launch_pipe25w2(")]):
         cfg = int(m.group(2)) if m.group(2) else 0
         out.append((cfg,) + tuple(int(x) for x in m.group(3).split(",")))
     return out

@@ -61,8 +61,8 @@ def _plans():
 
 def _plans25():
     src = open(os.path.join(ROOT, "paper_1410_3060_b200", "csrc", "pipe25.cu")).read()
-    body = src[src.index("cudaError_t launch_pipe25v2("):]
-    return [tuple(int(x) for x in a.split(",")) for a in re.findall(r"run_pipe25<([\d,\s]+)>", body)]
+    body = src[src.index("cudaError_t launch_pipe25v2("):src.index("cudaError_t launch_pipe25w2(")]
+    return [tuple(int(x) for x in a.split(",")) for a in re.findall(r"run_pipe25<K25V,\s*([\d,\s]+)>", body)]
 
 
 def test_every_configured_plan_fits_on_chip():
