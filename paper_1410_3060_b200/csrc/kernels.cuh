@@ -33,6 +33,7 @@ struct KParams {
                // kernel (the straight-line arithmetic still runs: results are wrong), bit 1 = skip level
                // barriers; fault injection for the mutation tests (STENCIL_FAULT):
                // bit 2 = never write the last plane of a z-chunk, bit 3 = skip work item 0
+               // (pipe25: bit 4 = box B re-reads plane s, a DRAM diagnostic with wrong results)
   unsigned int* sched;  // pipe kernel: 2 zeroed device counters (next work item, CTAs done)
   // Pipe kernel, several fused blocks in ONE launch (Jacobi kinds, single slab): nblk blocks; block i
   // reads the buffer block i-1 wrote (odd blocks: V from dst_raw, stores to dst_alt = the src buffer);
@@ -58,6 +59,8 @@ struct KParams {
   int lockstep;        // pipe kernels: static round-robin items, CTAs start each round together (launcher)
   int pfd;             // pipe25: TMA L2-prefetch distance in steps (launcher; STENCIL_PF)
   int skew_ns;         // pipe25 experiment (STENCIL_SKEW_NS): checkerboard-odd tiles start an item later
+  int l2h;             // pipe25 experiment (STENCIL_L2H): L2 priorities of boxes A/B/C, 2 bits each
+                       // (0 = no hint, 1 = evict_first, 2 = evict_last, 3 = evict_normal)
   int walign;  // pipe kernel: tiles write sector-aligned output segments (STENCIL_WALIGN=1; default 0:
                // measured slower under the power cap for OX % 4 != 0, profiles/r01_summary.md)
 };

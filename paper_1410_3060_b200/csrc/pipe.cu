@@ -200,6 +200,7 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN,
     if (tid == NCONS) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(&mapV) : "memory");
       if (HAS_C) asm volatile("prefetch.tensormap [%0];" ::"l"(&mapC) : "memory");
+      const uint64_t polA = l2_policy(p.l2h & 3), polC = l2_policy((p.l2h >> 4) & 3);  // STENCIL_L2H experiment
       uint32_t iv = 0;
       for (uint32_t n = 0;; ++n) {
         const uint32_t qs = n & 3;
@@ -287,7 +288,8 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN,
           const uint32_t sv = iv % DV, nv = iv / DV;
           mbar_wait(&emptyV[sv], (nv & 1) ^ 1);
           mbar_expect_tx(&fullV[sv], (C::VELEMS + (C::MERGE ? C::CFIELD * C::NCF : 0)) * sizeof(double));
-          tma_load_3d(sV + (size_t)sv * C::VSLOT, mv, &fullV[sv], xv, it.gy0 - R, s);
+          if (p.l2h) tma_load_3d_hint(sV + (size_t)sv * C::VSLOT, mv, &fullV[sv], xv, it.gy0 - R, s, polA);
+          else tma_load_3d(sV + (size_t)sv * C::VSLOT, mv, &fullV[sv], xv, it.gy0 - R, s);
           if constexpr (HAS_C) {
             const uint32_t sc = iv % DC, nc = iv / DC;
             uint64_t* fc = C::MERGE ? &fullV[sv] : &fullC[sc];
@@ -299,6 +301,8 @@ __global__ void __launch_bounds__(PipeCfg<KIND, BT, TX, TY, CX, CY, DV, DC, WIN,
               tma_load_3d(sC + (size_t)sc * C::CSLOT, &mapC, fc, xc, it.gy0, s - R);
               if constexpr (NC > 0)  // the wave's alpha field behind Omega^{t-1} in the same slot
                 tma_load_4d(sC + (size_t)sc * C::CSLOT + C::CF0, &mapA, fc, xc, it.gy0, s - R, 0);
+            } else if (p.l2h) {
+              tma_load_4d_hint(sC + (size_t)sc * C::CSLOT, &mapC, fc, xc, it.gy0, s - R, 0, polC);
             } else {
               tma_load_4d(sC + (size_t)sc * C::CSLOT, &mapC, fc, xc, it.gy0, s - R, 0);
             }
@@ -786,6 +790,8 @@ cudaError_t run_pipe(const KParams& p0, int zchunk_req, int num_sms, cudaStream_
   // single-block launches of single-CTA tiles: lockstep rounds over compact patches of tiles, so the
   // overlapping halo boxes of y-neighbours are streamed at the same time and hit L2 (STENCIL_SCHED=0:
   // dynamic work counter, row-major tiles)
+  static const int l2h_env = getenv("STENCIL_L2H") ? atoi(getenv("STENCIL_L2H")) : 0;
+  p.l2h = l2h_env;
   static const int sched_env = getenv("STENCIL_SCHED") ? atoi(getenv("STENCIL_SCHED")) : 1;
   if (CLU == 1 && sched_env && p.nblk <= 1 && p.tband == 0 && occ <= 1) {
     p.lockstep = 1;

@@ -208,6 +208,8 @@ __global__ void __launch_bounds__(P25Cfg<KIND, TX, TY, D, CLU>::THREADS, 1)
       asm volatile("prefetch.tensormap [%0];" ::"l"(&mapB) : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"(&mapC) : "memory");
       uint32_t iv = 0;
+      const uint64_t polA = l2_policy(p.l2h & 3), polB = l2_policy((p.l2h >> 2) & 3),
+                     polC = l2_policy((p.l2h >> 4) & 3);
       for (uint32_t n = 0;; ++n) {
         const uint32_t qs = n & 3;
         mbar_wait(&itemEmpty[qs], ((n >> 2) & 1) ^ 1);
@@ -264,11 +266,22 @@ __global__ void __launch_bounds__(P25Cfg<KIND, TX, TY, D, CLU>::THREADS, 1)
           const bool need1 = needB && (it.s_begin == 0 || q >= it.s_begin + R);
           mbar_expect_tx(&full[sl], C::TX_BYTES_A + (needB ? C::TX_BYTES_B : 0u) + (need1 ? C::TX_BYTES_C : 0u));
           double* slot = ring + (size_t)sl * C::SLOT;
-          tma_load_3d(slot, &mapA, &full[sl], xa, it.gy0, s);
-          if (needB) tma_load_3d(slot + C::BOFF, &mapB, &full[sl], xb, it.gy0 - R, q);
-          if (need1) {
-            if constexpr (WAVE) tma_load_3d(slot + C::COFF, &mapC, &full[sl], xa, it.gy0, q);  // Omega^{t-1}
-            else tma_load_4d(slot + C::COFF, &mapC, &full[sl], xa, it.gy0, q, 0);
+          // (STENCIL_DBG bit 16, a DRAM-traffic diagnostic with wrong results: box B re-reads plane s)
+          const int qb = (p.dbg & 16) ? s : q;
+          if (p.l2h == 0) {
+            tma_load_3d(slot, &mapA, &full[sl], xa, it.gy0, s);
+            if (needB) tma_load_3d(slot + C::BOFF, &mapB, &full[sl], xb, it.gy0 - R, qb);
+            if (need1) {
+              if constexpr (WAVE) tma_load_3d(slot + C::COFF, &mapC, &full[sl], xa, it.gy0, q);  // Omega^{t-1}
+              else tma_load_4d(slot + C::COFF, &mapC, &full[sl], xa, it.gy0, q, 0);
+            }
+          } else {  // experiment: L2 eviction priorities per box
+            tma_load_3d_hint(slot, &mapA, &full[sl], xa, it.gy0, s, polA);
+            if (needB) tma_load_3d_hint(slot + C::BOFF, &mapB, &full[sl], xb, it.gy0 - R, qb, polB);
+            if (need1) {
+              if constexpr (WAVE) tma_load_3d_hint(slot + C::COFF, &mapC, &full[sl], xa, it.gy0, q, polC);
+              else tma_load_4d_hint(slot + C::COFF, &mapC, &full[sl], xa, it.gy0, q, 0, polC);
+            }
           }
           if (p.pfd > 0 && s + p.pfd <= it.s_end) {  // warm L2 for the loads pfd steps ahead (beyond the ring)
             tma_prefetch_3d(&mapA, xa, it.gy0, s + p.pfd);
@@ -795,6 +808,8 @@ cudaError_t run_pipe25(const KParams& p0, int zchunk_req, int num_sms, cudaStrea
   p.pfd = pfd_env;  // L2 prefetch distance in steps (0 = none)
   static const int skew_env = getenv("STENCIL_SKEW_NS") ? atoi(getenv("STENCIL_SKEW_NS")) : 0;
   p.skew_ns = skew_env;
+  static const int l2h_env = getenv("STENCIL_L2H") ? atoi(getenv("STENCIL_L2H")) : 0;
+  p.l2h = l2h_env;
   // lockstep rounds over compact patches of tiles (STENCIL_SCHED=0: dynamic, row-major); a round is one
   // item per cluster (one CTA per SM), the patch about square in cells
   static const int sched_env = getenv("STENCIL_SCHED") ? atoi(getenv("STENCIL_SCHED")) : 1;
