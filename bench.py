@@ -368,6 +368,17 @@ def roofline_of(w, bt, value_per_gpu, kern_ms, kern_steps, cells_local, peak, fp
             "dram_bytes_per_lup": tr / (cells_local * bt) if tr else None}
 
 
+def modeled_dram(st, w, info):
+    """DRAM bytes per update the lockstep round model predicts for the plan that ran (model.py
+    lockstep_dram_bytes_per_lup: round-patch halo re-reads, ghosts, 128-byte lines), next
+    to ncu's `dram_bytes_per_lup`; None for plans without lockstep rounds."""
+    if info["variant"] != st.ST_VARIANT_PIPE:
+        return None
+    from paper_1410_3060_b200 import model
+    return round(model.lockstep_dram_bytes_per_lup(w.kind, info["bt"], (w.nx, w.ny, w.nz),
+                                                   (info["tile_x"], info["tile_y"])), 2)
+
+
 def alloc_pinned(shape, torch):
     """A page-locked host array (numpy view of a pinned torch tensor)."""
     n = int(np.prod(shape))
@@ -524,6 +535,8 @@ def main():
     roofline.update({"peak_source": peak_src, "fp64_source": fp64_src,
                      "avg_launch_ms": kern_ms / max(1, kern_launches),
                      "kernel_share_of_step": kern_ms / ms if ms else None})
+    if world == 1 and slabs == 1:
+        roofline["modeled_dram_bytes_per_lup"] = modeled_dram(st, w, info)
     plan = {"bt": bt, "variant": info["variant"], "tile": [info["tile_x"], info["tile_y"]],
             "zchunk": info["zchunk"], "halo": args.halo if (world > 1 or slabs > 1) else None,
             "halo_note": halo_note, "device_bytes": info["device_bytes"],
@@ -567,6 +580,7 @@ def main():
                                   "frac_of_roof_bt": rs["frac_of_roof_bt"], "roof_glups_bt": rs["roof_glups_bt"],
                                   "frac_of_roof_bt1": rs["frac_of_roof_bt1"], "hbm_frac": rs["frac"],
                                   "dram_bytes_per_lup": rs["dram_bytes_per_lup"],
+                                  "modeled_dram_bytes_per_lup": modeled_dram(st, ws, is_),
                                   "sm_mhz": cs_.get("sm_mhz"), "power_w": cs_.get("power_w")}
 
     # e2e: through the public API with HOST buffers: create from pinned host inputs (H2D), run T,

@@ -7,6 +7,7 @@ Kinds: 1 = 7-point constant (Fig. 1b), 2 = 7-point variable (Fig. 1c), 3 = 25-po
 alpha (Fig. 1e, BASELINE.json config 3), 4 = 25-point variable (Fig. 1d), 5 = the wave with the
 domain-sized alpha field as printed.
 """
+import math
 K7C, K7V, K25W, K25V, K25WA = 1, 2, 3, 4, 5
 WAVE_KINDS = (K25W, K25WA)
 COEF_FIELDS = {K7C: 0, K7V: 7, K25W: 0, K25V: 13, K25WA: 1}  # domain-sized read-only streams
@@ -121,6 +122,68 @@ def l2_retention_steps(out_tile, bt, kind, ctas=148, l2_bytes=126 * 2 ** 20):
     block's compulsory bytes per cell."""
     per_step = ctas * out_tile[0] * out_tile[1] * code_balance(kind, bt) * bt
     return l2_bytes / per_step
+
+
+def lockstep_tile_blocks(ntx, out_tile, conc=148):
+    """(tblk_w, tblk_h) of the lockstep tile order the launchers pick (pipe.cu / pipe25.cu: blocks of about
+    sqrt(conc * OY / OX) tile columns, sized so that a tile row splits into equal blocks)."""
+    OX, OY = out_tile
+    target = math.sqrt(conc * OY / OX)
+    nb = max(1, int(ntx / target + 0.5))
+    bw = max(1, min((ntx + nb - 1) // nb, ntx))
+    return bw, max(1, (conc + bw - 1) // bw)
+
+
+def lockstep_dram_bytes_per_lup(kind, bt, shape, out_tile, conc=148, granule=128):
+    """DRAM bytes per lattice update of one lockstep launch of bt fused levels over a grid of `shape`
+     if the L2 keeps everything a round streams and nothing across rounds.  Per round (conc
+    consecutive tiles of the blocked order, `sm100.cuh` decode, blocks from lockstep_tile_blocks): the union
+    of the coefficient boxes (the level-1 extent, i.e. the output tile grown by R per fused level beyond
+    the first; NC fields, the wave's Omega^{t-1} as one) and of the state boxes (the level-0 footprint, R
+    wider again) over the padded plane, taken in aligned `granule`-byte pieces of each row (the DRAM fetch
+    granularity; interior column x = R starts a 128-byte line, `runtime.cu`); every tile streams the
+    nz + 2R planes of the padded z extent; plus one write per cell (two for the wave at bt >= 2).  The
+    excess over code_balance is the re-read of halos across round-patch boundaries, the ghost cells and
+    the partial lines at patch and grid edges; what ncu measures beyond it is lost inside a round."""
+    import numpy as np
+    R, NC = RADIUS[kind], COEF_FIELDS[kind] + (1 if kind in WAVE_KINDS else 0)
+    nx, ny, nz = shape
+    OX, OY = out_tile
+    ntx, nty = -(-nx // OX), -(-ny // OY)
+    bw, bh = lockstep_tile_blocks(ntx, out_tile, conc)
+    H = R * (bt - 1)  # the level-1 extent reaches H beyond the output tile, the footprint H + R
+    ext_tile, foot_tile = (OX + 2 * H, OY + 2 * H), (OX + 2 * H + 2 * R, OY + 2 * H + 2 * R)
+    X, Y = nx + 2 * R, ny + 2 * R
+    g = max(1, granule // 8)  # doubles per granule
+    xoff = 16 - R               # raw column of padded column 0
+    XR = (xoff + X + g - 1) // g * g
+
+    def span(lo, hi):  # raw columns of the granules covering padded columns [lo, hi)
+        lo, hi = max(lo, 0), min(hi, X)
+        return (xoff + lo) // g * g, -(-(xoff + hi) // g) * g
+
+    ext, foot = 0, 0
+    items = ntx * nty
+    for r0 in range(0, items, conc):
+        mc = np.zeros((Y, XR), bool)
+        mv = np.zeros((Y, XR), bool)
+        for t in range(r0, min(items, r0 + conc)):
+            by, rem = divmod(t, ntx * bh)
+            h = min(bh, nty - by * bh)
+            bx, rem2 = divmod(rem, bw * h)
+            w = min(bw, ntx - bx * bw)
+            tx, ty = bx * bw + rem2 % w, by * bh + rem2 // w
+            x0, y0 = R + tx * OX - H, R + ty * OY - H
+            a, b = span(x0, x0 + ext_tile[0])
+            mc[max(y0, 0):y0 + ext_tile[1], a:b] = True
+            fx, fy = x0 - (foot_tile[0] - ext_tile[0]) // 2, y0 - (foot_tile[1] - ext_tile[1]) // 2
+            a, b = span(fx, fx + foot_tile[0])
+            mv[max(fy, 0):fy + foot_tile[1], a:b] = True
+        ext += int(mc.sum())
+        foot += int((mv | mc).sum())
+    cells = nx * ny
+    zpad = (nz + 2 * R) / nz
+    return (zpad * (8 * NC * ext + 8 * foot) + 8 * cells * (2 if kind in WAVE_KINDS and bt >= 2 else 1)) / (bt * cells)
 
 
 # ---------------------------------------------------------------------------------------------------------

@@ -1,5 +1,9 @@
 """The performance model (paper_1410_3060_b200/model.py) against the numbers PAPER.md prints (SURVEY.md §4
 item 2) and the GPU code balances DESIGN.md derives."""
+import json
+import os
+import re
+
 import pytest
 
 from paper_1410_3060_b200 import model as m
@@ -41,8 +45,6 @@ def test_fp64_bound_takes_over():
 
 
 # ------------------------------------------------------------------ footprint model
-import os
-import re
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 KINDS = {"K7C": m.K7C, "K7V": m.K7V, "K25W": m.K25W, "K25V": m.K25V, "K25WA": m.K25WA}
@@ -109,3 +111,33 @@ def test_l2_retention():
     # per z-step, so the 126 MiB L2 holds ~19 steps of them
     assert m.l2_retention_steps((24, 16), 2, m.K25V) == pytest.approx(126 * 2 ** 20 / (148 * 384 * 120))
     assert m.l2_retention_steps((24, 32), 2, m.K25V) == pytest.approx(m.l2_retention_steps((24, 16), 2, m.K25V) / 2)
+
+
+def test_lockstep_dram_model_single_round_is_compulsory_plus_ghosts():
+    # one round covering every tile, byte granules: each padded cell of every field crosses DRAM once
+    n, R = 64, 4
+    X = n + 2 * R
+    got = m.lockstep_dram_bytes_per_lup(m.K25V, 2, (n, n, n), (24, 16), conc=10 ** 6, granule=8)
+    want = ((n + 2 * R) / n * (8 * 13 * X * X + 8 * X * X) + 8 * n * n) / (2 * n * n)
+    assert abs(got - want) < 1e-9
+    # rounds of fewer tiles re-read the halos at their patch boundaries; coarser granules add partial lines
+    small = m.lockstep_dram_bytes_per_lup(m.K25V, 2, (n, n, n), (24, 16), conc=4, granule=8)
+    assert small > got
+    assert m.lockstep_dram_bytes_per_lup(m.K25V, 2, (n, n, n), (24, 16), conc=4, granule=128) > small
+
+
+def test_lockstep_dram_model_reproduces_ncu():
+    # the model with 148 concurrent tiles and 128-byte lines against ncu's DRAM bytes per update of the
+    # default plans (profiles/traffic.json, one launch each): the two-level 25v kernel to 0.5 %, the generic
+    # pipe kernel (C2 bt = 4, C3 bt = 1) to 3 %
+    t = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+    cases = [("C4-25pt-var-512/bt2", m.K25V, 2, 512, (24, 16), 0.005),
+             ("C5-25pt-var-1024/bt2", m.K25V, 2, 1024, (24, 16), 0.005),
+             ("C2-7pt-var-512/bt4", m.K7V, 4, 512, (26, 22), 0.03),
+             ("C3-25pt-wave-512/bt1", m.K25W, 1, 512, (64, 14), 0.03)]
+    for key, kind, bt, n, tile, tol in cases:
+        e = t[key]
+        meas = e["dram_bytes_per_lup"] if isinstance(e, dict) else e / (n ** 3 * bt)
+        mod = m.lockstep_dram_bytes_per_lup(kind, bt, (n, n, n), tile)
+        assert abs(mod - meas) / meas < tol, (key, mod, meas)
+        assert mod > m.code_balance(kind, bt)
