@@ -61,6 +61,14 @@ struct KParams {
   int skew_ns;         // pipe25 experiment (STENCIL_SKEW_NS): checkerboard-odd tiles start an item later
   int l2h;             // pipe25 experiment (STENCIL_L2H): L2 priorities of boxes A/B/C, 2 bits each
                        // (0 = no hint, 1 = evict_first, 2 = evict_last, 3 = evict_normal)
+  // pipe25 skewed tiles (SKEW): the level-1 rows a tile hands to the tile above go through
+  // xch (a state-sized buffer, offset like dst; xch_raw its allocation base); xflag[2 * item slot + w] =
+  // xbase + q + 1 once exporting warp w stored plane q (xflag_n entries); xbase grows by 65536 per launch
+  double* xch;
+  const double* xch_raw;
+  unsigned int* xflag;
+  long long xflag_n;
+  unsigned int xbase;
   int walign;  // pipe kernel: tiles write sector-aligned output segments (STENCIL_WALIGN=1; default 0:
                // measured slower under the power cap for OX % 4 != 0, profiles/r01_summary.md)
 };
@@ -93,6 +101,9 @@ int max_pipe_bt(int kind);
 
 // The 25-point variable-coefficient kind with two fused levels (pipe25.cu): same contract as
 // launch_pipe for (K25V, b = 2); cfg selects a tile configuration (0 = default).
+// tile_cfg entries of launch_pipe25v2 with skewed tiles (they need KParams::xch / xflag)
+bool pipe25v2_skewed(int cfg);
+long long pipe25v2_flag_slots(int cfg, int nx, int ny, int zl);
 cudaError_t launch_pipe25v2(const KParams& p, int zchunk_req, int num_sms, int cfg, cudaStream_t stream,
                             LaunchInfo* info);
 // The 25-point wave with two fused levels (pipe25.cu): contract of launch_pipe for (K25W, b = 2).

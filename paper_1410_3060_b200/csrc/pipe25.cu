@@ -51,7 +51,7 @@
 
 namespace st {
 
-template <int KIND, int TX, int TY, int D, int CLU>
+template <int KIND, int TX, int TY, int D, int CLU, int SKEW>
 struct P25Cfg {
   // KIND = K25V (Fig. 1d, 13 coefficient fields) or K25W (Fig. 1e with a scalar alpha: box C carries
   // Omega^{t-1} instead of coefficients, and the carried state has no z-coefficients)
@@ -62,14 +62,20 @@ struct P25Cfg {
   static constexpr int NCONS = LPR * (TY / CY);   // consumer threads
   static constexpr int NW = NCONS / 32;           // consumer warps
   static constexpr int THREADS = NCONS + 32;      // + the producer warp
-  static constexpr int OX = TX - 2 * R;           // output columns of a tile
-  static constexpr int OYP = CLU * TY - 2 * R;    // output rows of a (cluster) tile
+  // SKEW (parallelogram tiles in y): level 2 runs R rows below level 1 instead of
+  // shrinking, so y-neighbouring tiles never compute the same cell; the 2R level-1 rows below the tile
+  // come from the tile underneath through global memory (box I), and box C reaches R rows lower (CR)
+  static constexpr int CR = SKEW ? R : 0;
+  static constexpr int OX = TX - 2 * R;                     // output columns of a tile
+  static constexpr int OYP = SKEW ? TY : CLU * TY - 2 * R;  // output rows of a (cluster) tile
   static constexpr int FX = TX + 2 * R, FY = TY + 2 * R;  // box B (level-1 footprint)
-  static constexpr int AEL = TX * TY, BEL = FX * FY, CFIELD = TX * TY, CEL = CF * CFIELD;
+  static constexpr int AEL = TX * TY, BEL = FX * FY, CFIELD = TX * (TY + CR), CEL = CF * CFIELD;
+  static constexpr int IEL = SKEW ? 2 * R * TX : 0;       // box I: level-1 rows -2R..-1 of plane q
   static constexpr int BOFF = (AEL + 15) / 16 * 16, COFF = BOFF + (BEL + 15) / 16 * 16;
-  static constexpr int SLOT = COFF + (CEL + 15) / 16 * 16;  // doubles per ring slot (128-byte aligned parts)
+  static constexpr int IOFF = COFF + (CEL + 15) / 16 * 16;
+  static constexpr int SLOT = IOFF + (IEL + 15) / 16 * 16;  // doubles per ring slot (128-byte aligned parts)
   static constexpr int PEL = TX * TY;                       // one shared level-1 plane
-  static constexpr int NPB = 3;                             // level-1 planes kept (boundary warps read q-1)
+  static constexpr int NPB = SKEW ? 2 : 3;                  // level-1 planes kept (boundary warps read q-1)
   static constexpr int RXEL = R * TX;                       // one pushed boundary strip (R rows)
   static constexpr int NRX = CLU > 1 ? 4 : 0;               // receive slots per side
   static constexpr int STASH = CLU > 1 ? 2 * 32 * NCELL * 5 : 0;  // boundary warps' carried x chain + Wy
@@ -78,7 +84,9 @@ struct P25Cfg {
   static constexpr bool HELPER = CLU == 2;
   static constexpr int MBOX = HELPER ? 2 * 32 * NCELL : 0;
   static constexpr int WROWS = 32 / LPR * CY;               // E1 rows per consumer warp
-  static constexpr uint32_t TX_BYTES_A = AEL * 8, TX_BYTES_B = BEL * 8, TX_BYTES_C = CEL * 8, RX_BYTES = RXEL * 8;
+  static constexpr uint32_t TX_BYTES_A = AEL * 8, TX_BYTES_B = BEL * 8, TX_BYTES_C = CEL * 8, RX_BYTES = RXEL * 8,
+                            TX_BYTES_I = IEL * 8;
+  static constexpr int XROW0 = TY - 2 * R;  // SKEW: the tile's level-1 rows the tile above imports
   static constexpr size_t SMEM = 8 * ((size_t)D * SLOT + (size_t)NPB * PEL + 2 * (size_t)NRX * RXEL + STASH + MBOX) +
                                  8 * (2 * D + 8 + 2 * NRX + 8) + 4 * 8 + 128;
   static_assert(TX % 16 == 0 && TY % CY == 0 && NCONS % 32 == 0 && 32 % LPR == 0, "thread layout");
@@ -86,6 +94,8 @@ struct P25Cfg {
   static_assert(OX > 0 && TY > 2 * R && (OX & 3) == 0, "output tile (whole 32-byte sectors per row)");
   static_assert(CLU == 1 || CLU == 2 || CLU == 4, "clusters of 1, 2 or 4 CTAs along y");
   static_assert(!WAVE || CLU == 1, "wave: single-CTA tiles");
+  static_assert(!SKEW || (CLU == 1 && !WAVE && TY >= 4 * R && (2 * R) % WROWS == 0),
+                "skewed tiles: single CTA, 25v; the exporting rows are whole warps");
   static_assert(KIND == K25V || KIND == K25W, "25-point kinds");
   // TMEM (512 columns x 128 lanes; warp w reaches lanes 32*(w%4)..): warp w uses columns
   // [256*(w/4), +256): at most two warps per lane quadrant.
@@ -154,11 +164,12 @@ __device__ __forceinline__ void v0ring_st(uint32_t t, const uint32_t (&w)[28]) {
   }
 }
 
-template <int KIND, int TX, int TY, int D, int CLU>
-__global__ void __launch_bounds__(P25Cfg<KIND, TX, TY, D, CLU>::THREADS, 1)
+template <int KIND, int TX, int TY, int D, int CLU, int SKEW>
+__global__ void __launch_bounds__(P25Cfg<KIND, TX, TY, D, CLU, SKEW>::THREADS, 1)
     pipe25_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
-                  const __grid_constant__ CUtensorMap mapC, const KParams p, int ntx, int nty, int items) {
-  using C = P25Cfg<KIND, TX, TY, D, CLU>;
+                  const __grid_constant__ CUtensorMap mapC, const __grid_constant__ CUtensorMap mapI,
+                  const __grid_constant__ CUtensorMap mapS, const KParams p, int ntx, int nty, int items) {
+  using C = P25Cfg<KIND, TX, TY, D, CLU, SKEW>;
   constexpr int R = C::R, NC = C::NC, NCONS = C::NCONS, FX = C::FX, CX = C::CX, CY = C::CY, NW = C::NW;
   constexpr bool WAVE = C::WAVE;
 
@@ -207,6 +218,10 @@ __global__ void __launch_bounds__(P25Cfg<KIND, TX, TY, D, CLU>::THREADS, 1)
       asm volatile("prefetch.tensormap [%0];" ::"l"(&mapA) : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"(&mapB) : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"(&mapC) : "memory");
+      if constexpr (SKEW) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&mapI) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&mapS) : "memory");
+      }
       uint32_t iv = 0;
       const uint64_t polA = l2_policy(p.l2h & 3), polB = l2_policy((p.l2h >> 2) & 3),
                      polC = l2_policy((p.l2h >> 4) & 3);
@@ -250,7 +265,16 @@ __global__ void __launch_bounds__(P25Cfg<KIND, TX, TY, D, CLU>::THREADS, 1)
         if (g < 0) break;
         const bool skip = (p.dbg & 8) && g == 0;  // fault injection: item 0 never loaded (nor computed)
         Item it = decode<R, 1, C::OX, C::OYP>(g, ntx, nty, p);
-        it.gy0 += (int)crank * TY;
+        it.gy0 += (int)crank * TY + C::CR;  // SKEW: level-1 rows [R + ty*TY, +TY), level 2 R rows lower
+        // SKEW: the flags of this tile (two exporting warps) and of the tile underneath
+        const long long fme = 2ll * (((long long)it.zc * nty + it.ty) * ntx + it.tx);
+        const long long fbelow = fme - 2ll * ntx;
+        if constexpr (SKEW) {
+          if (skip) {  // fault injection: the skipped item still releases the tile above (wrong planes, no hang)
+            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p.xflag + fme), "r"(p.xbase + 0xFFFFu) : "memory");
+            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p.xflag + fme + 1), "r"(p.xbase + 0xFFFFu) : "memory");
+          }
+        }
         if (p.skew_ns > 0 && (((it.gx0 / C::OX) + (it.gy0 / C::OYP)) & 1)) {  // experiment: offset neighbours
           for (int w = 0; w < p.skew_ns; w += 1000) __nanosleep(1000);
         }
@@ -264,8 +288,33 @@ __global__ void __launch_bounds__(P25Cfg<KIND, TX, TY, D, CLU>::THREADS, 1)
           const int q = s - R;
           const bool needB = q >= it.s_begin;
           const bool need1 = needB && (it.s_begin == 0 || q >= it.s_begin + R);
-          mbar_expect_tx(&full[sl], C::TX_BYTES_A + (needB ? C::TX_BYTES_B : 0u) + (need1 ? C::TX_BYTES_C : 0u));
+          // SKEW: level 1's rows -2R..-1 of plane q, from the tile underneath (or the ghost rows, bottom tile)
+          const bool needI = SKEW && needB && q >= 0 && q < p.zl;
+          mbar_expect_tx(&full[sl], C::TX_BYTES_A + (needB ? C::TX_BYTES_B : 0u) + (need1 ? C::TX_BYTES_C : 0u) +
+                                        (needI ? C::TX_BYTES_I : 0u));
           double* slot = ring + (size_t)sl * C::SLOT;
+          if constexpr (SKEW) {
+            if (needI) {
+              if (it.ty > 0) {
+                // wait until both exporting warps of the tile underneath stored plane q (bounded: a lost
+                // producer makes wrong planes, not a hung GPU)
+                const unsigned int want = p.xbase + (unsigned int)q + 1u;
+                for (int w = 0; w < 2; ++w) {
+                  unsigned int v;
+                  for (long long spin = 0; spin < (1ll << 26); ++spin) {
+                    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p.xflag + fbelow + w) : "memory");
+                    if ((int)(v - want) >= 0) break;
+                    __nanosleep(64);
+                  }
+                }
+                // the generic-proxy stores just observed must be visible to the TMA (async proxy) load
+                asm volatile("fence.proxy.async.global;" ::: "memory");
+                tma_load_3d(slot + C::IOFF, &mapI, &full[sl], xa, it.gy0 - 2 * R, q);
+              } else {
+                tma_load_3d(slot + C::IOFF, &mapS, &full[sl], xa, it.gy0 - 2 * R, q);  // ghost rows of plane q
+              }
+            }
+          }
           // (STENCIL_DBG bit 16, a DRAM-traffic diagnostic with wrong results: box B re-reads plane s)
           const int qb = (p.dbg & 16) ? s : q;
           if (p.l2h == 0) {
@@ -273,14 +322,14 @@ __global__ void __launch_bounds__(P25Cfg<KIND, TX, TY, D, CLU>::THREADS, 1)
             if (needB) tma_load_3d(slot + C::BOFF, &mapB, &full[sl], xb, it.gy0 - R, qb);
             if (need1) {
               if constexpr (WAVE) tma_load_3d(slot + C::COFF, &mapC, &full[sl], xa, it.gy0, q);  // Omega^{t-1}
-              else tma_load_4d(slot + C::COFF, &mapC, &full[sl], xa, it.gy0, q, 0);
+              else tma_load_4d(slot + C::COFF, &mapC, &full[sl], xa, it.gy0 - C::CR, q, 0);
             }
           } else {  // experiment: L2 eviction priorities per box
             tma_load_3d_hint(slot, &mapA, &full[sl], xa, it.gy0, s, polA);
             if (needB) tma_load_3d_hint(slot + C::BOFF, &mapB, &full[sl], xb, it.gy0 - R, qb, polB);
             if (need1) {
               if constexpr (WAVE) tma_load_3d_hint(slot + C::COFF, &mapC, &full[sl], xa, it.gy0, q, polC);
-              else tma_load_4d_hint(slot + C::COFF, &mapC, &full[sl], xa, it.gy0, q, 0, polC);
+              else tma_load_4d_hint(slot + C::COFF, &mapC, &full[sl], xa, it.gy0 - C::CR, q, 0, polC);
             }
           }
           if (p.pfd > 0 && s + p.pfd <= it.s_end) {  // warm L2 for the loads pfd steps ahead (beyond the ring)
@@ -323,12 +372,14 @@ __global__ void __launch_bounds__(P25Cfg<KIND, TX, TY, D, CLU>::THREADS, 1)
   const int x0 = (tid % C::LPR) * CX;   // first E1 column of this thread's 2x2 block
   const int ly0 = (tid / C::LPR) * CY;  // first E1 row
   // level-2 rows of this CTA (the trapezoid shrinks by R only at the cluster's outer rows)
-  const int ylo = crank == 0 ? R : 0, yhi = crank == (uint32_t)CLU - 1 ? TY - R : TY;
+  const int ylo = SKEW ? -R : (crank == 0 ? R : 0), yhi = SKEW ? TY - R : (crank == (uint32_t)CLU - 1 ? TY - R : TY);
   const int wr0 = warp * C::WROWS;  // the warp's first row (warp-uniform)
   // level 2 runs on the warps whose rows hold output cells, on the same 2x2 blocks as level 1 (an
   // output-only mapping measured no faster)
-  const bool lvl2 = wr0 + C::WROWS > ylo && wr0 < yhi;
-  const int l2x = x0, l2y = ly0;
+  // (SKEW: every warp; a thread's level-2 cells sit R rows below its level-1 cells)
+  const bool lvl2 = SKEW || (wr0 + C::WROWS > ylo && wr0 < yhi);
+  const int l2x = x0, l2y = ly0 - C::CR;
+  const bool exporter = SKEW && ly0 >= C::XROW0;  // SKEW: level-1 rows the tile above imports
   const bool topB = CLU > 1 && warp == 0 && crank > 0;                        // needs rows of rank - 1
   const bool botB = CLU > 1 && warp == NW - 1 && crank < (uint32_t)CLU - 1;  // needs rows of rank + 1
   const bool bnd = topB || botB;
@@ -351,7 +402,8 @@ __global__ void __launch_bounds__(P25Cfg<KIND, TX, TY, D, CLU>::THREADS, 1)
     if (g < 0) break;
     if ((p.dbg & 8) && g == 0) continue;  // fault injection: work item 0 never computed
     Item it = decode<R, 1, C::OX, C::OYP>(g, ntx, nty, p);
-    it.gy0 += (int)crank * TY;
+    it.gy0 += (int)crank * TY + C::CR;
+    const long long fme = 2ll * (((long long)it.zc * nty + it.ty) * ntx + it.tx);
     bool act1[CY][CX], outc[CY][CX];
     long long col[CY];
 #pragma unroll
@@ -404,7 +456,7 @@ __global__ void __launch_bounds__(P25Cfg<KIND, TX, TY, D, CLU>::THREADS, 1)
           for (int i = 0; i < CX; ++i) xr[R + i] = ys[R + j][i];
           double Wr[NC > 0 ? NC : 1][CX];
 #pragma unroll
-          for (int f = 0; f < NC; ++f) lds_row<CX, true>(Cs + f * C::CFIELD + (ly0 + j) * TX + x0, Wr[f]);
+          for (int f = 0; f < NC; ++f) lds_row<CX, true>(Cs + f * C::CFIELD + (ly0 + j + C::CR) * TX + x0, Wr[f]);
           double urow[CX];  // the wave: Omega^{t-1} of plane q (box C)
           if constexpr (WAVE) lds_row<CX, true>(Cs + (ly0 + j) * TX + x0, urow);
           auto V0 = [&](int k, int i) -> double {  // plane s - 8 + k of cell (j, i)
@@ -448,6 +500,29 @@ __global__ void __launch_bounds__(P25Cfg<KIND, TX, TY, D, CLU>::THREADS, 1)
       double* P = sP + (size_t)(iv % C::NPB) * C::PEL;  // rotates with the CTA's step counter (pipe.cu)
 #pragma unroll
       for (int j = 0; j < CY; ++j) sts_row<CX, true>(P + (ly0 + j) * TX + x0, v1[j]);
+      if constexpr (SKEW) {
+        // hand the top 2R level-1 rows of plane q to the tile above (plain stores: they should stay in L2
+        // for its import a few steps later), then release them warp by warp
+        if (exporter && q >= it.s_begin && q >= 0 && q < p.zl) {
+#pragma unroll
+          for (int j = 0; j < CY; ++j) {
+            const int gy = it.gy0 + ly0 + j;
+            if (gy >= p.ny + 2 * R) continue;
+            double* dx = p.xch + (long long)q * p.plane + (long long)gy * p.pitch + it.gx0 + x0;
+#pragma unroll
+            for (int i = 0; i < CX; ++i) {
+              const int gx = it.gx0 + x0 + i;
+              if (gx >= 0 && gx < p.nx + 2 * R) dx[i] = v1[j][i];
+            }
+          }
+          __syncwarp();
+          if (lane == 0) {
+            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p.xflag + fme + (warp - C::XROW0 / C::WROWS)),
+                         "r"(p.xbase + (unsigned int)q + 1u)
+                         : "memory");
+          }
+        }
+      }
       if constexpr (CLU > 1) {
         // the push of two steps ago has read its rows before this barrier releases their rewrite (the
         // plane is rewritten NPB = 3 steps after it was pushed)
@@ -483,8 +558,13 @@ __global__ void __launch_bounds__(P25Cfg<KIND, TX, TY, D, CLU>::THREADS, 1)
         if (!bnd) {
 #pragma unroll
           for (int r = 0; r < CY + 2 * R; ++r) {
-            const int row = min(max(l2y - R + r, 0), TY - 1);  // rows outside E1 only feed discarded cells
-            lds_row<CX, true>(P + row * TX + l2x, ys[r]);
+            if constexpr (SKEW) {  // rows below the tile: box I (level-1 rows -2R..-1 of plane q)
+              const int row = l2y - R + r;
+              lds_row<CX, true>((row < 0 ? slot + C::IOFF + (row + 2 * R) * TX : P + row * TX) + l2x, ys[r]);
+            } else {
+              const int row = min(max(l2y - R + r, 0), TY - 1);  // rows outside E1 only feed discarded cells
+              lds_row<CX, true>(P + row * TX + l2x, ys[r]);
+            }
           }
         } else if constexpr (CLU > 1 && !C::HELPER) {
           // the y chain of plane q-1, one step late: level-1 plane q-1 and the neighbour's rows of it,
@@ -534,14 +614,15 @@ __global__ void __launch_bounds__(P25Cfg<KIND, TX, TY, D, CLU>::THREADS, 1)
           double Pq[CX];  // x/y half of plane q (boundary warps: its x chain goes to the stash)
           {
             double xr[R + CX + R];
-            lds_row<R, true>(P + (l2y + j) * TX + l2x - R, xr);
-            lds_row<R, true>(P + (l2y + j) * TX + l2x + CX, xr + R + CX);
+            const double* prow = (SKEW && l2y + j < 0) ? slot + C::IOFF + (l2y + j + 2 * R) * TX : P + (l2y + j) * TX;
+            lds_row<R, true>(prow + l2x - R, xr);
+            lds_row<R, true>(prow + l2x + CX, xr + R + CX);
 #pragma unroll
             for (int i = 0; i < CX; ++i) xr[R + i] = vc[j][i];
             double Wr[NC > 0 ? NC : 1][CX];
 #pragma unroll
             for (int f = 0; f < NC; ++f)
-              if (f % 3 != 0 || f == 0) lds_row<CX, true>(Cs + f * C::CFIELD + (l2y + j) * TX + l2x, Wr[f]);
+              if (f % 3 != 0 || f == 0) lds_row<CX, true>(Cs + f * C::CFIELD + (l2y + j + C::CR) * TX + l2x, Wr[f]);
 #pragma unroll
             for (int i = 0; i < CX; ++i) {
               double m[3][R], pl[3][R], W[NC > 0 ? NC : 1];
@@ -574,7 +655,8 @@ __global__ void __launch_bounds__(P25Cfg<KIND, TX, TY, D, CLU>::THREADS, 1)
           double Wz[4][CX];  // z coefficients of plane q, carried for its chain
           if constexpr (!WAVE) {
 #pragma unroll
-            for (int r = 1; r <= 4; ++r) lds_row<CX, true>(Cs + 3 * r * C::CFIELD + (l2y + j) * TX + l2x, Wz[r - 1]);
+            for (int r = 1; r <= 4; ++r)
+              lds_row<CX, true>(Cs + 3 * r * C::CFIELD + (l2y + j + C::CR) * TX + l2x, Wz[r - 1]);
           }
           double vout[CX], uout[CX];
 #pragma unroll
@@ -741,10 +823,10 @@ __global__ void __launch_bounds__(P25Cfg<KIND, TX, TY, D, CLU>::THREADS, 1)
 
 namespace {
 
-template <int KIND, int TX, int TY, int D, int CLU>
+template <int KIND, int TX, int TY, int D, int CLU, int SKEW>
 cudaError_t run_pipe25(const KParams& p0, int zchunk_req, int num_sms, cudaStream_t stream, LaunchInfo* info) {
-  using C = P25Cfg<KIND, TX, TY, D, CLU>;
-  auto kern = pipe25_kernel<KIND, TX, TY, D, CLU>;
+  using C = P25Cfg<KIND, TX, TY, D, CLU, SKEW>;
+  auto kern = pipe25_kernel<KIND, TX, TY, D, CLU, SKEW>;
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
@@ -758,7 +840,8 @@ cudaError_t run_pipe25(const KParams& p0, int zchunk_req, int num_sms, cudaStrea
   if (planes <= 0) return cudaSuccess;
   if (p.xoff != 16 - C::R) return cudaErrorInvalidValue;  // decode() assumes interior column R at raw 16
   const int dx = p.walign ? 0 : (p.xoff & 1);  // decode<R, 1, ...>'s shift
-  const int ntx = (p.nx + dx + C::OX - 1) / C::OX, nty = (p.ny + C::OYP - 1) / C::OYP;
+  // (SKEW: level-2 rows of tile ty are [ty*TY, (ty+1)*TY) in padded rows; interior rows end at ny + R)
+  const int ntx = (p.nx + dx + C::OX - 1) / C::OX, nty = (p.ny + C::CR + C::OYP - 1) / C::OYP;
   const long long tiles = (long long)ntx * nty;
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute attr[1];
@@ -794,15 +877,24 @@ cudaError_t run_pipe25(const KParams& p0, int zchunk_req, int num_sms, cudaStrea
   const int nzc = (planes + zchunk - 1) / zchunk;
   p.nzc = nzc;
   const long long items = tiles * nzc;
-  CUtensorMap mapA, mapB, mapC;
+  CUtensorMap mapA, mapB, mapC, mapI, mapS;
   const int X0 = p.xoff & ~1;
   const long long MX = p.xoff + p.nx + 2 * C::R - X0, MY = p.ny + 2 * C::R;
   if (!make_tensor_map(&mapA, p.src_raw + X0, 3, p.pitch, MX, MY, p.zl, 1, p.plane, 0, TX, TY, 1) ||
       !make_tensor_map(&mapB, p.src_raw + X0, 3, p.pitch, MX, MY, p.zl, 1, p.plane, 0, C::FX, C::FY, 1) ||
       !(C::WAVE ? make_tensor_map(&mapC, p.srcu_raw + X0, 3, p.pitch, MX, MY, p.zl, 1, p.plane, 0, TX, TY, 1)
-                : make_tensor_map(&mapC, p.coef_raw + X0, 4, p.pitch, MX, MY, p.zl, C::NC, p.plane, p.cstride, TX, TY,
-                                  C::NC)))
+                : make_tensor_map(&mapC, p.coef_raw + X0, 4, p.pitch, MX, MY, p.zl, C::NC, p.plane, p.cstride, TX,
+                                  TY + C::CR, C::NC)))
     return cudaErrorInvalidValue;
+  mapI = mapA;
+  mapS = mapA;
+  if constexpr (SKEW != 0) {
+    // box I: 2R level-1 rows below the tile, from the exchange buffer (or the ghost rows of Omega^t)
+    if (!p.xch_raw || !p.xflag || p.xflag_n < 2 * items) return cudaErrorInvalidValue;
+    if (!make_tensor_map(&mapI, p.xch_raw + X0, 3, p.pitch, MX, MY, p.zl, 1, p.plane, 0, TX, 2 * C::R, 1) ||
+        !make_tensor_map(&mapS, p.src_raw + X0, 3, p.pitch, MX, MY, p.zl, 1, p.plane, 0, TX, 2 * C::R, 1))
+      return cudaErrorInvalidValue;
+  }
   const int grid = (int)std::min<long long>(items, clusters) * CLU;
   static const int pfd_env = getenv("STENCIL_PF") ? atoi(getenv("STENCIL_PF")) : 0;
   p.pfd = pfd_env;  // L2 prefetch distance in steps (0 = none)
@@ -827,10 +919,10 @@ cudaError_t run_pipe25(const KParams& p0, int zchunk_req, int num_sms, cudaStrea
     p.tblk_h = std::max(1, (conc + bw - 1) / bw);
   }
   if constexpr (CLU == 1) {
-    kern<<<grid, C::THREADS, C::SMEM, stream>>>(mapA, mapB, mapC, p, ntx, nty, (int)items);
+    kern<<<grid, C::THREADS, C::SMEM, stream>>>(mapA, mapB, mapC, mapI, mapS, p, ntx, nty, (int)items);
   } else {
     cfg.gridDim = dim3(grid);
-    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, mapA, mapB, mapC, p, ntx, nty, (int)items);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, mapA, mapB, mapC, mapI, mapS, p, ntx, nty, (int)items);
     if (e != cudaSuccess) return e;
   }
   if (info) {
@@ -849,10 +941,22 @@ cudaError_t launch_pipe25v2(const KParams& p, int zchunk_req, int num_sms, int c
   // Measured on B200 (C4, sustained, profiles/r02_summary.md): the single-CTA tile is the fastest; the
   // cluster tiles move 15 % fewer L2->SM bytes but stall on their boundary warps (ncu: barrier stalls).
   switch (cfg) {
-    case 1: return run_pipe25<K25V, 32, 20, 2, 2>(p, zchunk_req, num_sms, stream, info);   // cluster pair: 24 x 32
-    case 2: return run_pipe25<K25V, 32, 20, 2, 4>(p, zchunk_req, num_sms, stream, info);   // cluster of 4: 24 x 72
-    default: return run_pipe25<K25V, 32, 24, 2, 1>(p, zchunk_req, num_sms, stream, info);  // single CTA: 24 x 16
+    case 1: return run_pipe25<K25V, 32, 20, 2, 2, 0>(p, zchunk_req, num_sms, stream, info);   // cluster pair: 24 x 32
+    case 2: return run_pipe25<K25V, 32, 20, 2, 4, 0>(p, zchunk_req, num_sms, stream, info);   // cluster of 4: 24 x 72
+    case 3: return run_pipe25<K25V, 32, 20, 2, 1, 1>(p, zchunk_req, num_sms, stream, info);   // skewed: 24 x 20
+    default: return run_pipe25<K25V, 32, 24, 2, 1, 0>(p, zchunk_req, num_sms, stream, info);  // single CTA: 24 x 16
   }
+}
+
+// tile_cfg entries of launch_pipe25v2 that hand level-1 rows between tiles (the runtime then provides
+// KParams::xch / xflag)
+bool pipe25v2_skewed(int cfg) { return cfg == 3; }
+// flag entries a skewed launch may need on an nx x ny x zl slab (2 per item, at most zl z-chunks)
+long long pipe25v2_flag_slots(int cfg, int nx, int ny, int zl) {
+  if (!pipe25v2_skewed(cfg)) return 0;
+  using C = P25Cfg<K25V, 32, 20, 2, 1, 1>;
+  const long long ntx = (nx + 1 + C::OX - 1) / C::OX, nty = (ny + C::CR + C::OYP - 1) / C::OYP;
+  return 2 * ntx * nty * std::max(1, zl);
 }
 
 // The 25-point wave (Fig. 1e, scalar alpha) with two fused levels: no coefficient fields, so a bigger
@@ -861,7 +965,7 @@ cudaError_t launch_pipe25v2(const KParams& p, int zchunk_req, int num_sms, int c
 cudaError_t launch_pipe25w2(const KParams& p, int zchunk_req, int num_sms, int cfg, cudaStream_t stream,
                             LaunchInfo* info) {
   switch (cfg) {
-    default: return run_pipe25<K25W, 32, 32, 4, 1>(p, zchunk_req, num_sms, stream, info);  // 24 x 24
+    default: return run_pipe25<K25W, 32, 32, 4, 1, 0>(p, zchunk_req, num_sms, stream, info);  // 24 x 24
   }
 }
 

@@ -137,6 +137,7 @@ struct Slab {
   int64_t own_z0 = 0, own_z1 = 0, store_z0 = 0, store_z1 = 0, zl = 0, lo = 0, hi = 0;
   double* buf[4] = {nullptr, nullptr, nullptr, nullptr};  // raw (un-offset) state buffers
   double* coef = nullptr;                                  // raw coefficient slab
+  double* xch = nullptr;  // skewed 25v tiles: level-1 rows handed between tiles (raw, lazily allocated)
 };
 
 }  // namespace
@@ -164,6 +165,9 @@ struct stencil_ctx {
   double scal[6] = {0, 0, 0, 0, 0, 0};
   unsigned int* sched = nullptr;  // pipe kernel work counters (zero between launches)
   unsigned int* done = nullptr;   // per-item completion counters of multi-block launches (lazy)
+  unsigned int* xflag = nullptr;  // skewed 25v tiles: per-item export flags (lazy), xflag_n entries
+  long long xflag_n = 0;
+  unsigned int xbase = 0;         // flag base of the last skewed launch (+65536 per launch)
 
   std::vector<std::pair<void*, size_t>> allocs;
   int64_t steps = 0;
@@ -710,6 +714,36 @@ void peer_targets(stencil_ctx* h, const Slab& s, int d0, int d1, st::KParams& p)
   p.rfence = h->ipc ? 1 : 0;
 }
 
+// Skewed two-level 25v tiles (pipe25.cu): the slab's exchange buffer (one state-sized
+// array: a tile stores its top 2R level-1 rows of every plane there for the tile above) and the per-item
+// flags, allocated at the first such launch; a fresh flag base per launch.
+int skew_params(stencil_ctx* h, Slab& s, st::KParams& p) {
+  if (!s.xch) {
+    const size_t bytes = (size_t)h->plane * (size_t)s.zl * sizeof(double);
+    s.xch = (double*)dev_alloc(h, bytes);
+    if (!s.xch) { set_err("device allocation of %zu bytes failed (skewed-tile exchange buffer)", bytes); return ST_E_NOMEM; }
+  }
+  const long long need = st::pipe25v2_flag_slots(h->tile_cfg, (int)h->nx, (int)h->ny, (int)s.zl);
+  if (h->xflag_n < need) {
+    h->xflag = (unsigned int*)dev_alloc(h, (size_t)need * sizeof(unsigned int));
+    if (!h->xflag) { set_err("device allocation failed (skewed-tile flags)"); return ST_E_NOMEM; }
+    h->xflag_n = need;
+    h->xbase = 0;
+    CK(cudaMemsetAsync(h->xflag, 0, (size_t)need * sizeof(unsigned int), h->stream), "zero skewed-tile flags");
+  }
+  h->xbase += 65536u;
+  if (h->xbase == 0) {  // wrapped: no flag may look newer than the next launch's base
+    CK(cudaMemsetAsync(h->xflag, 0, (size_t)h->xflag_n * sizeof(unsigned int), h->stream), "zero skewed-tile flags");
+    h->xbase = 65536u;
+  }
+  p.xch = s.xch + h->xoff;
+  p.xch_raw = s.xch;
+  p.xflag = h->xflag;
+  p.xflag_n = h->xflag_n;
+  p.xbase = h->xbase;
+  return ST_OK;
+}
+
 // Launch the kernel of the handle's variant for b levels over output planes [z0, z1) (global padded
 // indices) of slab s; peer = also store the neighbours' halo planes into their buffers.
 int launch_range(stencil_ctx* h, Slab& s, int b, int d0, int d1, int64_t z0, int64_t z1, bool peer = false) {
@@ -724,6 +758,10 @@ int launch_range(stencil_ctx* h, Slab& s, int b, int d0, int d1, int64_t z0, int
   p.dstu = d1 >= 0 ? h->at(s, d1) : nullptr;
   p.src_raw = s.buf[h->lv0];
   p.srcu_raw = s.buf[h->lv1];
+  if (h->variant == ST_VARIANT_PIPE && h->kind == ST_25PT_VAR && b == 2 && st::pipe25v2_skewed(h->tile_cfg)) {
+    const int rc = skew_params(h, s, p);
+    if (rc) return rc;
+  }
   cudaEvent_t ev_end = nullptr;
   cudaEvent_t ev_begin = timing_begin(h, &ev_end);
   cudaError_t e;

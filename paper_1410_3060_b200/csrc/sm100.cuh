@@ -79,6 +79,7 @@ __device__ __forceinline__ void named_sync(int id, int n) {
 
 struct Item {
   int gx0, gy0, zc0, zc1, s_begin, s_end;
+  int tx, ty, zc;  // tile column, tile row, z-chunk
 };
 
 // Tensor memory (TMEM) as a per-thread coefficient window (WIN = -1 configurations): a warp may
@@ -180,6 +181,9 @@ __device__ __forceinline__ Item decode(int item, int ntx, int nty, const KParams
     tx = t - ty * ntx;
   }
   Item it;
+  it.tx = tx;
+  it.ty = ty;
+  it.zc = zc;
   it.gx0 = R + tx * OXW - WOFF - R * H - dx;
   it.gy0 = ty * OY + R - R * H;
   it.zc0 = p.zo0 + zc * p.zchunk;

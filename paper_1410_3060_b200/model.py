@@ -98,20 +98,24 @@ def pipe_footprint(kind, bt, TX, TY, CX, CY, DV, DC, WIN, CLU=1):
                            "level_planes": 8 * NPL * 2 * TX * TY}}
 
 
-def pipe25_footprint(TX, TY, D, CLU):
-    """Footprint of pipe25.cu's two-level 25-point kernel pipe25_kernel<TX, TY, D, CLU> (P25Cfg)."""
+def pipe25_footprint(TX, TY, D, CLU, SKEW=0):
+    """Footprint of pipe25.cu's two-level 25-point kernel pipe25_kernel<K25V, TX, TY, D, CLU, SKEW> (P25Cfg).
+    SKEW: parallelogram tiles in y -- level 2 runs R rows below level 1, box C reaches R
+    rows lower, box I brings 2R level-1 rows from the tile underneath; output rows = TY."""
     R, NC = 4, 13
     NCONS = (TX // 2) * (TY // 2)
+    CR, IEL = (R, 2 * R * TX) if SKEW else (0, 0)
     AEL, BEL = TX * TY, (TX + 2 * R) * (TY + 2 * R)
-    SLOT = _ceil16(AEL) + _ceil16(BEL) + _ceil16(NC * TX * TY)
+    SLOT = _ceil16(AEL) + _ceil16(BEL) + _ceil16(NC * TX * (TY + CR)) + _ceil16(IEL)
     NRX = 4 if CLU > 1 else 0
     STASH = 2 * 32 * 4 * 5 if CLU > 1 else 0
-    smem = 8 * (D * SLOT + 3 * TX * TY + 2 * NRX * R * TX + STASH) + 8 * (2 * D + 8 + 2 * NRX + 8) + 4 * 8 + 128
-    OX, OYP = TX - 2 * R, CLU * TY - 2 * R
+    NPB = 2 if SKEW else 3
+    smem = 8 * (D * SLOT + NPB * TX * TY + 2 * NRX * R * TX + STASH) + 8 * (2 * D + 8 + 2 * NRX + 8) + 4 * 8 + 128
+    OX, OYP = TX - 2 * R, (TY if SKEW else CLU * TY - 2 * R)
     work = (TX * CLU * TY + OX * OYP) / (2 * OX * OYP)  # level 1 over every CTA's rows, level 2 = output
     return {"smem": smem, "tmem_cols": 512, "threads": NCONS + 32, "out_tile": (OX, OYP), "level_work": work,
             "level1_ratio": TX * CLU * TY / (OX * OYP),
-            "fits": smem <= SMEM_LIMIT, "coef_box_bytes_per_output": 8 * NC * TX * TY * CLU / (OX * OYP),
+            "fits": smem <= SMEM_LIMIT, "coef_box_bytes_per_output": 8 * NC * TX * (TY + CR) * CLU / (OX * OYP),
             "ring_bytes": {"slot": 8 * SLOT, "slots": D}}
 
 
@@ -213,7 +217,7 @@ def pipe_plans():
 
 
 def pipe25_plans():
-    """[(tile_cfg, TX, TY, D, CLU)] of pipe25.cu's launch_pipe25v2 table (the default entry is cfg 0)."""
+    """[(tile_cfg, TX, TY, D, CLU, SKEW)] of pipe25.cu's launch_pipe25v2 table (the default entry is cfg 0)."""
     import re
     src = open(__import__("os").path.join(_CSRC, "pipe25.cu")).read()
     body = src[src.index("cudaError_t launch_pipe25v2("):]

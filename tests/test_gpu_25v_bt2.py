@@ -17,8 +17,9 @@ SHAPES = [(130, 37, 41), (24, 16, 9), (25, 17, 13), (71, 50, 30), (1, 1, 1), (3,
           (48, 150, 12)]
 
 
-# tile_cfg: 0 = single CTA (24 x 16 output tiles), 1 = cluster pair (24 x 32), 2 = cluster of 4 (24 x 72)
-CFGS = (0, 1, 2)
+# tile_cfg: 0 = single CTA (24 x 16 output tiles), 1 = cluster pair (24 x 32), 2 = cluster of 4 (24 x 72),
+# 3 = skewed single-CTA tiles (24 x 20, level-1 rows handed to the tile above through global memory)
+CFGS = (0, 1, 2, 3)
 
 
 @pytest.mark.parametrize("shape", SHAPES)
@@ -56,12 +57,13 @@ def test_bt2_consecutive_runs_and_odd_T():
         assert np.array_equal(g.read(0), ref[0])
 
 
+@pytest.mark.parametrize("cfg", [0, 3])
 @pytest.mark.parametrize("halo", [st.ST_HALO_COPY, st.ST_HALO_PEER])
 @pytest.mark.parametrize("P", [2, 3])
-def test_bt2_loopback_slabs(halo, P):
+def test_bt2_loopback_slabs(halo, P, cfg):
     nx, ny, nz = 70, 33, 40
     ref = gpu_run(K, nx, ny, nz, 6, seed=6, variant=st.ST_VARIANT_NAIVE)
-    with st.Grid(K, nx, ny, nz, seed=6, bt=2, nranks=P, local_slabs=P, halo=halo) as g:
+    with st.Grid(K, nx, ny, nz, seed=6, bt=2, nranks=P, local_slabs=P, halo=halo, tile_cfg=cfg, tuned=False) as g:
         g.run(6)
         assert g.info()["bt"] == 2
         assert np.array_equal(g.read(0), ref[0])

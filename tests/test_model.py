@@ -77,10 +77,11 @@ def test_every_configured_plan_fits_on_chip():
         if p["WIN"] < 0:  # TMEM-window plans also keep a second CTA off the SM (pipe.cu static_assert)
             assert f["smem"] > 116 * 1024 and f["tmem_cols"] <= 512, (p, f)
     p25 = _plans25()
-    assert len(p25) == 3
-    for TX, TY, D, CLU in p25:
-        f = m.pipe25_footprint(TX, TY, D, CLU)
+    assert len(p25) == 4
+    for TX, TY, D, CLU, SKEW in p25:
+        f = m.pipe25_footprint(TX, TY, D, CLU, SKEW)
         assert f["fits"] and f["out_tile"][0] == TX - 8, f
+        assert f["out_tile"][1] == (TY if SKEW else CLU * TY - 8), f
 
 
 def test_footprint_rules_out_what_the_design_says():

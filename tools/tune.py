@@ -40,8 +40,8 @@ def candidates(kind):
         if f["fits"]:
             out.append((model.modeled_nj_per_lup(kind, bt, f), bt, cfg, f))
     if kind == model.K25V:
-        for cfg, TX, TY, D, CLU in model.pipe25_plans():
-            f = model.pipe25_footprint(TX, TY, D, CLU)
+        for cfg, TX, TY, D, CLU, SKEW in model.pipe25_plans():
+            f = model.pipe25_footprint(TX, TY, D, CLU, SKEW)
             if f["fits"]:
                 out.append((model.modeled_nj_per_lup(kind, 2, f), 2, cfg, f))
     return sorted(out, key=lambda c: c[0])
