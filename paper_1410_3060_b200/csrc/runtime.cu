@@ -732,7 +732,7 @@ int skew_params(stencil_ctx* h, Slab& s, st::KParams& p) {
     CK(cudaMemsetAsync(h->xflag, 0, (size_t)need * sizeof(unsigned int), h->stream), "zero skewed-tile flags");
   }
   h->xbase += 65536u;
-  if (h->xbase == 0) {  // wrapped: no flag may look newer than the next launch's base
+  if (h->xbase >= 0x80000000u) {  // flags are compared as (int)(v - want): restart before that wraps
     CK(cudaMemsetAsync(h->xflag, 0, (size_t)h->xflag_n * sizeof(unsigned int), h->stream), "zero skewed-tile flags");
     h->xbase = 65536u;
   }
