@@ -515,6 +515,9 @@ __global__ void __launch_bounds__(P25Cfg<KIND, TX, TY, D, CLU, SKEW>::THREADS, 1
               if (gx >= 0 && gx < p.nx + 2 * R) dx[i] = v1[j][i];
             }
           }
+          // every lane orders its own stores before the warp's release (a release by lane 0 after
+          // __syncwarp alone let the importer's TMA read stale rows: measured, tools/dbg_skew.py)
+          __threadfence();
           __syncwarp();
           if (lane == 0) {
             asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p.xflag + fme + (warp - C::XROW0 / C::WROWS)),
