@@ -289,7 +289,9 @@ __global__ void __launch_bounds__(P25Cfg<KIND, TX, TY, D, CLU, SKEW>::THREADS, 1
           const bool needB = q >= it.s_begin;
           const bool need1 = needB && (it.s_begin == 0 || q >= it.s_begin + R);
           // SKEW: level 1's rows -2R..-1 of plane q, from the tile underneath (or the ghost rows, bottom tile)
-          const bool needI = SKEW && needB && q >= 0 && q < p.zl;
+          // (only planes whose level 1 is real: adjacent z-chunks write the same exchange planes, and a
+          // chunk's fill planes hold its input instead)
+          const bool needI = SKEW && need1 && q >= 0 && q < p.zl;
           mbar_expect_tx(&full[sl], C::TX_BYTES_A + (needB ? C::TX_BYTES_B : 0u) + (need1 ? C::TX_BYTES_C : 0u) +
                                         (needI ? C::TX_BYTES_I : 0u));
           double* slot = ring + (size_t)sl * C::SLOT;
@@ -502,8 +504,9 @@ __global__ void __launch_bounds__(P25Cfg<KIND, TX, TY, D, CLU, SKEW>::THREADS, 1
       for (int j = 0; j < CY; ++j) sts_row<CX, true>(P + (ly0 + j) * TX + x0, v1[j]);
       if constexpr (SKEW) {
         // hand the top 2R level-1 rows of plane q to the tile above (plain stores: they should stay in L2
-        // for its import a few steps later), then release them warp by warp
-        if (exporter && q >= it.s_begin && q >= 0 && q < p.zl) {
+        // for its import a few steps later), then release them warp by warp -- only planes whose level 1
+        // is computed (not a z-chunk's fill planes: the neighbouring chunk writes the same exchange plane)
+        if (exporter && q >= it.s_begin && (it.s_begin == 0 || q >= it.s_begin + R) && q >= 0 && q < p.zl) {
 #pragma unroll
           for (int j = 0; j < CY; ++j) {
             const int gy = it.gy0 + ly0 + j;
