@@ -69,6 +69,7 @@ struct KParams {
   unsigned int* xflag;
   long long xflag_n;
   unsigned int xbase;
+  int xg;  // skewed tiles: exported planes are released every xg steps (launcher; STENCIL_XG)
   int walign;  // pipe kernel: tiles write sector-aligned output segments (STENCIL_WALIGN=1; default 0:
                // measured slower under the power cap for OX % 4 != 0, profiles/r01_summary.md)
 };

@@ -427,9 +427,24 @@ __global__ void __launch_bounds__(P25Cfg<KIND, TX, TY, D, CLU, SKEW>::THREADS, 1
       }
     }
 
+    unsigned int xpend = 0;  // SKEW exporters: planes stored but not yet released (+1)
     for (int s = it.s_begin; s <= it.s_end; ++s, ++iv) {
       const uint32_t sl = iv % D;
       const double* slot = ring + (size_t)sl * C::SLOT;
+      if constexpr (SKEW) {
+        // release the exported planes every xg steps, at the start of a step: by now the stores of the
+        // last step have long completed, so the fence costs little (every lane fences its own stores,
+        // then lane 0 publishes the warp's flag)
+        if (exporter && xpend && (int)(xpend % (unsigned int)p.xg) == 0) {
+          __threadfence();
+          __syncwarp();
+          if (lane == 0)
+            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p.xflag + fme + (warp - C::XROW0 / C::WROWS)),
+                         "r"(p.xbase + xpend)
+                         : "memory");
+          xpend = 0;
+        }
+      }
       mbar_wait(&full[sl], (iv / D) & 1);
 
       // ---------------- level 1: plane q = s - R over the level-1 extent (all consumer warps)
@@ -518,15 +533,7 @@ __global__ void __launch_bounds__(P25Cfg<KIND, TX, TY, D, CLU, SKEW>::THREADS, 1
               if (gx >= 0 && gx < p.nx + 2 * R) dx[i] = v1[j][i];
             }
           }
-          // every lane orders its own stores before the warp's release (a release by lane 0 after
-          // __syncwarp alone let the importer's TMA read stale rows: measured, tools/dbg_skew.py)
-          __threadfence();
-          __syncwarp();
-          if (lane == 0) {
-            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p.xflag + fme + (warp - C::XROW0 / C::WROWS)),
-                         "r"(p.xbase + (unsigned int)q + 1u)
-                         : "memory");
-          }
+          xpend = (unsigned int)q + 1u;  // released at the start of a later step (below), off this step's path
         }
       }
       if constexpr (CLU > 1) {
@@ -786,6 +793,17 @@ __global__ void __launch_bounds__(P25Cfg<KIND, TX, TY, D, CLU, SKEW>::THREADS, 1
       if (lane == 0) mbar_arrive(&empty[sl]);
     }
 
+    if constexpr (SKEW) {
+      if (exporter && xpend) {  // the item's last exported planes
+        __threadfence();
+        __syncwarp();
+        if (lane == 0)
+          asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p.xflag + fme + (warp - C::XROW0 / C::WROWS)),
+                       "r"(p.xbase + xpend)
+                       : "memory");
+      }
+    }
+
     // Fused halo exchange (ST_HALO_PEER; pipe.cu): the item's output planes that are a z-neighbour's halo
     // go straight into the neighbour's buffer once the item is done (each thread forwards its own stores).
     if (lvl2) {
@@ -908,6 +926,8 @@ cudaError_t run_pipe25(const KParams& p0, int zchunk_req, int num_sms, cudaStrea
   p.skew_ns = skew_env;
   static const int l2h_env = getenv("STENCIL_L2H") ? atoi(getenv("STENCIL_L2H")) : 0;
   p.l2h = l2h_env;
+  static const int xg_env = getenv("STENCIL_XG") ? atoi(getenv("STENCIL_XG")) : 1;
+  p.xg = std::max(1, xg_env);
   // lockstep rounds over compact patches of tiles (STENCIL_SCHED=0: dynamic, row-major); a round is one
   // item per cluster (one CTA per SM), the patch about square in cells
   static const int sched_env = getenv("STENCIL_SCHED") ? atoi(getenv("STENCIL_SCHED")) : 1;
