@@ -297,7 +297,7 @@ __global__ void __launch_bounds__(P25Cfg<KIND, TX, TY, D, CLU, SKEW>::THREADS, 1
           double* slot = ring + (size_t)sl * C::SLOT;
           if constexpr (SKEW) {
             if (needI) {
-              if (it.ty > 0) {
+              if (it.ty > 0 && !(p.dbg & 64)) {  // (STENCIL_DBG bit 64, experiment: no wait, wrong results)
                 // wait until both exporting warps of the tile underneath stored plane q (bounded: a lost
                 // producer makes wrong planes, not a hung GPU)
                 const unsigned int want = p.xbase + (unsigned int)q + 1u;
@@ -436,7 +436,7 @@ __global__ void __launch_bounds__(P25Cfg<KIND, TX, TY, D, CLU, SKEW>::THREADS, 1
         // last step have long completed, so the fence costs little (every lane fences its own stores,
         // then lane 0 publishes the warp's flag)
         if (exporter && xpend && (int)(xpend % (unsigned int)p.xg) == 0) {
-          __threadfence();
+          if (!(p.dbg & 128)) __threadfence();  // (STENCIL_DBG bit 128, experiment: no fence)
           __syncwarp();
           if (lane == 0)
             asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p.xflag + fme + (warp - C::XROW0 / C::WROWS)),
