@@ -123,7 +123,10 @@ typedef struct {
   int bt;              /* time-block depth (levels fused per launch); 0 = auto; >= 1 otherwise */
   int tile_cfg;        /* kernel tile configuration index of the variant (0 = default; an index the
                           pipe / stream variants do not define selects the default; ST_VARIANT_COOP
-                          accepts 0, 1 and, for the 7-point Jacobi kinds, 2 -- else ST_E_INVAL) */
+                          accepts 0, 1 and, for the 7-point Jacobi kinds, 2 -- else ST_E_INVAL).
+                          25-point variable at bt = 2 (pipe25.cu): 0 = 32x24 overlapped tile, 1 / 2 =
+                          cluster pair / quad, 3 = skewed tiles (non-redundant in y; the library then
+                          allocates one more state-sized exchange buffer per slab) */
   int local_slabs;     /* z-slabs held by this handle: 1 (one slab per process and GPU; neighbours
                           exchange halos with NCCL), or nranks with rank = 0 ("loopback": all slabs
                           on this handle's device, halos exchanged by device copies -- the multi-GPU
