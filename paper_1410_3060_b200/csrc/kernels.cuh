@@ -58,7 +58,6 @@ struct KParams {
   int tblk_w, tblk_h;  // tile order in blocks of tblk_w x tblk_h tiles (0 = row-major; set by launchers)
   int lockstep;        // pipe kernels: static round-robin items, CTAs start each round together (launcher)
   int pfd;             // pipe25: TMA L2-prefetch distance in steps (launcher; STENCIL_PF)
-  int skew_ns;         // pipe25 experiment (STENCIL_SKEW_NS): checkerboard-odd tiles start an item later
   int l2h;             // pipe25 experiment (STENCIL_L2H): L2 priorities of boxes A/B/C, 2 bits each
                        // (0 = no hint, 1 = evict_first, 2 = evict_last, 3 = evict_normal)
   // pipe25 skewed tiles (SKEW): the level-1 rows a tile hands to the tile above go through

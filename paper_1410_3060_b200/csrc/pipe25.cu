@@ -275,9 +275,6 @@ __global__ void __launch_bounds__(P25Cfg<KIND, TX, TY, D, CLU, SKEW>::THREADS, 1
             asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p.xflag + fme + 1), "r"(p.xbase + 0xFFFFu) : "memory");
           }
         }
-        if (p.skew_ns > 0 && (((it.gx0 / C::OX) + (it.gy0 / C::OYP)) & 1)) {  // experiment: offset neighbours
-          for (int w = 0; w < p.skew_ns; w += 1000) __nanosleep(1000);
-        }
         const int xb = ((it.gx0 - R + p.xoff) & ~1) - (p.xoff & ~1);  // box B (footprint)
         const int xa = ((it.gx0 + p.xoff) & ~1) - (p.xoff & ~1);      // boxes A, C (level-1 extent)
         for (int s = it.s_begin; s <= it.s_end && !skip; ++s, ++iv) {
@@ -922,8 +919,6 @@ cudaError_t run_pipe25(const KParams& p0, int zchunk_req, int num_sms, cudaStrea
   const int grid = (int)std::min<long long>(items, clusters) * CLU;
   static const int pfd_env = getenv("STENCIL_PF") ? atoi(getenv("STENCIL_PF")) : 0;
   p.pfd = pfd_env;  // L2 prefetch distance in steps (0 = none)
-  static const int skew_env = getenv("STENCIL_SKEW_NS") ? atoi(getenv("STENCIL_SKEW_NS")) : 0;
-  p.skew_ns = skew_env;
   static const int l2h_env = getenv("STENCIL_L2H") ? atoi(getenv("STENCIL_L2H")) : 0;
   p.l2h = l2h_env;
   static const int xg_env = getenv("STENCIL_XG") ? atoi(getenv("STENCIL_XG")) : 1;
