@@ -432,7 +432,7 @@ __global__ void __launch_bounds__(P25Cfg<KIND, TX, TY, D, CLU, SKEW>::THREADS, 1
         // release the exported planes every xg steps, at the start of a step: by now the stores of the
         // last step have long completed, so the fence costs little (every lane fences its own stores,
         // then lane 0 publishes the warp's flag)
-        if (exporter && xpend && (int)(xpend % (unsigned int)p.xg) == 0) {
+        if (exporter && xpend && (int)(xpend % (unsigned int)p.xg) == 0 && !(p.dbg & 256)) {
           if (!(p.dbg & 128)) __threadfence();  // (STENCIL_DBG bit 128, experiment: no fence)
           __syncwarp();
           if (lane == 0)
