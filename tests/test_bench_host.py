@@ -85,3 +85,15 @@ def test_gpus_2_spawns_two_ranks():
     assert r.returncode == 0, r.stderr[-2000:]
     lines = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
     assert len(lines) == 1 and lines[0]["world"] == 2 and sorted(lines[0]["ranks"]) == [0, 1]
+
+
+def test_modeled_dram_reports_the_round_model_for_pipe_plans_only():
+    # bench.py's roofline carries model.lockstep_dram_bytes_per_lup for the plan that ran (next to ncu's
+    # measured bytes); the cooperative and naive plans have no lockstep rounds
+    import paper_1410_3060_b200 as st
+    from paper_1410_3060_b200 import model
+    info = {"variant": st.ST_VARIANT_PIPE, "bt": 2, "tile_x": 24, "tile_y": 16}
+    got = bench.modeled_dram(st, workloads.C4, info)
+    assert got == round(model.lockstep_dram_bytes_per_lup(model.K25V, 2, (512, 512, 512), (24, 16)), 2)
+    assert 60.0 < got < 75.0
+    assert bench.modeled_dram(st, workloads.C4, dict(info, variant=st.ST_VARIANT_COOP)) is None
