@@ -80,7 +80,7 @@ enum {
   ST_VARIANT_PIPE = 3,   /* the same wavefront with TMA-fed shared-memory rings: a producer warp
                             streams planes and coefficient fields ahead with cp.async.bulk.tensor +
                             mbarriers; persistent CTAs.  The default.  bt per kind:
-                            7c <= 8, 7v <= 4, the 25-point kinds <= 2 (two fused levels of the
+                            7c <= 8, 7v <= 5, the 25-point kinds <= 2 (two fused levels of the
                             25-point stencils run the two-level kernel of DESIGN.md §5b, whose
                             z-chains are carried in tensor memory), the alpha-field wave 1.  Library
                             defaults: 7c 4, 7v 4, 25v 2, the waves 1 (the Python binding applies

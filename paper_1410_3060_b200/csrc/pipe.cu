@@ -838,7 +838,7 @@ cudaError_t run_pipe(const KParams& p0, int zchunk_req, int num_sms, cudaStream_
 int max_pipe_bt(int kind) {
   switch (kind) {
     case K7C: return 8;
-    case K7V: return 4;
+    case K7V: return 5;
     case K25W: return 2;
     case K25WA: return 1;
     case K25V: return 2;  // bt = 2: pipe25.cu
@@ -909,6 +909,9 @@ cudaError_t launch_pipe(int kind, int b, const KParams& p, int zchunk_req, int n
           if (cfg == 4) CFGC(K7V, 4, 32, 28, 2, 2, 4, 2, -1, 1);  // cluster pair: 32 x 56 tile
           // 7 consumer warps, 2-slot coefficient ring (lookahead 1): 199 -> 202 GLUP/s (session 3)
           CFGU(K7V, 4, 32, 28, 2, 2, 4, 2, -1, 1);
+        case 5:  // TMEM window of 5 slots: 2x1 cells so that 3 warps per lane quadrant fit 480 columns
+          if (cfg == 1) CFG(K7V, 5, 32, 24, 2, 1, 4, 2, -1, 1);
+          CFGU(K7V, 5, 32, 24, 2, 1, 4, 2, -1, 1);
       }
       break;
     case K25W:

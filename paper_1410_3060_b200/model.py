@@ -89,11 +89,21 @@ def pipe_footprint(kind, bt, TX, TY, CX, CY, DV, DC, WIN, CLU=1):
         NSL = (bt - 1) * R + 1
         WPQ = (NCONS // 32 + 3) // 4
         tmem = WPQ * NSL * CY * 32
+    # the ring-depth and window rules of PipeCfg's static_asserts: the V ring holds the R + 2 planes a
+    # step reads, the coefficient ring keeps a plane CLAG = (bt - 1 - WIN) * R steps after level 1 (0 for
+    # the wave and the TMEM window), a TMEM window slot holds a cell row's NC * CX coefficients
+    TW = WIN < 0
+    CLAG = 0 if (wave or TW) else (bt - 1 - WIN) * R
+    # a register window (WIN = k > 0) keeps k*R coefficient planes of the thread's cells in registers:
+    # at most 32 doubles (64 of the 255 registers; the configured windows use 28)
+    REGWIN = max(WIN, 0) * R * NC * CX * CY
+    valid = (DV >= R + 2 and (NCF == 0 or DC >= CLAG + 2) and -1 <= WIN <= bt - 1 and (WIN == 0 or NC > 0)
+             and (not TW or (not wave and bt >= 2 and 2 * NC * CX <= 32)) and REGWIN <= 32 and OX > 0 and OYP > 0)
     # level-k extent (TX - 2R(k-1)) x (CLU*TY - 2R(k-1)): a cluster pair shrinks only at its outer rows
     work = sum((TX - 2 * R * (k - 1)) * (CLU * TY - 2 * R * (k - 1)) for k in range(1, bt + 1))
     return {"smem": smem, "tmem_cols": tmem, "threads": NCONS + 32, "out_tile": (OX, OYP),
             "level_work": work / (bt * OX * OYP), "level1_ratio": TX * CLU * TY / (OX * OYP),
-            "fits": smem <= SMEM_LIMIT and tmem <= TMEM_COLUMNS,
+            "fits": valid and smem <= SMEM_LIMIT and tmem <= TMEM_COLUMNS, "valid": valid,
             "ring_bytes": {"state": 8 * DV * VSLOT, "coef": 8 * DC * CSLOT if NCF > 0 else 0,
                            "level_planes": 8 * NPL * 2 * TX * TY}}
 

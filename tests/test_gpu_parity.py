@@ -21,7 +21,7 @@ SHAPES = {synth.K7C: (61, 70, 45), synth.K7V: (61, 70, 45), synth.K25W: (130, 37
 def max_bt(kind, variant=st.ST_VARIANT_PIPE):
     if variant == st.ST_VARIANT_STREAM:
         return {synth.K7C: 6, synth.K7V: 4, synth.K25W: 1, synth.K25V: 1, synth.K25WA: 1}[kind]
-    return {synth.K7C: 8, synth.K7V: 4, synth.K25W: 2, synth.K25V: 2, synth.K25WA: 1}[kind]
+    return {synth.K7C: 8, synth.K7V: 5, synth.K25W: 2, synth.K25V: 2, synth.K25WA: 1}[kind]
 
 
 N_CFG = {synth.K7C: 1, synth.K7V: 10, synth.K25W: 9, synth.K25V: 4, synth.K25WA: 5}  # pipe tile configurations

@@ -18,7 +18,7 @@ import paper_1410_3060_b200 as st  # noqa: E402
 import synth  # noqa: E402
 
 N_CFG = {synth.K7C: 1, synth.K7V: 10, synth.K25W: 9, synth.K25V: 4, synth.K25WA: 5}
-MAX_BT = {synth.K7C: 8, synth.K7V: 4, synth.K25W: 2, synth.K25V: 2, synth.K25WA: 1}
+MAX_BT = {synth.K7C: 8, synth.K7V: 5, synth.K25W: 2, synth.K25V: 2, synth.K25WA: 1}
 
 
 def run(kind, n, T, seed, **kw):
