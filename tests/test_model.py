@@ -142,3 +142,17 @@ def test_lockstep_dram_model_reproduces_ncu():
         mod = m.lockstep_dram_bytes_per_lup(kind, bt, (n, n, n), tile)
         assert abs(mod - meas) / meas < tol, (key, mod, meas)
         assert mod > m.code_balance(kind, bt)
+
+
+def test_footprint_rules_for_deeper_7v_blocks():
+    # PipeCfg's static_asserts as model rules: a 5-level TMEM window of 2x2-cell warps needs 640 columns;
+    # a shared-memory coefficient ring keeps each plane (bt - 1 - WIN) * R steps and needs that + 2 slots;
+    # a register window is capped at 32 doubles per thread
+    f = m.pipe_footprint(m.K7V, 5, 32, 28, 2, 2, 4, 2, -1)
+    assert f["tmem_cols"] == 640 and not f["fits"]
+    assert not m.pipe_footprint(m.K7V, 5, 32, 20, 2, 2, 4, 2, 0)["valid"]   # CLAG 4 needs DC >= 6
+    assert m.pipe_footprint(m.K7V, 5, 32, 20, 2, 2, 4, 6, 0)["valid"]
+    assert not m.pipe_footprint(m.K7V, 5, 32, 20, 2, 2, 4, 4, 2)["valid"]   # 2 planes x 7 x 4 cells = 56
+    # the b_t = 5 plan pipe.cu instantiates: 2x1 cells, 3 warps per lane quadrant, 480 columns
+    f = m.pipe_footprint(m.K7V, 5, 32, 24, 2, 1, 4, 2, -1)
+    assert f["fits"] and f["tmem_cols"] == 480 and f["out_tile"] == (24, 16)
