@@ -160,6 +160,24 @@ def load_fp64_peak():
         return 37.2, "nominal (64 FP64 FMA lanes per SM x 148 SMs x 1.965 GHz)"
 
 
+def energy_split(energy_nj, glups_per_gpu, dram_bytes_per_lup):
+    """Board energy per update split with round 1's probe (profiles/r01_energy_probe.json, tools/
+    energy_probe.py): idle power / rate, DRAM bytes x the streaming copy's incremental pJ per byte, the rest
+    (SM, L2, shared memory, TMEM at the plan's clock).  None without the probe file or the ncu bytes."""
+    try:
+        probe = {}
+        for line in open(os.path.join(ROOT, "profiles", "r01_energy_probe.json")):
+            if line.strip():
+                d = json.loads(line)
+                probe[d["case"]] = d
+        idle = probe["idle"]["power_w"] / glups_per_gpu
+        dram = dram_bytes_per_lup * probe["hbm_copy"]["pj_per_unit"] / 1e3
+    except Exception:
+        return None
+    return {"idle_nj": round(idle, 2), "dram_nj": round(dram, 2), "rest_nj": round(energy_nj - idle - dram, 2),
+            "source": "profiles/r01_energy_probe.json (idle W, HBM copy pJ/B) and the ncu DRAM bytes per update"}
+
+
 def pick_workload(name, n_gpus, scaling="weak"):
     """The workload of an N-GPU run.  weak: per-GPU work fixed (the global nz grows with N; C5 uses
     BASELINE.json's weak variant 1024 x 1024 x 256N); strong: the configuration's global grid split over N."""
@@ -603,6 +621,9 @@ def main():
         roofline["observed_limiter"] = observed_limiter(clocks, roofline["bound"])
         if clocks.get("power_w"):  # board energy per lattice update on this GPU (cf. the paper's Table 1)
             clocks["energy_nj_per_lup"] = round(clocks["power_w"] / (value / world), 3)
+            if roofline.get("dram_bytes_per_lup"):
+                clocks["energy_split"] = energy_split(clocks["energy_nj_per_lup"], value / world,
+                                                      roofline["dram_bytes_per_lup"])
         line = {
             "metric": METRIC, "value": value, "unit": METRIC, "n_gpus": n, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,

@@ -97,3 +97,9 @@ def test_modeled_dram_reports_the_round_model_for_pipe_plans_only():
     assert got == round(model.lockstep_dram_bytes_per_lup(model.K25V, 2, (512, 512, 512), (24, 16)), 2)
     assert 60.0 < got < 75.0
     assert bench.modeled_dram(st, workloads.C4, dict(info, variant=st.ST_VARIANT_COOP)) is None
+
+
+def test_energy_split_adds_up():
+    e = bench.energy_split(16.98, 58.7, 70.31)
+    assert e is not None and abs(e["idle_nj"] + e["dram_nj"] + e["rest_nj"] - 16.98) < 0.02
+    assert 4.0 < e["idle_nj"] < 5.0 and 6.0 < e["dram_nj"] < 7.0
