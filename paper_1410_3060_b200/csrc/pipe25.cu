@@ -890,6 +890,10 @@ cudaError_t run_pipe25(const KParams& p0, int zchunk_req, int num_sms, cudaStrea
     if (tiles * ((planes + min_chunk - 1) / min_chunk) >= 2 * slots) {
       const long long chunks = std::max<long long>(1, (4 * slots + tiles - 1) / tiles);
       zchunk = std::max((int)((planes + chunks - 1) / chunks), std::min(planes, min_chunk));
+      // equal chunks (256 planes as 192 + 64 left the short chunks' CTAs idle: 25v 256^3 42.7 -> 48.2
+      // GLUP/s; profiles/r02_grid_size_sweep.md)
+      const int n = (planes + zchunk - 1) / zchunk;
+      zchunk = (planes + n - 1) / n;
     } else {
       zchunk = (int)std::max<long long>(2, (planes * tiles + slots - 1) / slots);
     }
